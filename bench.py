@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""RACE attention layer fwd+bwd throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the metric's config): causal RACE
+attention layer, B=1, H=4, d=dv=128, N=131072 tokens per GPU, bf16, sketch
+P=2, L=2, M=1, beta=8 (the reference defaults, ra/cli.py:71-76).  One step =
+forward + backward of the whole layer over synthetic Q, K, V, dO resident in
+HBM (512 MiB per step > 126 MB L2, so no L2 flush is needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU over NCCL: each rank owns an
+N-token slice of one N*world-token sequence (weak scaling); the bucket tables
+cross NVLink through the causal exclusive scan (sharded.py).
+
+--impl reference times the reference's CPU algorithm (the numpy port in
+oracle/, since the reference is pure Python and cannot travel to the box) on
+the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd tokens/s, RACE layer B=1 H=4 d=128; max context at 1/8 B200"
+HEADS, DIM, P_, L_, BETA = 4, 128, 2, 2, 8.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=131072, help="tokens per GPU")
+    ap.add_argument("--noncausal", action="store_true")
+    ap.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _config(args, world):
+    return {
+        "workload": f"{'non-causal' if args.noncausal else 'causal'} RACE attention layer fwd+bwd, "
+                    f"B=1 H={HEADS} d={DIM} N={args.n * world} ({args.n} per GPU), {args.dtype}",
+        "batch": 1, "heads": HEADS, "head_dim": DIM, "seq_len": args.n * world, "tokens_per_gpu": args.n,
+        "P": P_, "L": L_, "M": 1, "beta": BETA, "causal": not args.noncausal,
+        "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
+        "l2": "inputs (Q,K,V,dO = 4 x H*N*d) exceed the 126 MB L2; no flush needed",
+    }
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (numpy port) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_reference_step(n_sample, causal, seed=0):
+    import numpy as np
+
+    from oracle import race_oracle as ro
+
+    per_head = ro.head_inputs(seed, n_sample, DIM, HEADS, np.float32)
+    t0 = time.perf_counter()
+    for h, (q, k, v, g) in enumerate(per_head):
+        w = ro.stacked_hyperplanes(seed + h, P_, L_, 1, DIM)  # seed + h per head (ra/bench.py:175)
+        ro.forward(q, k, v, w, BETA, causal)
+        ro.vjp(q, k, v, w, BETA, g, causal)
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(blas) if blas else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    causal = not args.noncausal
+    n_sample = 4096 if causal else 16384
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt = cpu_reference_step(n_sample, causal, seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = n_sample * len(times) / tot
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) Q,K,V,dO (ra/bench.py:161-169 order)", "config": _config(args, world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{n_sample}-token {'causal' if causal else 'non-causal'} fwd+bwd, "
+                                   f"H={HEADS}, d={DIM}, f32, per step (oracle/race_oracle.py)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        self.thread.join(timeout=1)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our GPU path
+# ---------------------------------------------------------------------------
+# algorithmic bytes per token-head of each kernel (e = element bytes)
+def kernel_bytes(e, causal):
+    d = dv = DIM
+    if causal:
+        return {"kside_partials": (d + dv) * e,                          # read K, V
+                "fwd_causal": (2 * d + dv) * e + dv * e + 4,            # read Q, K, V; write O, den
+                "bwd_causal_q": (2 * d + 2 * dv) * e + d * e + 8,       # read Q, K, V, dO; write dQ, rden, gden
+                "bwd_causal_k": (2 * d + 2 * dv) * e + 8 + (d + dv) * e}  # read Q, K, V, dO, rden, gden; write dK, dV
+    return {"kside_partials": (d + dv) * e, "fwd_readout": d * e + dv * e + 4,
+            "bwd_qside": (d + dv) * e + d * e, "bwd_kside": 2 * (d + dv) * e}
+
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+
+    import paper_2510_04008_b200 as rb
+    from paper_2510_04008_b200 import _lib
+    from paper_2510_04008_b200.functional import Problem, _stream, _vp
+    from paper_2510_04008_b200.sharded import TorchDistComm, sharded_backward, sharded_forward
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    e = 2 if dtype == torch.bfloat16 else 4
+    causal = not args.noncausal
+    n = args.n
+    cfg = rb.SketchConfig(hyperplanes=P_, tables=L_, beta=BETA, seed=0, causal=causal)
+    w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
+    p = cfg.params()
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    shape = (1, HEADS, n, DIM)
+    q, k, v, g = (torch.randn(shape, generator=gen, device=dev, dtype=torch.float32).to(dtype) for _ in range(4))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    comm = TorchDistComm() if world > 1 else None
+
+    def step():
+        if world > 1:
+            o, den, st = sharded_forward(q, k, v, w, p, comm=comm)
+            return sharded_backward(q, k, v, w, g, p, st, comm=comm)
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        return rb.race_backward(q, k, v, w, g, p, state=st)
+
+    L = _lib.lib()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    c0 = L.race_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches = L.race_launch_count() - c0
+
+    graph = None
+    if world == 1 and not args.no_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+
+    def run():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
+    # settle clocks, then time exactly K steps
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    t_settle = time.perf_counter()
+    while time.perf_counter() - t_settle < 0.5:
+        run()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        run()
+    ev1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    tokens = n * world
+    value = tokens / (ms_step / 1e3)
+
+    # per-kernel breakdown (split-phase entries, events on the launching stream)
+    pr = Problem(q, k, v, w, p)
+    E = pr.table_elems
+    ws = pr.ws()
+    part = torch.empty((pr.bh, pr.nseg, E), device=dev)
+    tabs = torch.empty_like(part)
+    dpart = torch.empty_like(part)
+    dtabs = torch.empty_like(part)
+    o = torch.empty_like(v)
+    den = torch.empty((1, HEADS, n), device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    rden = torch.empty((pr.bh, n), device=dev)
+    gden = torch.empty_like(rden)
+    S = _stream()
+    ptr = _vp
+    if causal:
+        calls = [
+            ("kside_partials", lambda: L.race_kside_partials(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(part), ptr(ws), S)),
+            ("combine", lambda: L.race_combine(pr.dref, 1, ptr(part), None, ptr(tabs), S)),
+            ("fwd_causal", lambda: L.race_fwd_causal(pr.dref, ptr(q), ptr(k), ptr(v), ptr(pr.w), ptr(tabs), ptr(o),
+                                                     ptr(den), ptr(ws), S)),
+            ("bwd_causal_q", lambda: L.race_bwd_causal_q(pr.dref, ptr(q), ptr(k), ptr(v), ptr(g), ptr(pr.w), ptr(tabs),
+                                                         ptr(dq), ptr(rden), ptr(gden), ptr(dpart), ptr(ws), S)),
+            ("combine_d", lambda: L.race_combine(pr.dref, 2, ptr(dpart), None, ptr(dtabs), S)),
+            ("bwd_causal_k", lambda: L.race_bwd_causal_k(pr.dref, ptr(q), ptr(k), ptr(v), ptr(g), ptr(pr.w), ptr(rden),
+                                                         ptr(gden), ptr(dtabs), ptr(dk), ptr(dv), ptr(ws), S)),
+        ]
+    else:
+        calls = [
+            ("kside_partials", lambda: L.race_kside_partials(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(part), ptr(ws), S)),
+            ("combine", lambda: L.race_combine(pr.dref, 0, ptr(part), None, ptr(tabs), S)),
+            ("fwd_readout", lambda: L.race_fwd_readout(pr.dref, ptr(q), ptr(pr.w), ptr(tabs), ptr(o), ptr(den),
+                                                       ptr(ws), S)),
+            ("bwd_qside", lambda: L.race_bwd_qside(pr.dref, ptr(q), ptr(g), ptr(pr.w), ptr(tabs), ptr(dq), ptr(dpart),
+                                                   ptr(ws), S)),
+            ("combine_d", lambda: L.race_combine(pr.dref, 0, ptr(dpart), None, ptr(dtabs), S)),
+            ("bwd_kside", lambda: L.race_bwd_kside(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(dtabs), ptr(dk), ptr(dv),
+                                                   ptr(ws), S)),
+        ]
+    reps = 10
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(reps)]
+    for r in range(reps):
+        evs[r][0].record()
+        for i, (name, fn) in enumerate(calls):
+            _lib.check(fn(), name)
+            evs[r][i + 1].record()
+    torch.cuda.synchronize()
+    per = {name: statistics.median(evs[r][i].elapsed_time(evs[r][i + 1]) for r in range(reps))
+           for i, (name, _) in enumerate(calls)}
+    kb = kernel_bytes(e, causal)
+    dom = max(kb, key=lambda nm: per[nm])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    dom_bytes = kb[dom] * HEADS * n
+    achieved = dom_bytes / (per[dom] / 1e3) / 1e9
+    step_bytes = ((7 * DIM + 5 * DIM) * e + 8) * HEADS * n   # (7d+5dv)e+8 per token-head
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dom_bytes,
+                "kernel_ms": {k2: round(v2, 4) for k2, v2 in per.items()},
+                "step_algorithmic_GBps": step_bytes / (ms_step / 1e3) / 1e9,
+                "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak}
+
+    # e2e through the public module API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        layer = rb.RaceAttention(HEADS, DIM, cfg).to(dev)
+        hq, hk, hv, hg = (t.cpu().pin_memory() for t in (q, k, v, g))
+        outs = [torch.empty(shape, dtype=dtype).pin_memory() for _ in range(4)]
+
+        def e2e_step():
+            dq_, dk_, dv_ = (x.to(dev, non_blocking=True).requires_grad_(True) for x in (hq, hk, hv))
+            dg = hg.to(dev, non_blocking=True)
+            out = layer(dq_, dk_, dv_)
+            out.backward(dg)
+            for dst, src in zip(outs, (out.detach(), dq_.grad, dk_.grad, dv_.grad)):
+                dst.copy_(src, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        k_e2e = max(3, min(args.steps, 10))
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k_e2e):
+            e2e_step()
+        a1.record()
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1) / k_e2e
+        nb = q.numel() * e
+        e2e = {"value": n / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": 4 * nb,
+               "d2h_bytes_per_step": 4 * nb, "ms_per_step": ems,
+               "api": "RaceAttention (nn.Module) forward+backward, pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s = 8192 if causal else 32768
+        dt = cpu_reference_step(n_s, causal)
+        cpu = {"value": n_s / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{n_s}-token {'causal' if causal else 'non-causal'} fwd+bwd, H={HEADS}, d={DIM}, f32 "
+                         f"(oracle/race_oracle.py, the reference algorithm), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic N(0,1) Q,K,V,dO resident in HBM",
+            "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "cuda_graph": graph is not None, "clocks": clocks,
+            "fast_path": bool(_lib.fast_path(pr.desc)),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

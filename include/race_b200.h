@@ -1,0 +1,176 @@
+/*
+ * race_b200.h -- C ABI of the B200-native RACE attention hot path.
+ *
+ * The reference (arXiv 2510.04008, /root/reference/pkg/src/race_attention)
+ * is pure Python + numpy and has no FFI layer: its hot-path entry points are
+ *
+ *   race_attention(inp, cfg, workers)            ra/forward.py:147
+ *   race_attention_vjp(inp, cfg, d_out, workers) ra/backward.py:184
+ *   accumulate_num_den(q, k, v, cfg, workers)    ra/forward.py:124
+ *
+ * Each function below replaces one step of those (cited per entry).  The
+ * Python drop-in (paper_2510_04008_b200/api.py) binds them through ctypes;
+ * INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers, contiguous, row-major:
+ *       q, k, dq, dk : [BH, N, d]        v, o, d_o, dv : [BH, N, dv]
+ *       den          : [BH, N] float32   (the reference's averaged den)
+ *       w            : [H, T*P, d] float32 (w_per_head=1) or [T*P, d] (0);
+ *                      tables in the reference's (m, l) task order
+ *                      (ra/forward.py:128); head of row bh is bh % H.
+ *       tables       : [BH, F, dv+1] float32, F = T * 2^P, column dv is
+ *                      the normaliser ("ones") column:  S = phi(K)^T [V | 1].
+ *       seg tables   : [BH, nseg, F, dv+1] float32 (see race_segments).
+ *   - Input/output element type is desc->dtype (f32 or bf16); every
+ *     accumulation is fp32.
+ *   - No hidden allocation, no global mutable state; all launches go on the
+ *     caller's stream.  Scratch comes from a caller-provided workspace of
+ *     race_workspace_bytes() bytes.
+ *   - Return value: RACE_OK, or a RACE_E* code; race_last_error() gives text.
+ */
+#ifndef RACE_B200_H
+#define RACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RACE_ABI_VERSION 1
+
+enum race_status {
+  RACE_OK = 0,
+  RACE_EBADSHAPE = 1,    /* inconsistent / non-positive sizes            */
+  RACE_EUNSUPPORTED = 2, /* valid config the CUDA path does not support  */
+  RACE_ECUDA = 3,        /* a CUDA launch / runtime error                */
+};
+
+enum race_dtype { RACE_F32 = 0, RACE_BF16 = 1 };
+
+enum race_combine_mode {
+  RACE_COMBINE_TOTAL = 0,  /* out[bh]      = carry + sum_s part[bh][s]     */
+  RACE_COMBINE_PREFIX = 1, /* out[bh][s]   = carry + sum_{s'<s} part[bh][s'] */
+  RACE_COMBINE_SUFFIX = 2, /* out[bh][s]   = carry + sum_{s'>s} part[bh][s'] */
+};
+
+/* Problem descriptor; mirrors SketchConfig (ra/core.py:45-90) plus shapes. */
+typedef struct race_desc {
+  int32_t abi_version;  /* RACE_ABI_VERSION                                  */
+  int32_t dtype;        /* race_dtype of q, k, v, o, d_o, dq, dk, dv         */
+  int64_t batch_heads;  /* B*H                                               */
+  int64_t heads;        /* H                                                 */
+  int64_t n;            /* tokens of this (shard of the) sequence            */
+  int32_t dim;          /* d                                                 */
+  int32_t dim_v;        /* dv                                                */
+  int32_t hyperplanes;  /* P          (SketchConfig.hyperplanes)             */
+  int32_t tables;       /* T = M * L  (SketchConfig.total_tables)            */
+  float beta;           /* softmax temperature (SketchConfig.beta)           */
+  int32_t causal;       /* SketchConfig.causal                               */
+  int32_t normalize;    /* SketchConfig.normalize_inputs                     */
+  int32_t w_per_head;   /* 1: w is [H, T*P, d]; 0: [T*P, d]                  */
+  int32_t reserved[4];  /* must be zero                                      */
+} race_desc_t;
+
+int race_abi_version(void);
+const char* race_last_error(void);
+
+/* Number of kernels this library has launched in this process (diagnostic;
+ * bench.py reports launches per step from it).                            */
+int64_t race_launch_count(void);
+
+/* 0 = generic SIMT kernels, 1 = sm_100a tcgen05/TMA fast path for this desc. */
+int race_fast_path(const race_desc_t* desc);
+
+/* Sequence segmentation shared by every kernel: tokens are cut into nseg
+ * contiguous segments of seg_tokens (a multiple of 128) per (b, h).  The
+ * causal carries and all per-segment partial tables use this split.       */
+int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens);
+
+/* Scratch bytes needed by any entry point below for this desc.           */
+int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
+
+/* Elements (float32) of the state race_fwd saves for race_bwd:
+ * non-causal: tables [BH, F, dv+1];  causal: carries [BH, nseg, F, dv+1]. */
+int race_state_elems(const race_desc_t* desc, int64_t* elems);
+
+/* ---- monolithic single-device entry points ---------------------------- */
+
+/* Forward: o = num / den, den = averaged denominator (ra/forward.py:147-164,
+ * accumulate_num_den ra/forward.py:124-144).  Rows whose averaged den is
+ * <= 1e-30 are written as zeros (ra/forward.py:157-163); the host derives
+ * degenerate_rows from den.  `state` (may be NULL) receives what race_bwd
+ * needs (race_state_elems floats).                                        */
+int race_fwd(const race_desc_t* desc, const void* q, const void* k,
+             const void* v, const float* w, void* o, float* den,
+             float* state, void* workspace, void* stream);
+
+/* Backward (ra/backward.py:184-235).  If state is NULL it is recomputed
+ * from k, v exactly as race_fwd would (the reference recomputes too,
+ * ra/backward.py:200).                                                    */
+int race_bwd(const race_desc_t* desc, const void* q, const void* k,
+             const void* v, const float* w, const void* d_o,
+             const float* state, void* dq, void* dk, void* dv,
+             void* workspace, void* stream);
+
+/* ---- split-phase entry points (sequence sharding across GPUs) --------- */
+
+/* Key-side aggregation per segment: part[bh][s] = phi(K_s)^T [V_s | 1]
+ * (ra/forward.py:84-87 per table; concatenated over tables).             */
+int race_kside_partials(const race_desc_t* desc, const void* k, const void* v,
+                        const float* w, float* part, void* workspace,
+                        void* stream);
+
+/* Fixed-order (deterministic) reduction of per-segment tables; carry may
+ * be NULL (= 0) and is [BH, F, dv+1].  out is [BH, F, dv+1] for TOTAL and
+ * [BH, nseg, F, dv+1] for PREFIX / SUFFIX.                                */
+int race_combine(const race_desc_t* desc, int32_t mode, const float* part,
+                 const float* carry, float* out, void* stream);
+
+/* Non-causal query-side readout with global tables (ra/forward.py:93-96,
+ * 157-163).                                                               */
+int race_fwd_readout(const race_desc_t* desc, const void* q, const float* w,
+                     const float* tables, void* o, float* den,
+                     void* workspace, void* stream);
+
+/* Causal chunked scan given per-segment carry-in tables
+ * (ra/forward.py:100-121).                                                */
+int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k,
+                    const void* v, const float* w, const float* carries,
+                    void* o, float* den, void* workspace, void* stream);
+
+/* Non-causal backward, query side: dq and per-segment partial dS
+ * (ra/backward.py:109-118 + the d_num/d_den prologue 201-209).           */
+int race_bwd_qside(const race_desc_t* desc, const void* q, const void* d_o,
+                   const float* w, const float* tables, void* dq,
+                   float* dpart, void* workspace, void* stream);
+
+/* Non-causal backward, key side given global dS (ra/backward.py:122-128). */
+int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v,
+                   const float* w, const float* dtables, void* dk, void* dv,
+                   void* workspace, void* stream);
+
+/* Causal backward, forward-direction scan: dq, per-token normaliser terms
+ * rden = 1/(T*den), gden = -(dO.O)/(T*den), and per-segment dS totals
+ * (ra/backward.py:142-168).                                               */
+int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k,
+                      const void* v, const void* d_o, const float* w,
+                      const float* carries, void* dq, float* rden,
+                      float* gden, float* dpart, void* workspace,
+                      void* stream);
+
+/* Causal backward, reverse-direction scan given per-segment suffix dS
+ * (ra/backward.py:169-180).                                               */
+int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k,
+                      const void* v, const void* d_o, const float* w,
+                      const float* rden, const float* gden,
+                      const float* dcarries, void* dk, void* dv,
+                      void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RACE_B200_H */

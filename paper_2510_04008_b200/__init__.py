@@ -1,0 +1,45 @@
+"""B200-native RACE attention (arXiv 2510.04008): forward + backward, causal and
+non-causal, as hand-written sm_100a CUDA behind the reference package's API.
+
+Drop-in names (same meaning as ``race_attention`` in the reference):
+``SketchConfig, AttnInputs, RaceOutput, RaceGradients, race_attention,
+race_attention_vjp, accumulate_num_den, table_hyperplanes, derive_table_rng,
+gaussian_matrix``.  Device-level: ``race_forward``, ``race_backward``,
+``RaceAttentionFunction``, ``RaceAttention`` (nn.Module), and the
+sequence-sharded ``sharded_forward`` / ``sharded_backward``.
+"""
+
+from .attention import (
+    DEGENERATE_DEN_EPS,
+    ZERO_ROW_EPS,
+    AttnInputs,
+    RaceGradients,
+    RaceOutput,
+    SketchConfig,
+    accumulate_num_den,
+    all_hyperplanes,
+    derive_table_rng,
+    gaussian_matrix,
+    race_attention,
+    race_attention_vjp,
+    table_hyperplanes,
+)
+from .functional import (
+    RaceAttentionFunction,
+    SketchParams,
+    race_attention_torch,
+    race_backward,
+    race_forward,
+)
+from .module import RaceAttention, head_hyperplanes
+from .sharded import sharded_backward, sharded_forward, shard_bounds
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AttnInputs", "DEGENERATE_DEN_EPS", "RaceAttention", "RaceAttentionFunction", "RaceGradients",
+    "RaceOutput", "SketchConfig", "SketchParams", "ZERO_ROW_EPS", "accumulate_num_den",
+    "all_hyperplanes", "derive_table_rng", "gaussian_matrix", "head_hyperplanes", "race_attention",
+    "race_attention_torch", "race_attention_vjp", "race_backward", "race_forward", "shard_bounds",
+    "sharded_backward", "sharded_forward", "table_hyperplanes",
+]

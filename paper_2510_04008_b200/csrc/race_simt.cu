@@ -1,0 +1,794 @@
+// race_simt.cu -- generic CUDA-core kernels for every RACE attention pass.
+//
+// These handle ANY shape the reference accepts within the shared-memory
+// budget (d, dv, P, T arbitrary; N arbitrary incl. ragged tails).  They run
+// entirely on the device; the sm_100a tcgen05 fast path (race_tc.cu) takes
+// over for the production shapes.  Everything here follows the chunk
+// formulation of DESIGN.md section 3, which restates the reference's
+// per-table loops (ra/forward.py:77-144, ra/backward.py:93-235):
+//
+//   S      = phi(K)^T [V | 1]                                (F x (dv+1))
+//   fwd    : D_t = phi_q,t . A,  O_t = phi_q,t S_v / D_t,    den_t = D_t / T
+//   causal : S_<c carried across tiles/segments; intra-tile  P = tril(Phi_q Phi_k^T)
+//   bwd    : y_t = S_v dO_t,  rho_t = dO_t . O_t,
+//            dphi_q,t = (y_t - rho_t A) / D_t   (+ intra-tile terms, causal)
+//            G_t = [dO_t / D_t | -rho_t / D_t],  dS = Phi_q^T G
+//            dphi_k,i = [v_i | 1] dS^T,  dV_i = phi_k,i dS_v
+//   then the softmax / tanh / row-normalisation VJPs.
+//
+// Determinism: no atomics; every reduction has a fixed order, so results are
+// bit-identical run to run (the reference's criterion 9, ra/acceptance.py:419).
+#include "race_common.cuh"
+#include "race_internal.h"
+
+namespace race {
+namespace simt {
+
+constexpr int TILE = 32;   // tokens per tile
+constexpr int NT = 128;    // threads per CTA
+
+__host__ __device__ inline int odd_ld(int n) { return n | 1; }
+
+// ---------------------------------------------------------------------------
+// shared-memory plan (same arithmetic on host and device)
+// ---------------------------------------------------------------------------
+enum Need : unsigned {
+  kW = 1u << 0, kS = 1u << 1, kAcc = 1u << 2, kXq = 1u << 3, kXk = 1u << 4,
+  kDx = 1u << 5, kV = 1u << 6, kG = 1u << 7, kPhq = 1u << 8, kPhk = 1u << 9,
+  kDph = 1u << 10, kY = 1u << 11, kU = 1u << 12, kDproj = 1u << 13,
+  kPm = 1u << 14, kEm = 1u << 15,
+};
+
+struct Plan {
+  int d, dv, P, T, R, F, TP;
+  int ldx, ldv, ldf, ldS, ldu, ldp;
+  // float offsets (all buffers are float)
+  int oW, oS, oAcc, oXq, oXk, oDx, oV, oG, oPhq, oPhk, oDph, oY, oU, oDproj, oPm, oEm;
+  int oRow;      // 8 row-scalar arrays of TILE floats
+  int total;     // floats
+
+  __host__ __device__ Plan(const Geo& g, unsigned need) {
+    d = g.d; dv = g.dv; P = g.P; T = g.T; R = 1 << g.P; F = g.T * R; TP = g.T * g.P;
+    ldx = odd_ld(d + 1); ldv = odd_ld(dv + 1); ldf = odd_ld(F); ldS = odd_ld(dv + 1);
+    ldu = odd_ld(TP); ldp = TILE + 1;
+    int o = 0;
+    auto take = [&](unsigned bit, int n) { int r = (need & bit) ? o : -1; if (need & bit) o += (n + 3) & ~3; return r; };
+    oW = take(kW, TP * d);
+    oS = take(kS, F * ldS);
+    oAcc = take(kAcc, F * ldS);
+    oXq = take(kXq, TILE * ldx);
+    oXk = take(kXk, TILE * ldx);
+    oDx = take(kDx, TILE * ldx);
+    oV = take(kV, TILE * ldv);
+    oG = take(kG, TILE * ldv);
+    oPhq = take(kPhq, TILE * ldf);
+    oPhk = take(kPhk, TILE * ldf);
+    oDph = take(kDph, TILE * ldf);
+    oY = take(kY, TILE * ldf);
+    oU = take(kU, TILE * ldu);
+    oDproj = take(kDproj, TILE * ldu);
+    oPm = take(kPm, TILE * ldp);
+    oEm = take(kEm, TILE * ldp);
+    oRow = o; o += 8 * TILE;
+    total = o;
+  }
+  __host__ __device__ size_t bytes() const { return size_t(total) * sizeof(float); }
+};
+
+// row-scalar slots inside Plan::oRow
+enum RowSlot { kScQ = 0, kScK = 1, kD = 2, kRho = 3, kRD = 4, kGD = 5, kDot = 6, kTmp = 7 };
+
+// ---------------------------------------------------------------------------
+// block-level building blocks
+// ---------------------------------------------------------------------------
+
+// Load `rows` rows (row stride `cols`) of a [*, cols] tensor into smem
+// (stride ld), zero-filling rows >= rows.  If `scale` is given, also stores
+// the per-row normalisation scale: ||x|| (or -1 if < 1e-12, the pass-through
+// rows of ra/core.py:120-122), or 1 when normalisation is off.
+template <typename Tin>
+__device__ void load_rows(const Tin* __restrict__ src, int rows, int cols, float* dst, int ld,
+                          float* scale, bool normalize) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < TILE; r += NT / 32) {
+    float ss = 0.f;
+    if (r < rows) {
+      const Tin* s = src + size_t(r) * cols;
+      for (int c = lane; c < cols; c += 32) {
+        const float x = to_f32(s[c]);
+        dst[r * ld + c] = x;
+        ss = fmaf(x, x, ss);
+      }
+    } else {
+      for (int c = lane; c < cols; c += 32) dst[r * ld + c] = 0.f;
+    }
+    if (scale) {
+      ss = warp_sum(ss);
+      if (lane == 0) {
+        const float nrm = sqrtf(ss);
+        scale[r] = normalize ? (nrm < kZeroRowEps ? -1.f : nrm) : 1.f;
+      }
+    }
+  }
+}
+
+// V (or dO) tile with an appended ones column at index dv (1 for valid rows).
+template <typename Tin>
+__device__ void load_v_ones(const Tin* __restrict__ src, int rows, int dv, float* dst, int ld) {
+  load_rows<Tin>(src, rows, dv, dst, ld, nullptr, false);
+  for (int r = threadIdx.x; r < TILE; r += NT) dst[r * ld + dv] = r < rows ? 1.f : 0.f;
+}
+
+// phi (and optionally u) for the TILE rows in xs.  Items are (row, table).
+__device__ void tile_features(const Plan& pl, const float* xs, const float* scale, const float* ws,
+                              float beta, float* phi, float* u_out) {
+  for (int it = threadIdx.x; it < TILE * pl.T; it += NT) {
+    const int tau = it / TILE, r = it % TILE;
+    const float sc = scale[r];
+    const float inv = sc > 0.f ? 1.f / sc : 1.f;
+    float u[kPMax];
+    const float* x = xs + r * pl.ldx;
+#pragma unroll
+    for (int p = 0; p < kPMax; ++p) {
+      if (p < pl.P) {
+        const float* w = ws + (tau * pl.P + p) * pl.d;
+        float acc = 0.f;
+        for (int c = 0; c < pl.d; ++c) acc = fmaf(x[c], w[c], acc);
+        u[p] = tanhf(acc * inv);
+        if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = u[p];
+      }
+    }
+    corner_softmax(u, pl.P, beta, phi + r * pl.ldf + tau * pl.R);
+  }
+}
+
+// Feature VJP for the TILE rows: given dphi (smem [TILE][ldf]) produce dx
+// (the gradient w.r.t. the RAW input rows, i.e. including the
+// row-normalisation VJP of ra/core.py:126-139) and write valid rows to dst.
+// ra/backward.py:53-90 (softmax + tanh VJP), then dx^ = dproj . W.
+template <typename Tout>
+__device__ void tile_feature_vjp(const Plan& pl, const float* xs, const float* scale,
+                                 const float* ws, float beta, const float* phi, const float* u,
+                                 const float* dphi, float* dproj, float* dx, float* dots,
+                                 bool normalize, int rows, Tout* __restrict__ dst) {
+  // (1) softmax + tanh VJP per (row, table)
+  for (int it = threadIdx.x; it < TILE * pl.T; it += NT) {
+    const int tau = it / TILE, r = it % TILE;
+    const float* ph = phi + r * pl.ldf + tau * pl.R;
+    const float* dp = dphi + r * pl.ldf + tau * pl.R;
+    float s = 0.f;
+    for (int rr = 0; rr < pl.R; ++rr) s = fmaf(dp[rr], ph[rr], s);
+    float du[kPMax];
+#pragma unroll
+    for (int p = 0; p < kPMax; ++p) du[p] = 0.f;
+    for (int rr = 0; rr < pl.R; ++rr) {
+      const float dl = ph[rr] * (dp[rr] - s);
+#pragma unroll
+      for (int p = 0; p < kPMax; ++p)
+        if (p < pl.P) du[p] += ((rr >> p) & 1) ? -dl : dl;
+    }
+#pragma unroll
+    for (int p = 0; p < kPMax; ++p) {
+      if (p < pl.P) {
+        const float uu = u[r * pl.ldu + tau * pl.P + p];
+        dproj[r * pl.ldu + tau * pl.P + p] = beta * du[p] * (1.f - uu * uu);
+      }
+    }
+  }
+  __syncthreads();
+  // (2) dx^ = dproj . W  (items (row, col)); the projection used x^ = x / scale
+  for (int it = threadIdx.x; it < TILE * pl.d; it += NT) {
+    const int r = it / pl.d, c = it % pl.d;
+    const float* dpr = dproj + r * pl.ldu;
+    float acc = 0.f;
+    for (int j = 0; j < pl.TP; ++j) acc = fmaf(dpr[j], ws[j * pl.d + c], acc);
+    dx[r * pl.ldx + c] = acc;
+  }
+  __syncthreads();
+  // (3) radial component (dx^ . x^) per row, warp per row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < TILE; r += NT / 32) {
+    const float sc = scale[r];
+    float acc = 0.f;
+    if (normalize && sc > 0.f) {
+      for (int c = lane; c < pl.d; c += 32) acc = fmaf(dx[r * pl.ldx + c], xs[r * pl.ldx + c], acc);
+      acc = warp_sum(acc) / sc;
+    }
+    if (lane == 0) dots[r] = acc;
+  }
+  __syncthreads();
+  // (4) sphere-tangent projection, scaled by 1/||x||; pass-through rows keep dx^
+  for (int it = threadIdx.x; it < rows * pl.d; it += NT) {
+    const int r = it / pl.d, c = it % pl.d;
+    const float sc = scale[r];
+    float g = dx[r * pl.ldx + c];
+    if (normalize && sc > 0.f) {
+      const float rs = 1.f / sc;
+      g = (g - dots[r] * xs[r * pl.ldx + c] * rs) * rs;
+    }
+    dst[size_t(r) * pl.d + c] = from_f32<Tout>(g);
+  }
+}
+
+// acc[f][c] += sum_{t<TILE} A[t][f] * B[t][c] for every (f, c <= dv); each
+// output is owned by one thread, so this is a fixed-order reduction.
+__device__ __forceinline__ void owner_accumulate(const Plan& pl, float* acc, const float* A,
+                                                 const float* B) {
+  const int nout = pl.F * (pl.dv + 1);
+  for (int o = threadIdx.x; o < nout; o += NT) {
+    const int f = o / (pl.dv + 1), c = o % (pl.dv + 1);
+    float s = acc[f * pl.ldS + c];
+    float part = 0.f;
+#pragma unroll 8
+    for (int t = 0; t < TILE; ++t) part = fmaf(A[t * pl.ldf + f], B[t * pl.ldv + c], part);
+    acc[f * pl.ldS + c] = s + part;
+  }
+}
+
+__device__ __forceinline__ void load_w(const Plan& pl, const float* __restrict__ w, float* ws) {
+  for (int i = threadIdx.x; i < pl.TP * pl.d; i += NT) ws[i] = w[i];
+}
+
+__device__ __forceinline__ void load_table(const Plan& pl, const float* __restrict__ src, float* dst) {
+  const int nout = pl.F * (pl.dv + 1);
+  for (int o = threadIdx.x; o < nout; o += NT) {
+    const int f = o / (pl.dv + 1), c = o % (pl.dv + 1);
+    dst[f * pl.ldS + c] = src ? src[o] : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store_table(const Plan& pl, const float* src, float* __restrict__ dst) {
+  const int nout = pl.F * (pl.dv + 1);
+  for (int o = threadIdx.x; o < nout; o += NT) {
+    const int f = o / (pl.dv + 1), c = o % (pl.dv + 1);
+    dst[o] = src[f * pl.ldS + c];
+  }
+}
+
+struct Range {
+  int64_t begin, end;
+};
+__device__ __forceinline__ Range seg_range(const Geo& g) {
+  const int64_t b = int64_t(blockIdx.x) * g.seg_tokens;
+  const int64_t e = b + g.seg_tokens < g.N ? b + g.seg_tokens : g.N;
+  return {b, e};
+}
+__device__ __forceinline__ const float* w_of(const Geo& g, const float* w, int64_t bh) {
+  return w + (g.w_per_head ? (bh % g.H) * int64_t(g.T * g.P * g.d) : 0);
+}
+
+extern __shared__ float4 smem_f4[];
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+// part[bh][seg] = phi(K_seg)^T [V_seg | 1]
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_aggregate(Geo g, const Tin* __restrict__ k,
+                                                  const Tin* __restrict__ v,
+                                                  const float* __restrict__ w, float* __restrict__ part) {
+  const Plan pl(g, kW | kAcc | kXk | kV | kPhk);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* acc = sm + pl.oAcc; float* xk = sm + pl.oXk;
+  float* vs = sm + pl.oV; float* phk = sm + pl.oPhk; float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, nullptr, acc);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
+    __syncthreads();
+    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    __syncthreads();
+    owner_accumulate(pl, acc, phk, vs);
+  }
+  __syncthreads();
+  store_table(pl, acc, part + (bh * g.nseg + blockIdx.x) * int64_t(pl.F * (g.dv + 1)));
+}
+
+// Non-causal readout: O = phi_q S_v / D, den = D / T.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_readout(Geo g, const Tin* __restrict__ q,
+                                                const float* __restrict__ w,
+                                                const float* __restrict__ tables, Tin* __restrict__ o,
+                                                float* __restrict__ den) {
+  const Plan pl(g, kW | kS | kXq | kPhq);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* S = sm + pl.oS; float* xq = sm + pl.oXq; float* phq = sm + pl.oPhq;
+  float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, tables + bh * int64_t(pl.F * (g.dv + 1)), S);
+  const float invT = 1.f / float(g.T);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
+    __syncthreads();
+    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
+    __syncthreads();
+    for (int r = threadIdx.x; r < TILE; r += NT) {
+      float D = 0.f;
+      for (int f = 0; f < pl.F; ++f) D = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + g.dv], D);
+      rowv[kD * TILE + r] = D;
+      if (r < rows) den[bh * g.N + t0 + r] = D * invT;
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
+      const int r = it / g.dv, c = it % g.dv;
+      float num = 0.f;
+      for (int f = 0; f < pl.F; ++f) num = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + c], num);
+      const float D = rowv[kD * TILE + r];
+      o[(bh * g.N + t0 + r) * g.dv + c] = from_f32<Tin>(D * invT <= kDegenerateDenEps ? 0.f : num / D);
+    }
+  }
+}
+
+// Causal forward over one segment with carry-in S_<seg.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict__ q,
+                                                   const Tin* __restrict__ k, const Tin* __restrict__ v,
+                                                   const float* __restrict__ w,
+                                                   const float* __restrict__ carries,
+                                                   Tin* __restrict__ o, float* __restrict__ den) {
+  const Plan pl(g, kW | kS | kXq | kXk | kV | kPhq | kPhk | kPm);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* S = sm + pl.oS; float* xq = sm + pl.oXq; float* xk = sm + pl.oXk;
+  float* vs = sm + pl.oV; float* phq = sm + pl.oPhq; float* phk = sm + pl.oPhk; float* Pm = sm + pl.oPm;
+  float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  const int64_t tsz = int64_t(pl.F) * (g.dv + 1);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, carries + (bh * g.nseg + blockIdx.x) * tsz, S);
+  const float invT = 1.f / float(g.T);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
+    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
+    __syncthreads();
+    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
+    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
+      const int r = it / TILE, j = it % TILE;
+      float p = 0.f;
+      if (j <= r && j < rows)
+        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[r * pl.ldf + f], phk[j * pl.ldf + f], p);
+      Pm[r * pl.ldp + j] = p;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < TILE; r += NT) {
+      float D = 0.f;
+      for (int f = 0; f < pl.F; ++f) D = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + g.dv], D);
+      for (int j = 0; j <= r; ++j) D += Pm[r * pl.ldp + j];
+      rowv[kD * TILE + r] = D;
+      if (r < rows) den[bh * g.N + t0 + r] = D * invT;
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
+      const int r = it / g.dv, c = it % g.dv;
+      float num = 0.f;
+      for (int f = 0; f < pl.F; ++f) num = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + c], num);
+      for (int j = 0; j <= r; ++j) num = fmaf(Pm[r * pl.ldp + j], vs[j * pl.ldv + c], num);
+      const float D = rowv[kD * TILE + r];
+      o[(bh * g.N + t0 + r) * g.dv + c] = from_f32<Tin>(D * invT <= kDegenerateDenEps ? 0.f : num / D);
+    }
+    __syncthreads();
+    owner_accumulate(pl, S, phk, vs);  // S_<next tile
+  }
+}
+
+// Non-causal backward, query side.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_bwd_q(Geo g, const Tin* __restrict__ q, const Tin* __restrict__ d_o,
+                                              const float* __restrict__ w,
+                                              const float* __restrict__ tables, Tin* __restrict__ dq,
+                                              float* __restrict__ dpart) {
+  const Plan pl(g, kW | kS | kAcc | kXq | kDx | kG | kPhq | kDph | kY | kU | kDproj);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* S = sm + pl.oS; float* acc = sm + pl.oAcc; float* xq = sm + pl.oXq;
+  float* dx = sm + pl.oDx; float* gs = sm + pl.oG; float* phq = sm + pl.oPhq; float* dph = sm + pl.oDph;
+  float* ys = sm + pl.oY; float* us = sm + pl.oU; float* dproj = sm + pl.oDproj; float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  const int64_t tsz = int64_t(pl.F) * (g.dv + 1);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, tables + bh * tsz, S);
+  load_table(pl, nullptr, acc);
+  const float invT = 1.f / float(g.T);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
+    load_rows<Tin>(d_o + (bh * g.N + t0) * g.dv, rows, g.dv, gs, pl.ldv, nullptr, false);
+    __syncthreads();
+    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us);
+    // y[t][f] = S_v[f] . dO_t
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int r = it / pl.F, f = it % pl.F;
+      float y = 0.f;
+      for (int c = 0; c < g.dv; ++c) y = fmaf(S[f * pl.ldS + c], gs[r * pl.ldv + c], y);
+      ys[r * pl.ldf + f] = y;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < TILE; r += NT) {
+      float D = 0.f, num = 0.f;
+      for (int f = 0; f < pl.F; ++f) {
+        D = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + g.dv], D);
+        num = fmaf(phq[r * pl.ldf + f], ys[r * pl.ldf + f], num);
+      }
+      const bool live = r < rows && D * invT > kDegenerateDenEps;
+      const float rD = live ? 1.f / D : 0.f;
+      rowv[kRD * TILE + r] = rD;
+      rowv[kRho * TILE + r] = live ? num * rD : 0.f;  // rho = dO . O
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int r = it / pl.F, f = it % pl.F;
+      dph[r * pl.ldf + f] = (ys[r * pl.ldf + f] - rowv[kRho * TILE + r] * S[f * pl.ldS + g.dv]) * rowv[kRD * TILE + r];
+    }
+    for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
+      const int r = it / (g.dv + 1), c = it % (g.dv + 1);
+      const float rD = rowv[kRD * TILE + r];
+      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rD : -rowv[kRho * TILE + r] * rD;
+    }
+    __syncthreads();
+    tile_feature_vjp<Tin>(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us, dph, dproj, dx,
+                          rowv + kDot * TILE, g.normalize, rows, dq + (bh * g.N + t0) * g.d);
+    owner_accumulate(pl, acc, phq, gs);
+  }
+  __syncthreads();
+  store_table(pl, acc, dpart + (bh * g.nseg + blockIdx.x) * tsz);
+}
+
+// Non-causal backward, key side given global dS.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_bwd_k(Geo g, const Tin* __restrict__ k, const Tin* __restrict__ v,
+                                              const float* __restrict__ w,
+                                              const float* __restrict__ dtables, Tin* __restrict__ dk,
+                                              Tin* __restrict__ dvo) {
+  const Plan pl(g, kW | kS | kXk | kDx | kV | kPhk | kDph | kU | kDproj);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* dS = sm + pl.oS; float* xk = sm + pl.oXk; float* dx = sm + pl.oDx;
+  float* vs = sm + pl.oV; float* phk = sm + pl.oPhk; float* dph = sm + pl.oDph; float* us = sm + pl.oU;
+  float* dproj = sm + pl.oDproj; float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, dtables + bh * int64_t(pl.F) * (g.dv + 1), dS);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
+    __syncthreads();
+    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us);
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int r = it / pl.F, f = it % pl.F;
+      float z = 0.f;
+      for (int c = 0; c <= g.dv; ++c) z = fmaf(dS[f * pl.ldS + c], vs[r * pl.ldv + c], z);
+      dph[r * pl.ldf + f] = z;
+    }
+    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
+      const int r = it / g.dv, c = it % g.dv;
+      float a = 0.f;
+      for (int f = 0; f < pl.F; ++f) a = fmaf(phk[r * pl.ldf + f], dS[f * pl.ldS + c], a);
+      dvo[(bh * g.N + t0 + r) * g.dv + c] = from_f32<Tin>(a);
+    }
+    __syncthreads();
+    tile_feature_vjp<Tin>(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us, dph, dproj, dx,
+                          rowv + kDot * TILE, g.normalize, rows, dk + (bh * g.N + t0) * g.d);
+  }
+}
+
+// Causal backward, forward scan: dq, per-token rden / gden, per-segment dS.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restrict__ q,
+                                                     const Tin* __restrict__ k, const Tin* __restrict__ v,
+                                                     const Tin* __restrict__ d_o, const float* __restrict__ w,
+                                                     const float* __restrict__ carries, Tin* __restrict__ dq,
+                                                     float* __restrict__ rden, float* __restrict__ gden,
+                                                     float* __restrict__ dpart) {
+  const Plan pl(g, kW | kS | kAcc | kXq | kXk | kDx | kV | kG | kPhq | kPhk | kDph | kY | kU | kDproj | kPm | kEm);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* S = sm + pl.oS; float* acc = sm + pl.oAcc; float* xq = sm + pl.oXq;
+  float* xk = sm + pl.oXk; float* dx = sm + pl.oDx; float* vs = sm + pl.oV; float* gs = sm + pl.oG;
+  float* phq = sm + pl.oPhq; float* phk = sm + pl.oPhk; float* dph = sm + pl.oDph; float* ys = sm + pl.oY;
+  float* us = sm + pl.oU; float* dproj = sm + pl.oDproj; float* Pm = sm + pl.oPm; float* Em = sm + pl.oEm;
+  float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  const int64_t tsz = int64_t(pl.F) * (g.dv + 1);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, carries + (bh * g.nseg + blockIdx.x) * tsz, S);
+  load_table(pl, nullptr, acc);
+  const float invT = 1.f / float(g.T);
+  for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
+    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
+    load_rows<Tin>(d_o + (bh * g.N + t0) * g.dv, rows, g.dv, gs, pl.ldv, nullptr, false);
+    __syncthreads();
+    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us);
+    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
+      const int r = it / TILE, j = it % TILE;
+      float p = 0.f, e = 0.f;
+      if (j <= r && j < rows) {
+        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[r * pl.ldf + f], phk[j * pl.ldf + f], p);
+        for (int c = 0; c < g.dv; ++c) e = fmaf(gs[r * pl.ldv + c], vs[j * pl.ldv + c], e);
+      }
+      Pm[r * pl.ldp + j] = p;
+      Em[r * pl.ldp + j] = e;
+    }
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int r = it / pl.F, f = it % pl.F;
+      float y = 0.f;
+      for (int c = 0; c < g.dv; ++c) y = fmaf(S[f * pl.ldS + c], gs[r * pl.ldv + c], y);
+      ys[r * pl.ldf + f] = y;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < TILE; r += NT) {
+      float D = 0.f, num = 0.f;
+      for (int f = 0; f < pl.F; ++f) {
+        D = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + g.dv], D);
+        num = fmaf(phq[r * pl.ldf + f], ys[r * pl.ldf + f], num);
+      }
+      for (int j = 0; j <= r; ++j) {
+        D += Pm[r * pl.ldp + j];
+        num = fmaf(Pm[r * pl.ldp + j], Em[r * pl.ldp + j], num);
+      }
+      const bool live = r < rows && D * invT > kDegenerateDenEps;
+      const float rD = live ? 1.f / D : 0.f;
+      const float rho = live ? num * rD : 0.f;
+      rowv[kRD * TILE + r] = rD;
+      rowv[kRho * TILE + r] = rho;
+      if (r < rows) {
+        rden[bh * g.N + t0 + r] = rD;
+        gden[bh * g.N + t0 + r] = -rho * rD;
+      }
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int r = it / pl.F, f = it % pl.F;
+      const float rho = rowv[kRho * TILE + r];
+      float a = ys[r * pl.ldf + f] - rho * S[f * pl.ldS + g.dv];
+      const int jmax = r < rows ? r : rows - 1;
+      for (int j = 0; j <= jmax; ++j) a = fmaf(Em[r * pl.ldp + j] - rho, phk[j * pl.ldf + f], a);
+      dph[r * pl.ldf + f] = a * rowv[kRD * TILE + r];
+    }
+    for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
+      const int r = it / (g.dv + 1), c = it % (g.dv + 1);
+      const float rD = rowv[kRD * TILE + r];
+      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rD : -rowv[kRho * TILE + r] * rD;
+    }
+    __syncthreads();
+    tile_feature_vjp<Tin>(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us, dph, dproj, dx,
+                          rowv + kDot * TILE, g.normalize, rows, dq + (bh * g.N + t0) * g.d);
+    owner_accumulate(pl, acc, phq, gs);
+    owner_accumulate(pl, S, phk, vs);
+  }
+  __syncthreads();
+  store_table(pl, acc, dpart + (bh * g.nseg + blockIdx.x) * tsz);
+}
+
+// Causal backward, reverse scan over one segment with suffix carry dS_>seg.
+template <typename Tin>
+__global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restrict__ q,
+                                                     const Tin* __restrict__ k, const Tin* __restrict__ v,
+                                                     const Tin* __restrict__ d_o, const float* __restrict__ w,
+                                                     const float* __restrict__ rden,
+                                                     const float* __restrict__ gden,
+                                                     const float* __restrict__ dcarries,
+                                                     Tin* __restrict__ dk, Tin* __restrict__ dvo) {
+  const Plan pl(g, kW | kS | kXq | kXk | kDx | kV | kG | kPhq | kPhk | kDph | kU | kDproj | kPm | kEm);
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float* ws = sm + pl.oW; float* dS = sm + pl.oS; float* xq = sm + pl.oXq; float* xk = sm + pl.oXk;
+  float* dx = sm + pl.oDx; float* vs = sm + pl.oV; float* gs = sm + pl.oG; float* phq = sm + pl.oPhq;
+  float* phk = sm + pl.oPhk; float* dph = sm + pl.oDph; float* us = sm + pl.oU; float* dproj = sm + pl.oDproj;
+  float* PmT = sm + pl.oPm; float* EGT = sm + pl.oEm; float* rowv = sm + pl.oRow;
+  const int64_t bh = blockIdx.y;
+  const Range rg = seg_range(g);
+  const int64_t tsz = int64_t(pl.F) * (g.dv + 1);
+  load_w(pl, w_of(g, w, bh), ws);
+  load_table(pl, dcarries + (bh * g.nseg + blockIdx.x) * tsz, dS);
+  const int64_t ntile = (rg.end - rg.begin + TILE - 1) / TILE;
+  for (int64_t ti = ntile - 1; ti >= 0; --ti) {
+    const int64_t t0 = rg.begin + ti * TILE;
+    const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
+    __syncthreads();
+    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
+    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
+    load_rows<Tin>(d_o + (bh * g.N + t0) * g.dv, rows, g.dv, gs, pl.ldv, nullptr, false);
+    for (int r = threadIdx.x; r < TILE; r += NT) {
+      rowv[kRD * TILE + r] = r < rows ? rden[bh * g.N + t0 + r] : 0.f;
+      rowv[kGD * TILE + r] = r < rows ? gden[bh * g.N + t0 + r] : 0.f;
+    }
+    __syncthreads();
+    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
+    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us);
+    for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
+      const int r = it / (g.dv + 1), c = it % (g.dv + 1);
+      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rowv[kRD * TILE + r] : rowv[kGD * TILE + r];
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
+      const int i = it / TILE, t = it % TILE;
+      float p = 0.f, e = 0.f;
+      if (t >= i && t < rows) {
+        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[t * pl.ldf + f], phk[i * pl.ldf + f], p);
+        for (int c = 0; c <= g.dv; ++c) e = fmaf(gs[t * pl.ldv + c], vs[i * pl.ldv + c], e);
+      }
+      PmT[i * pl.ldp + t] = p;
+      EGT[i * pl.ldp + t] = e;
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
+      const int i = it / pl.F, f = it % pl.F;
+      float a = 0.f;
+      for (int c = 0; c <= g.dv; ++c) a = fmaf(dS[f * pl.ldS + c], vs[i * pl.ldv + c], a);
+      for (int t = i; t < rows; ++t) a = fmaf(EGT[i * pl.ldp + t], phq[t * pl.ldf + f], a);
+      dph[i * pl.ldf + f] = a;
+    }
+    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
+      const int i = it / g.dv, c = it % g.dv;
+      float a = 0.f;
+      for (int f = 0; f < pl.F; ++f) a = fmaf(phk[i * pl.ldf + f], dS[f * pl.ldS + c], a);
+      for (int t = i; t < rows; ++t) a = fmaf(PmT[i * pl.ldp + t], gs[t * pl.ldv + c], a);
+      dvo[(bh * g.N + t0 + i) * g.dv + c] = from_f32<Tin>(a);
+    }
+    __syncthreads();
+    tile_feature_vjp<Tin>(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us, dph, dproj, dx,
+                          rowv + kDot * TILE, g.normalize, rows, dk + (bh * g.N + t0) * g.d);
+    owner_accumulate(pl, dS, phq, gs);
+  }
+}
+
+// Fixed-order segment reduction (see race_combine in race_b200.h).
+__global__ void k_combine(int64_t BH, int64_t nseg, int64_t E, int mode, const float* __restrict__ part,
+                          const float* __restrict__ carry, float* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t bh = blockIdx.y;
+  if (e >= E) return;
+  const float* p = part + bh * nseg * E + e;
+  float s = carry ? carry[bh * E + e] : 0.f;
+  if (mode == 0) {
+    for (int64_t i = 0; i < nseg; ++i) s += p[i * E];
+    out[bh * E + e] = s;
+  } else if (mode == 1) {
+    for (int64_t i = 0; i < nseg; ++i) {
+      out[(bh * nseg + i) * E + e] = s;
+      s += p[i * E];
+    }
+  } else {
+    for (int64_t i = nseg - 1; i >= 0; --i) {
+      out[(bh * nseg + i) * E + e] = s;
+      s += p[i * E];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+template <typename K>
+static cudaError_t prep(K kernel, size_t smem) {
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  return cudaSuccess;
+}
+
+#define RACE_LAUNCH(KER, NEED, ...)                                                      \
+  do {                                                                                   \
+    const size_t smem = Plan(g, NEED).bytes();                                           \
+    if (smem > kMaxSmem) return cudaErrorInvalidConfiguration;                           \
+    cudaError_t e_ = prep(KER, smem);                                                    \
+    if (e_ != cudaSuccess) return e_;                                                    \
+    KER<<<dim3(unsigned(g.nseg), unsigned(g.BH)), NT, smem, st>>>(g, __VA_ARGS__);       \
+    note_launch();                                                                       \
+    return cudaGetLastError();                                                           \
+  } while (0)
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+template <typename Tin>
+struct Launch {
+  static cudaError_t aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st) {
+    RACE_LAUNCH(k_aggregate<Tin>, kW | kAcc | kXk | kV | kPhk, (const Tin*)k, (const Tin*)v, w, part);
+  }
+  static cudaError_t readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
+                             cudaStream_t st) {
+    RACE_LAUNCH(k_readout<Tin>, kW | kS | kXq | kPhq, (const Tin*)q, w, tab, (Tin*)o, den);
+  }
+  static cudaError_t causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
+                                const float* car, void* o, float* den, cudaStream_t st) {
+    RACE_LAUNCH(k_causal_fwd<Tin>, kW | kS | kXq | kXk | kV | kPhq | kPhk | kPm, (const Tin*)q, (const Tin*)k,
+                (const Tin*)v, w, car, (Tin*)o, den);
+  }
+  static cudaError_t bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
+                           float* dpart, cudaStream_t st) {
+    RACE_LAUNCH(k_bwd_q<Tin>, kW | kS | kAcc | kXq | kDx | kG | kPhq | kDph | kY | kU | kDproj, (const Tin*)q,
+                (const Tin*)d_o, w, tab, (Tin*)dq, dpart);
+  }
+  static cudaError_t bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
+                           void* dv, cudaStream_t st) {
+    RACE_LAUNCH(k_bwd_k<Tin>, kW | kS | kXk | kDx | kV | kPhk | kDph | kU | kDproj, (const Tin*)k, (const Tin*)v, w,
+                dtab, (Tin*)dk, (Tin*)dv);
+  }
+  static cudaError_t bwd_causal_q(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                                  const float* w, const float* car, void* dq, float* rden, float* gden, float* dpart,
+                                  cudaStream_t st) {
+    RACE_LAUNCH(k_bwd_causal_q<Tin>,
+                kW | kS | kAcc | kXq | kXk | kDx | kV | kG | kPhq | kPhk | kDph | kY | kU | kDproj | kPm | kEm,
+                (const Tin*)q, (const Tin*)k, (const Tin*)v, (const Tin*)d_o, w, car, (Tin*)dq, rden, gden, dpart);
+  }
+  static cudaError_t bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                                  const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
+                                  void* dv, cudaStream_t st) {
+    RACE_LAUNCH(k_bwd_causal_k<Tin>,
+                kW | kS | kXq | kXk | kDx | kV | kG | kPhq | kPhk | kDph | kU | kDproj | kPm | kEm, (const Tin*)q,
+                (const Tin*)k, (const Tin*)v, (const Tin*)d_o, w, rden, gden, dcar, (Tin*)dk, (Tin*)dv);
+  }
+};
+
+}  // namespace simt
+
+// ---- dispatch used by race_abi.cu ------------------------------------------
+size_t simt_max_smem(const Geo& g) {
+  using namespace simt;
+  return Plan(g, kW | kS | kAcc | kXq | kXk | kDx | kV | kG | kPhq | kPhk | kDph | kY | kU | kDproj | kPm | kEm).bytes();
+}
+
+#define RACE_DISPATCH(FN, ...) \
+  (g.dtype == 1 ? simt::Launch<__nv_bfloat16>::FN(__VA_ARGS__) : simt::Launch<float>::FN(__VA_ARGS__))
+
+cudaError_t simt_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st) {
+  return RACE_DISPATCH(aggregate, g, k, v, w, part, st);
+}
+cudaError_t simt_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
+                         cudaStream_t st) {
+  return RACE_DISPATCH(readout, g, q, w, tab, o, den, st);
+}
+cudaError_t simt_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
+                            const float* car, void* o, float* den, cudaStream_t st) {
+  return RACE_DISPATCH(causal_fwd, g, q, k, v, w, car, o, den, st);
+}
+cudaError_t simt_bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
+                       float* dpart, cudaStream_t st) {
+  return RACE_DISPATCH(bwd_q, g, q, d_o, w, tab, dq, dpart, st);
+}
+cudaError_t simt_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
+                       void* dv, cudaStream_t st) {
+  return RACE_DISPATCH(bwd_k, g, k, v, w, dtab, dk, dv, st);
+}
+cudaError_t simt_bwd_causal_q(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                              const float* w, const float* car, void* dq, float* rden, float* gden, float* dpart,
+                              cudaStream_t st) {
+  return RACE_DISPATCH(bwd_causal_q, g, q, k, v, d_o, w, car, dq, rden, gden, dpart, st);
+}
+cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                              const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
+                              void* dv, cudaStream_t st) {
+  return RACE_DISPATCH(bwd_causal_k, g, q, k, v, d_o, w, rden, gden, dcar, dk, dv, st);
+}
+cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st) {
+  const int64_t E = int64_t(g.T << g.P) * (g.dv + 1);
+  dim3 grid(unsigned((E + 255) / 256), unsigned(g.BH));
+  simt::k_combine<<<grid, 256, 0, st>>>(g.BH, g.nseg, E, mode, part, carry, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace race

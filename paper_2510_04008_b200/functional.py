@@ -1,0 +1,191 @@
+"""Device-tensor entry points over the C-ABI (the layer the drop-in API,
+the autograd Function and the sharded path all call).
+
+Tensors are torch CUDA tensors; the C library sees only raw device pointers,
+sizes and the current stream (include/race_b200.h).  Layout: q, k are
+``[..., N, d]`` and v, o, d_o are ``[..., N, dv]``; the leading dimensions are
+flattened to ``BH`` rows, the last of which is the head index ``h`` used to
+pick that head's hyperplanes (``bh % H``).
+
+Hyperplanes ``w`` (float32 on the device) are either shared ``[T, P, d]`` /
+``[T*P, d]`` or per head ``[H, T, P, d]`` / ``[H, T*P, d]``; tables are in the
+reference's (m, l) task order (``ra/forward.py:128``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+_DTYPES = {torch.float32: _lib.RACE_F32, torch.bfloat16: _lib.RACE_BF16}
+
+
+@dataclass(frozen=True)
+class SketchParams:
+    """The estimator hyper-parameters the kernels need (SketchConfig minus RNG)."""
+
+    hyperplanes: int
+    tables: int  # total tables T = M * L
+    beta: float
+    causal: bool = False
+    normalize: bool = True
+
+
+# ---------------------------------------------------------------------------
+# workspace cache (one growing buffer per device; allocate before graph capture)
+# ---------------------------------------------------------------------------
+_WS: dict[int, torch.Tensor] = {}
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    buf = _WS.get(idx)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS[idx] = buf
+    return buf
+
+
+def _vp(t: torch.Tensor | None) -> ctypes.c_void_p | None:
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def prepare_w(w: torch.Tensor, p: SketchParams, d: int, device) -> tuple[torch.Tensor, bool, int]:
+    """Return (w contiguous fp32 [H?, T*P, d], per_head, heads)."""
+    w = w.to(device=device, dtype=torch.float32)
+    tp = p.tables * p.hyperplanes
+    shared3 = w.dim() == 3 and w.shape[0] == p.tables and w.shape[1] == p.hyperplanes
+    if w.dim() == 4 or (w.dim() == 3 and not shared3):
+        w = w.reshape(w.shape[0], tp, d)
+        per_head, heads = True, w.shape[0]
+    elif w.dim() in (2, 3):
+        w = w.reshape(tp, d)
+        per_head, heads = False, 1
+    else:
+        raise ValueError(f"hyperplane tensor has unsupported shape {tuple(w.shape)}")
+    if w.shape[-1] != d or w.shape[-2] != tp:
+        raise ValueError(f"hyperplanes {tuple(w.shape)} do not match T*P={tp}, d={d}")
+    return w.contiguous(), per_head, heads
+
+
+class Problem:
+    """Validated shapes + descriptor for one call."""
+
+    def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, w: torch.Tensor,
+                 p: SketchParams):
+        if not q.is_cuda:
+            raise ValueError("the RACE B200 path needs CUDA tensors (there is no CPU fallback)")
+        if q.dtype not in _DTYPES:
+            raise ValueError(f"unsupported dtype {q.dtype}; use float32 or bfloat16")
+        if k.dtype != q.dtype or v.dtype != q.dtype:
+            raise ValueError("q, k, v must share one dtype")
+        if q.shape != k.shape:
+            raise ValueError(f"q and k shapes differ: {tuple(q.shape)} vs {tuple(k.shape)}")
+        if q.dim() < 2 or v.dim() != q.dim() or v.shape[:-1] != q.shape[:-1]:
+            raise ValueError(f"v shape {tuple(v.shape)} does not match q {tuple(q.shape)}")
+        self.lead = tuple(q.shape[:-2])
+        self.n, self.d, self.dv = q.shape[-2], q.shape[-1], v.shape[-1]
+        bh = 1
+        for s in self.lead:
+            bh *= s
+        self.bh = bh
+        self.p = p
+        self.device = q.device
+        self.dtype = q.dtype
+        self.w, per_head, heads = prepare_w(w, p, self.d, q.device)
+        if per_head and (len(self.lead) == 0 or self.lead[-1] != heads):
+            raise ValueError(f"per-head hyperplanes for {heads} heads but inputs have lead dims {self.lead}")
+        self.desc = _lib.make_desc(
+            dtype=_DTYPES[q.dtype], batch_heads=max(bh, 1), heads=heads, n=self.n, dim=self.d,
+            dim_v=self.dv, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
+            causal=p.causal, normalize=p.normalize, w_per_head=per_head)
+        self.dref = _lib.ref(self.desc)
+        self.nseg, self.seg_tokens = _lib.segments(self.desc)
+        self.table_elems = (p.tables << p.hyperplanes) * (self.dv + 1)
+
+    def ws(self) -> torch.Tensor:
+        return workspace(_lib.workspace_bytes(self.desc), self.device)
+
+    def state_shape(self) -> tuple[int, ...]:
+        f = self.p.tables << self.p.hyperplanes
+        if self.p.causal:
+            return (self.bh, self.nseg, f, self.dv + 1)
+        return (self.bh, f, self.dv + 1)
+
+
+def _c(t: torch.Tensor) -> torch.Tensor:
+    return t if t.is_contiguous() else t.contiguous()
+
+
+def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
+    """O, den (float32, the reference's averaged den) and the backward state.
+
+    One fwd pass = key-side aggregation -> fixed-order combine -> readout
+    (non-causal) or chunked scan (causal); see race_fwd in race_b200.h.
+    """
+    q, k, v = _c(q), _c(k), _c(v)
+    pr = Problem(q, k, v, w, p)
+    o = torch.empty_like(v)
+    den = torch.empty(pr.lead + (pr.n,), dtype=torch.float32, device=pr.device)
+    state = torch.empty(pr.state_shape(), dtype=torch.float32, device=pr.device) if want_state else None
+    if pr.n == 0 or pr.bh == 0:
+        if state is not None:
+            state.zero_()
+        return o, den, state
+    ws = pr.ws()
+    _lib.check(_lib.lib().race_fwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(o), _vp(den),
+                                   _vp(state), _vp(ws), _stream()), "race_fwd")
+    return o, den, state
+
+
+def race_backward(q, k, v, w, d_o, p: SketchParams, state=None):
+    """(dq, dk, dv).  ``state`` from race_forward avoids re-aggregating K/V."""
+    q, k, v, d_o = _c(q), _c(k), _c(v), _c(d_o)
+    pr = Problem(q, k, v, w, p)
+    if d_o.shape != v.shape or d_o.dtype != v.dtype:
+        raise ValueError(f"d_out shape {tuple(d_o.shape)} does not match output shape {tuple(v.shape)}")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    if pr.n == 0 or pr.bh == 0:
+        return dq, dk, dv
+    if state is not None:
+        state = _c(state)
+        if tuple(state.shape) != pr.state_shape() or state.dtype != torch.float32:
+            raise ValueError("state does not match this problem")
+    ws = pr.ws()
+    _lib.check(_lib.lib().race_bwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(d_o), _vp(state),
+                                   _vp(dq), _vp(dk), _vp(dv), _vp(ws), _stream()), "race_bwd")
+    return dq, dk, dv
+
+
+class RaceAttentionFunction(torch.autograd.Function):
+    """Autograd wrapper: saves the tiny bucket-table state instead of phi."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, w, hyperplanes, tables, beta, causal, normalize):
+        p = SketchParams(hyperplanes, tables, beta, causal, normalize)
+        o, den, state = race_forward(q, k, v, w, p, want_state=True)
+        ctx.p = p
+        ctx.save_for_backward(q, k, v, w, state)
+        ctx.mark_non_differentiable(den)
+        return o, den
+
+    @staticmethod
+    def backward(ctx, d_o, d_den):
+        q, k, v, w, state = ctx.saved_tensors
+        dq, dk, dv = race_backward(q, k, v, w, d_o, ctx.p, state=state)
+        return dq, dk, dv, None, None, None, None, None, None
+
+
+def race_attention_torch(q, k, v, w, p: SketchParams):
+    """Differentiable RACE attention on ``[..., N, d]`` CUDA tensors; returns O."""
+    o, _ = RaceAttentionFunction.apply(q, k, v, w, p.hyperplanes, p.tables, float(p.beta),
+                                       bool(p.causal), bool(p.normalize))
+    return o

@@ -1,0 +1,74 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol
+include/race_b200.h declares, and its host-side queries/validation behave
+(no kernel is launched here)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+from paper_2510_04008_b200 import _lib
+
+HEADER = os.path.join(ROOT, "include", "race_b200.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(race_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_matches_binding():
+    assert set(declared_symbols()) == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_symbol():
+    so = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(so, name), name
+    assert _lib.lib().race_abi_version() == _lib.ABI_VERSION
+
+
+def _desc(**kw):
+    base = dict(dtype=_lib.RACE_BF16, batch_heads=4, heads=4, n=131072, dim=128, dim_v=128,
+                hyperplanes=2, tables=2, beta=8.0, causal=True, normalize=True, w_per_head=True)
+    base.update(kw)
+    return _lib.make_desc(**base)
+
+
+def test_segmentation_and_sizes():
+    d = _desc()
+    nseg, seg = _lib.segments(d)
+    assert seg % 128 == 0 and nseg * seg >= 131072 > (nseg - 1) * seg
+    assert _lib.state_elems(d) == 4 * nseg * 8 * 129
+    assert _lib.state_elems(_desc(causal=False)) == 4 * 8 * 129
+    assert _lib.workspace_bytes(d) >= 4 * 4 * nseg * 8 * 129
+    assert _lib.segments(_desc(n=1)) == (1, 128)
+    assert _lib.segments(_desc(n=0))[0] == 1
+
+
+@pytest.mark.parametrize("kw, exc", [
+    (dict(hyperplanes=0), ValueError),
+    (dict(hyperplanes=21), ValueError),
+    (dict(tables=0), ValueError),
+    (dict(beta=0.0), ValueError),
+    (dict(beta=float("inf")), ValueError),
+    (dict(dim=0), ValueError),
+    (dict(batch_heads=6, heads=4), ValueError),
+    (dict(hyperplanes=11), _lib.RaceUnsupported),
+    (dict(dim=4096), _lib.RaceUnsupported),
+])
+def test_validation(kw, exc):
+    with pytest.raises(exc):
+        _lib.segments(_desc(**kw))
+
+
+def test_bad_abi_version():
+    d = _desc()
+    d.abi_version = 99
+    with pytest.raises(ValueError):
+        _lib.segments(d)

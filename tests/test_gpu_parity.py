@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+Tolerances (BASELINE.json north_star): rel err <= 1e-3 for fp32 inputs and
+<= 1e-2 for bf16 inputs, metric max|a-b|/max|b| (ra/acceptance.py:89-91).
+For gradients the denominator is floored at 5% of the call's largest
+reference gradient, so components that vanish in exact arithmetic (d = 1,
+N = 1) are judged on the natural gradient scale rather than on 1e-17 noise.
+
+* golden fixtures (tests/golden, produced by the real reference): every case
+  through the drop-in numpy API (fp32 on device), and the bf16-valued cases
+  again as bf16 tensors;
+* config-1 shapes (B=1, H=4, d=128, N=4096, P=2, L=2) against the oracle on
+  the same (upcast) inputs, fp32 and bf16, causal and non-causal;
+* size-independent properties at the BASELINE sizes (N=131072 bf16 causal):
+  constant V, determinism, causal prefix consistency, sequence sharding.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_04008_b200 as rb
+from conftest import grad_errs, load_golden, rel_err
+from oracle import race_oracle as ro
+from paper_2510_04008_b200 import _lib
+from paper_2510_04008_b200.sharded import sharded_backward, sharded_forward
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-3
+TOL_BF16 = 1e-2
+GRAD_FLOOR = 0.05
+
+CASES = load_golden()
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda")
+
+
+def _is_bf16_valued(a):
+    f = np.asarray(a, dtype=np.float32)
+    return np.array_equal(f.view(np.uint32) & 0xFFFF, np.zeros_like(f.view(np.uint32)))
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['index']:03d}-{c['tag']}")
+def test_golden_fp32(case):
+    _cuda()
+    cfg = rb.SketchConfig(**case.cfg_kwargs)
+    inp = rb.AttnInputs(case["q"], case["k"], case["v"])
+    if cfg.hyperplanes > 10:
+        with pytest.raises(_lib.RaceUnsupported):
+            rb.race_attention(inp, cfg)
+        return
+    out = rb.race_attention(inp, cfg)
+    assert out.o.dtype == np.float64 and out.den.dtype == np.float64
+    assert rel_err(out.o, case["o"]) <= TOL_F32
+    assert rel_err(out.den, case["den"]) <= TOL_F32
+    flags = np.zeros(inp.n, dtype=bool)
+    flags[list(out.degenerate_rows)] = True
+    assert np.array_equal(flags, case["degenerate"])
+    g = rb.race_attention_vjp(inp, cfg, case["d_out"])
+    errs = grad_errs((g.dq, g.dk, g.dv), (case["dq"], case["dk"], case["dv"]), GRAD_FLOOR)
+    assert max(errs) <= TOL_F32, errs
+
+
+BF16_CASES = [c for c in CASES if all(_is_bf16_valued(c[x]) for x in ("q", "k", "v", "d_out"))
+              and int(c["P"]) <= 10]
+
+
+@pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"{c['index']:03d}-{c['tag']}")
+def test_golden_bf16(case):
+    dev = _cuda()
+    cfg = rb.SketchConfig(**case.cfg_kwargs)
+    t = {x: torch.from_numpy(case[x].astype(np.float32)).to(dev, torch.bfloat16) for x in ("q", "k", "v", "d_out")}
+    inp = rb.AttnInputs(t["q"], t["k"], t["v"])
+    out = rb.race_attention(inp, cfg)
+    assert out.o.dtype == torch.bfloat16
+    assert rel_err(out.o.float().cpu(), case["o"]) <= TOL_BF16
+    assert rel_err(out.den.cpu(), case["den"]) <= TOL_F32  # den is kept in fp32
+    g = rb.race_attention_vjp(inp, cfg, t["d_out"])
+    errs = grad_errs([x.float().cpu().numpy() for x in (g.dq, g.dk, g.dv)],
+                     (case["dq"], case["dk"], case["dv"]), GRAD_FLOOR)
+    assert max(errs) <= TOL_BF16, errs
+
+
+# ---------------------------------------------------------------------------
+# config-1 shapes vs the oracle on identical inputs
+# ---------------------------------------------------------------------------
+def _layer_inputs(n, d, heads, dtype, seed=0):
+    per_head = ro.head_inputs(seed, n, d, heads, np.float32)
+    dev = _cuda()
+    stack = [np.stack([h[i] for h in per_head])[None] for i in range(4)]  # [1, H, N, d]
+    q, k, v, g = (torch.from_numpy(a).to(dev, dtype) for a in stack)
+    return q, k, v, g
+
+
+def _oracle_layer(q, k, v, g, w, beta, causal):
+    """Per-head oracle in float64 on the device's exact input values."""
+    outs = []
+    for h in range(q.shape[1]):
+        qh, kh, vh, gh = (t[0, h].double().cpu().numpy() for t in (q, k, v, g))
+        wh = w[h].double().cpu().numpy()
+        o, den, _ = ro.forward(qh, kh, vh, wh, beta, causal)
+        dq, dk, dv = ro.vjp(qh, kh, vh, wh, beta, gh, causal)
+        outs.append((o, den, dq, dk, dv))
+    return outs
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("n", [4096, 1000])
+def test_config1_layer(dtype, causal, n):
+    q, k, v, g = _layer_inputs(n, 128, 4, dtype)
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=0, causal=causal)
+    layer = rb.RaceAttention(4, 128, cfg).to(q.device)
+    p = layer.params_
+    o, den, state = rb.race_forward(q, k, v, layer.w, p)
+    dq, dk, dv = rb.race_backward(q, k, v, layer.w, g, p, state=state)
+    ref = _oracle_layer(q, k, v, g, layer.w, cfg.beta, causal)
+    tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+    for h, (o_r, den_r, dq_r, dk_r, dv_r) in enumerate(ref):
+        assert rel_err(o[0, h].float().cpu(), o_r) <= tol
+        assert rel_err(den[0, h].cpu(), den_r) <= TOL_F32
+        errs = grad_errs([t[0, h].float().cpu().numpy() for t in (dq, dk, dv)], (dq_r, dk_r, dv_r), GRAD_FLOOR)
+        assert max(errs) <= tol, (h, errs)
+    # backward without saved state (reference-style recompute) is bit-identical
+    dq2, dk2, dv2 = rb.race_backward(q, k, v, layer.w, g, p, state=None)
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+
+
+def test_autograd_matches_vjp():
+    q, k, v, g = _layer_inputs(777, 64, 2, torch.float32, seed=3)
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=9, causal=True)
+    layer = rb.RaceAttention(2, 64, cfg).to(q.device)
+    qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
+    o = layer(qq, kk, vv)
+    (o * g).sum().backward()
+    dq, dk, dv = rb.race_backward(q, k, v, layer.w, g, layer.params_)
+    assert torch.equal(qq.grad, dq) and torch.equal(kk.grad, dk) and torch.equal(vv.grad, dv)
+
+
+# ---------------------------------------------------------------------------
+# properties at the BASELINE size (config 2: causal N=131072 bf16, H=4)
+# ---------------------------------------------------------------------------
+def _big(n=131072, dtype=torch.bfloat16, causal=True, seed=1):
+    dev = _cuda()
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    shape = (1, 4, n, 128)
+    q, k, v, g = (torch.randn(shape, generator=gen, device=dev).to(dtype) for _ in range(4))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=0, causal=causal)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(dev)
+    return q, k, v, g, w, cfg.params()
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+def test_constant_values_give_constant_output(causal):
+    q, k, v, g, w, p = _big(causal=causal)
+    c = torch.randn(128, device=q.device).to(torch.bfloat16)
+    vc = c.expand_as(v).contiguous()
+    o, den, _ = rb.race_forward(q, k, vc, w, p, want_state=False)
+    assert rel_err(o.float().cpu(), c.float().expand_as(o).cpu()) <= 1e-2
+    assert bool((den > 0).all())
+
+
+def test_determinism_bitwise():
+    q, k, v, g, w, p = _big()
+    a = rb.race_forward(q, k, v, w, p)
+    b = rb.race_forward(q, k, v, w, p)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    ga = rb.race_backward(q, k, v, w, g, p, a[2])
+    gb = rb.race_backward(q, k, v, w, g, p, b[2])
+    assert all(torch.equal(x, y) for x, y in zip(ga, gb))
+
+
+def test_causal_prefix_consistency():
+    """Criterion 2 (ra/acceptance.py:167-196): causal row t == non-causal on keys 0..t."""
+    q, k, v, g, w, p = _big(n=20000, dtype=torch.float32)
+    o, _, _ = rb.race_forward(q, k, v, w, p, want_state=False)
+    pn = rb.SketchParams(p.hyperplanes, p.tables, p.beta, False)
+    for t in (0, 1, 127, 128, 4095, 12345, 19999):
+        on, _, _ = rb.race_forward(q[:, :, :t + 1], k[:, :, :t + 1], v[:, :, :t + 1], w, pn, want_state=False)
+        assert rel_err(o[0, :, t].cpu(), on[0, :, t].cpu()) <= TOL_F32, t
+
+
+def test_mass_conservation():
+    """Criterion 8 (ra/acceptance.py:383-416): column dv of S sums to N*T; colsum of B = T*colsum V."""
+    q, k, v, g, w, p = _big(n=65536, dtype=torch.float32, causal=False)
+    _, _, state = rb.race_forward(q, k, v, w, p)
+    s = state.double()
+    n = q.shape[2]
+    assert torch.allclose(s[..., -1].sum(-1), torch.full((4,), float(n * p.tables), dtype=torch.float64,
+                                                          device=s.device), rtol=1e-5)
+    colsum = s[..., :-1].sum(1)
+    assert rel_err(colsum.cpu(), (p.tables * v[0].double().sum(1)).cpu()) <= 1e-4
+
+
+class _EmuComm:
+    """Single-process stand-in for torch.distributed: rank `r` of `world`."""
+
+    def __init__(self, rank, totals, record):
+        self.rank, self.totals, self.record = rank, totals, record
+
+    def allreduce(self, local):
+        self.record.append(local.clone())
+        return sum(self.totals) if self.totals else local.clone()
+
+    def carry(self, local, direction):
+        self.record.append(local.clone())
+        if not self.totals:
+            return torch.zeros_like(local)
+        idx = range(self.rank) if direction == "prefix" else range(len(self.totals) - 1, self.rank, -1)
+        out = torch.zeros_like(local)
+        for r in idx:
+            out += self.totals[r]
+        return out
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+def test_sequence_sharding_matches_single_gpu(causal):
+    """Split-phase C-ABI + exchange algebra with 3 emulated ranks."""
+    q, k, v, g, w, p = _big(n=50000, dtype=torch.float32, causal=causal)
+    o1, den1, st1 = rb.race_forward(q, k, v, w, p)
+    dq1, dk1, dv1 = rb.race_backward(q, k, v, w, g, p, st1)
+    world = 3
+    bounds = [rb.shard_bounds(q.shape[2], world, r) for r in range(world)]
+    sl = [(q[:, :, a:b], k[:, :, a:b], v[:, :, a:b], g[:, :, a:b]) for a, b in bounds]
+    # pass 1: record local totals; pass 2: run with the true exchange
+    rec = [[] for _ in range(world)]
+    for r in range(world):
+        sharded_forward(*sl[r][:3], w, p, comm=_EmuComm(r, None, rec[r]))
+    totals = [rec[r][0] for r in range(world)]
+    outs = [sharded_forward(*sl[r][:3], w, p, comm=_EmuComm(r, totals, [])) for r in range(world)]
+    o = torch.cat([x[0] for x in outs], dim=2)
+    den = torch.cat([x[1] for x in outs], dim=2)
+    assert rel_err(o.cpu(), o1.cpu()) <= TOL_F32 and rel_err(den.cpu(), den1.cpu()) <= TOL_F32
+    rec = [[] for _ in range(world)]
+    for r in range(world):
+        sharded_backward(*sl[r], w, p, outs[r][2], comm=_EmuComm(r, None, rec[r]))
+    dtot = [rec[r][0] for r in range(world)]
+    grads = [sharded_backward(*sl[r], w, p, outs[r][2], comm=_EmuComm(r, dtot, [])) for r in range(world)]
+    for i, ref in enumerate((dq1, dk1, dv1)):
+        got = torch.cat([x[i] for x in grads], dim=2)
+        assert rel_err(got.cpu(), ref.cpu()) <= TOL_F32, i
+
+
+def test_n1_output_is_v_and_empty():
+    dev = _cuda()
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2)
+    v = np.random.default_rng(0).standard_normal((1, 16)).astype(np.float32)
+    out = rb.race_attention(rb.AttnInputs(v[:, :8], v[:, 8:], v), cfg)
+    assert np.allclose(out.o, v, rtol=1e-6, atol=1e-6)
+    e = np.zeros((0, 8), np.float32)
+    out = rb.race_attention(rb.AttnInputs(e, e, e), cfg)
+    assert out.o.shape == (0, 8) and out.degenerate_rows == ()
+    assert dev.type == "cuda"
+
+
+def test_bad_d_out_raises():
+    _cuda()
+    rng = np.random.default_rng(0)
+    inp = rb.AttnInputs(*(rng.standard_normal((8, 4)) for _ in range(3)))
+    with pytest.raises(ValueError):
+        rb.race_attention_vjp(inp, rb.SketchConfig(hyperplanes=2, tables=2), np.ones((8, 3)))
+
+
+def test_workers_invariance():
+    """Criterion 9: identical results for any `workers` value."""
+    _cuda()
+    rng = np.random.default_rng(19)
+    inp = rb.AttnInputs(*(rng.standard_normal((33, 6)) for _ in range(2)), rng.standard_normal((33, 5)))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=3, ensembles=2, seed=777, causal=True)
+    a, b = rb.race_attention(inp, cfg), rb.race_attention(inp, cfg, workers=4)
+    assert np.array_equal(a.o, b.o) and np.array_equal(a.den, b.den)
