@@ -240,9 +240,11 @@ def test_sequence_sharding_matches_single_gpu(causal):
     assert rel_err(o.cpu(), o1.cpu()) <= TOL_F32 and rel_err(den.cpu(), den1.cpu()) <= TOL_F32
     rec = [[] for _ in range(world)]
     for r in range(world):
-        sharded_backward(*sl[r], w, p, outs[r][2], comm=_EmuComm(r, None, rec[r]))
+        q_, k_, v_, g_ = sl[r]
+        sharded_backward(q_, k_, v_, w, g_, p, outs[r][2], comm=_EmuComm(r, None, rec[r]))
     dtot = [rec[r][0] for r in range(world)]
-    grads = [sharded_backward(*sl[r], w, p, outs[r][2], comm=_EmuComm(r, dtot, [])) for r in range(world)]
+    grads = [sharded_backward(sl[r][0], sl[r][1], sl[r][2], w, sl[r][3], p, outs[r][2], comm=_EmuComm(r, dtot, []))
+             for r in range(world)]
     for i, ref in enumerate((dq1, dk1, dv1)):
         got = torch.cat([x[i] for x in grads], dim=2)
         assert rel_err(got.cpu(), ref.cpu()) <= TOL_F32, i
