@@ -1,0 +1,118 @@
+// tc_selftest.cu -- on-device check of the UMMA operand layouts / descriptors
+// used by the fast path (built as a separate diagnostic library,
+// libtc_selftest.so, exercised by tests/test_tc_selftest.py).
+//
+// One CTA: A [M x K] and B [N x K] (row-major bf16 in global memory) are
+// written into shared memory in the canonical layout selected by
+// (major, swizzle), one tcgen05.mma chain computes D = A B^T into TMEM, and
+// D is read back with tcgen05.ld.  The host compares with torch.
+#include <cstdio>
+
+#include "tc_common.cuh"
+
+using namespace race::tc;
+
+namespace {
+
+__device__ uint32_t swz_rt(uint32_t off, int sw_bytes) {
+  const uint32_t mask = sw_bytes == 128 ? 7 : sw_bytes == 64 ? 3 : sw_bytes == 32 ? 1 : 0;
+  return off ^ (((off >> 7) & mask) << 4);
+}
+
+// byte offset of element (mn, k) of an [MN x K] operand tile
+__device__ uint32_t canon_off(int mn, int k, int MN, int K, int mn_major, int sw) {
+  if (!mn_major) {
+    const int per_row = sw / 2;  // elements of K per swizzle row
+    const int blk = k / per_row, kin = k % per_row;
+    const uint32_t off = uint32_t(blk) * MN * sw + uint32_t(mn / 8) * (8 * sw) + (mn % 8) * sw + kin * 2;
+    return swz_rt(off, sw);
+  }
+  const int per_row = sw / 2;  // elements of MN per swizzle row
+  const int blk = mn / per_row, mnin = mn % per_row;
+  const uint32_t off = uint32_t(blk) * K * sw + uint32_t(k / 8) * (8 * sw) + (k % 8) * sw + mnin * 2;
+  return swz_rt(off, sw);
+}
+
+__device__ uint64_t operand_desc(uint32_t base, int kk, int MN, int K, int mn_major, int sw) {
+  const uint32_t layout = sw == 128 ? kSw128 : sw == 64 ? kSw64 : kSw32;
+  if (!mn_major) {
+    const int per_row = sw / 2;
+    const int k0 = kk * 16;
+    const uint32_t start = base + uint32_t(k0 / per_row) * MN * sw + (k0 % per_row) * 2;
+    return smem_desc(start, 16, 8 * sw, layout);
+  }
+  const uint32_t start = base + uint32_t(kk) * 2 * (8 * sw);
+  return smem_desc(start, uint32_t(K) * sw, 8 * sw, layout);
+}
+
+__global__ void __launch_bounds__(128) k_selftest(int M, int N, int K, int a_mn, int b_mn, int a_sw, int b_sw,
+                                                  const __nv_bfloat16* __restrict__ A,
+                                                  const __nv_bfloat16* __restrict__ B, float* __restrict__ D) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sa = smem;                    // up to 32 KB
+  uint8_t* sb = smem + 32768;            // up to 32 KB
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int i = tid; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  for (int i = tid; i < M * K; i += 128) {
+    const int m = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sa + canon_off(m, k, M, K, a_mn, a_sw)) = A[i];
+  }
+  for (int i = tid; i < N * K; i += 128) {
+    const int n = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sb + canon_off(n, k, N, K, b_mn, b_sw)) = B[i];
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tslot);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16(M, N, a_mn, b_mn);
+    for (int kk = 0; kk < K / 16; ++kk) {
+      umma_bf16(tmem, operand_desc(smem_u32(sa), kk, M, K, a_mn, a_sw), operand_desc(smem_u32(sb), kk, N, K, b_mn, b_sw),
+                idesc, kk > 0);
+    }
+    umma_commit(bar);
+  }
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + (tid & 31);
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+    tmem_ld_wait();
+    if (row < M)
+      for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+}  // namespace
+
+extern "C" int tc_selftest_gemm(int M, int N, int K, int a_mn, int b_mn, int a_sw, int b_sw, const void* A,
+                                const void* B, float* D, void* stream) {
+  if (M != 128 || N % 16 || N < 16 || N > 256 || K % 16 || K > 128) return 1;
+  if (M * K * 2 > 32768 || N * K * 2 > 32768) return 1;
+  const size_t smem = 65536 + 128;
+  cudaFuncSetAttribute(k_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_selftest<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(M, N, K, a_mn, b_mn, a_sw, b_sw,
+                                                                 static_cast<const __nv_bfloat16*>(A),
+                                                                 static_cast<const __nv_bfloat16*>(B), D);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "tc_selftest launch: %s\n", cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}

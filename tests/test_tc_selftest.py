@@ -1,0 +1,53 @@
+"""Device check of the tcgen05 operand layouts the fast path relies on.
+
+libtc_selftest.so builds each canonical UMMA layout (K-/MN-major, SW128 /
+SW64 / SW32) in shared memory, runs one tcgen05.mma chain and reads D back
+from TMEM; the result must equal A @ B^T (bf16 products are exact in fp32).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import pytest
+import torch
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+LIB = os.path.join(ROOT, "paper_2510_04008_b200", "libtc_selftest.so")
+
+# (N, K, a_mn, b_mn, a_sw, b_sw): the operand pairings of the fast-path kernels
+COMBOS = [
+    (16, 128, 0, 0, 128, 128),   # projection: X tile (TMA SW128) x W' (K-major)
+    (32, 128, 1, 1, 128, 64),    # state update: V^T (MN-major) x Phi (MN-major SW64)
+    (128, 32, 0, 0, 64, 64),     # Phi_q Phi_k^T and Phi_q x S-operand
+    (128, 128, 0, 1, 128, 128),  # P~ x V (B MN-major SW128)
+    (128, 16, 0, 1, 32, 128),    # dproj x W (bwd)
+    (128, 128, 0, 0, 128, 128),  # dO V^T (bwd)
+    (32, 128, 1, 1, 128, 128),   # dO^T x Phi~ with Phi in SW128 rows
+    (64, 64, 1, 0, 128, 128),
+]
+
+
+@pytest.mark.parametrize("combo", COMBOS, ids=lambda c: "N%d_K%d_a%s%d_b%s%d" % (
+    c[0], c[1], "MN" if c[2] else "K", c[4], "MN" if c[3] else "K", c[5]))
+def test_umma_layouts(combo):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    n, k, a_mn, b_mn, a_sw, b_sw = combo
+    lib = ctypes.CDLL(LIB)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(n * 1000 + k)
+    a = torch.randn(128, k, generator=g, device=dev).to(torch.bfloat16)
+    b = torch.randn(n, k, generator=g, device=dev).to(torch.bfloat16)
+    d = torch.full((128, n), float("nan"), device=dev)
+    rc = lib.tc_selftest_gemm(128, n, k, a_mn, b_mn, a_sw, b_sw, ctypes.c_void_p(a.data_ptr()),
+                              ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(d.data_ptr()),
+                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = a.double() @ b.double().T
+    err = (d.double() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
