@@ -20,6 +20,8 @@ bool tc_supported(const Geo& g);
 cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st);
 cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
                        cudaStream_t st);
+cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
+                          const float* car, void* o, float* den, cudaStream_t st);
 }  // namespace race
 
 namespace race {
@@ -206,6 +208,8 @@ int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k, const
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, S(stream)), "tc_causal_fwd");
   return cuda_status(race::simt_causal_fwd(g, q, k, v, w, carries, o, den, S(stream)), "causal_fwd");
 }
 

@@ -1,12 +1,982 @@
-// race_tc.cu -- sm_100a tcgen05/TMA fast path (placeholder until implemented).
+// race_tc.cu -- sm_100a fast path: persistent, warp-specialised kernels with
+// TMA loads/stores, tcgen05 MMAs accumulating in TMEM, and the soft-LSH
+// features computed in registers (the N x F assignment never reaches HBM).
+//
+// Scope: bf16 inputs, d = dv = 128, F = T * 2^P <= 8 (the reference default
+// P=2, L=2 is F=8), any N and B*H.  Everything else runs on the generic
+// kernels in race_simt.cu.
+//
+// CTA = 6 warps: warp 0 TMA producer, warp 1 MMA issuer (+ TMEM owner),
+// warps 2..5 compute (thread r <-> token r of the 128-token chunk <-> TMEM
+// lane r).  Work items are (b*h, segment) pairs (race_segments), taken
+// round-robin by a persistent grid of one CTA per SM.
+//
+// Precision: the projection x.W must be fp32-exact, so W
+// enters the MMA as three bf16 pieces (W_hi + W_mid + W_lo = W to 24 bits;
+// bf16 x bf16 products are exact in fp32).  phi and the bucket tables enter
+// as hi/lo bf16 pairs (16-bit mantissa); only the causal intra-chunk matrix
+// tril(Phi_q Phi_k^T) is rounded to bf16 before multiplying V.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "race_common.cuh"
 #include "race_internal.h"
+#include "tc_common.cuh"
 
 namespace race {
-bool tc_supported(const Geo&) { return false; }
-cudaError_t tc_aggregate(const Geo&, const void*, const void*, const float*, float*, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace tcfast {
+
+using namespace tc;
+
+constexpr int CH = 128;              // tokens per chunk (= MMA M)
+constexpr int DH = 128;              // d = dv
+constexpr int SUB = CH * 64 * 2;     // one [128 x 64] bf16 SW128 sub-tile (16 KB)
+constexpr int TILE = 2 * SUB;        // [128 x 128] bf16 tile (32 KB)
+constexpr int WOP = 2 * 16 * 128;    // W' operand: [16 x 128] bf16, 2 SW128 sub-tiles of 2 KB
+constexpr int PHI = CH * 64;         // [128 x 32] bf16 K-major SW64 (8 KB)
+constexpr int NTHREADS = 192;
+constexpr int FP = 8;                // padded feature count
+constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
+
+// TMEM column map
+constexpr uint32_t TM_PROJQ = 0, TM_PROJK = 16, TM_SACC = 32, TM_PM = 64, TM_NUM = 256;
+
+struct Args {
+  int64_t BH, H, N, nseg, seg_tokens;
+  int P, T, TP;
+  float beta;
+  int normalize, w_per_head;
+  const float* w;
+  const float* tin;   // tables / carries
+  float* tout;        // partial tables
+  float* den;
+};
+
+// ---------------------------------------------------------------------------
+// role helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int crow() { return ((warp_id() & 3) << 5) | lane_id(); }       // compute row
+__device__ __forceinline__ uint32_t lane_base() { return uint32_t((warp_id() & 3) * 32) << 16; }
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
+  return pred != 0;
 }
-cudaError_t tc_readout(const Geo&, const void*, const float*, const float*, void*, float*, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+struct Item {
+  int64_t bh, seg, t0, t1;  // tokens [t0, t1) of sequence bh
+};
+__device__ __forceinline__ Item item_of(const Args& a, int64_t it) {
+  Item r;
+  r.bh = it / a.nseg;
+  r.seg = it % a.nseg;
+  r.t0 = r.seg * a.seg_tokens;
+  r.t1 = r.t0 + a.seg_tokens < a.N ? r.t0 + a.seg_tokens : a.N;
+  return r;
 }
+
+// operand descriptors ------------------------------------------------------
+// [128 x 128] bf16 tile from TMA (two SW128 sub-tiles), K-major, K-step kk of 16
+__device__ __forceinline__ uint64_t desc_tile_k(uint32_t base, int kk) {
+  return smem_desc(base + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024, kSw128);
+}
+// same tile used MN-major (rows = K = tokens, 128 MN = 2 sub-tiles at LBO = SUB)
+__device__ __forceinline__ uint64_t desc_tile_mn(uint32_t base, int kk) {
+  return smem_desc(base + kk * 2048, SUB, 1024, kSw128);
+}
+// W' [16 x 128] K-major SW128 (sub-tiles of 16 rows x 128 B)
+__device__ __forceinline__ uint64_t desc_w(uint32_t base, int kk) {
+  return smem_desc(base + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024, kSw128);
+}
+// [128 x 32] K-major SW64 (Phi / S operand), K-step kk in {0, 1}
+__device__ __forceinline__ uint64_t desc_phi_k(uint32_t base, int kk) {
+  return smem_desc(base + kk * 32, 16, 512, kSw64);
+}
+// same buffer used MN-major: N = 32 columns, K = 128 tokens
+__device__ __forceinline__ uint64_t desc_phi_mn(uint32_t base, int kk) {
+  return smem_desc(base + kk * 1024, 8192, 512, kSw64);
+}
+
+constexpr uint32_t ID_PROJ = idesc_bf16(128, 16, 0, 0);
+constexpr uint32_t ID_PM = idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t ID_STATE = idesc_bf16(128, 32, 1, 1);
+constexpr uint32_t ID_NUMA = idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t ID_NUMB = idesc_bf16(128, 128, 0, 1);
+
+// ---------------------------------------------------------------------------
+// compute-thread building blocks
+// ---------------------------------------------------------------------------
+// sum of squares of row r of a [128 x 128] SW128 tile
+__device__ __forceinline__ float tile_row_sumsq(uint32_t tile, int r) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint4 v = ld_shared_v4(tile + h * SUB + r * 128 + ((j ^ (r & 7)) << 4));
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float a = bf16_lo(w4[q]), b = bf16_hi(w4[q]);
+        s0 = fmaf(a, a, s0);
+        s1 = fmaf(b, b, s1);
+      }
+    }
+  }
+  return s0 + s1;
+}
+
+// per-row inverse scale (1/||x|| or 1 for pass-through / unnormalised rows)
+__device__ __forceinline__ float inv_scale(float sumsq, int normalize) {
+  if (!normalize) return 1.f;
+  const float nrm = sqrtf(sumsq);
+  return nrm < kZeroRowEps ? 1.f : 1.f / nrm;
+}
+
+// W' rows 3j, 3j+1, 3j+2 = W_hi[j], W_mid[j], W_lo[j] (W to 24 bits), K-major SW128
+__device__ void build_wop(const Args& a, int64_t bh, uint32_t wop) {
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  for (int idx = threadIdx.x - 64; idx < 16 * 16; idx += 128) {
+    const int n = idx >> 4, j = idx & 15;  // row n, 8-element chunk j
+    const int hp = n / 3, piece = n % 3;
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v = 0.f;
+        if (hp < a.TP) {
+          const float x = w[hp * DH + j * 8 + e * 2 + h];
+          const float hi = bf16_round(x);
+          const float mid = bf16_round(x - hi);
+          v = piece == 0 ? hi : piece == 1 ? mid : bf16_round(x - hi - mid);
+        }
+        v2[h] = v;
+      }
+      pk[e] = pack_bf16(v2[0], v2[1]);
+    }
+    const uint32_t off = (j >> 3) * 2048 + n * 128 + (((j & 7) ^ (n & 7)) << 4);
+    st_shared_v4(wop + off, pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// features of one row from its 16 projection columns (P compile-time, T <= 8 >> P)
+template <int P>
+__device__ __forceinline__ void row_features(const Args& a, const float* proj, float inv, bool valid, float* phi) {
+  constexpr int R = 1 << P;
+  constexpr int TMAX = FP / R;
+#pragma unroll
+  for (int f = 0; f < FP; ++f) phi[f] = 0.f;
+#pragma unroll
+  for (int tau = 0; tau < TMAX; ++tau) {
+    if (tau < a.T && valid) {
+      float e[P], z = 1.f;
+      bool neg[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int j = tau * P + p;
+        const float u = tanhf((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
+        e[p] = expf(-2.f * a.beta * fabsf(u));
+        neg[p] = u < 0.f;
+        z *= 1.f + e[p];
+      }
+      const float rz = 1.f / z;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float prod = rz;
+#pragma unroll
+        for (int p = 0; p < P; ++p) prod *= (((rr >> p) & 1) == int(neg[p])) ? 1.f : e[p];
+        phi[tau * R + rr] = prod;
+      }
+    }
+  }
+}
+
+// row r of a [128 x 32] SW64 operand: four 8-element bf16 blocks
+__device__ __forceinline__ void write_row32(uint32_t buf, int r, const uint32_t (*blk)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+    st_shared_v4(buf + off, blk[j][0], blk[j][1], blk[j][2], blk[j][3]);
+  }
+}
+__device__ __forceinline__ void split8(const float* x, uint32_t* hi, uint32_t* lo) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float h0 = bf16_round(x[2 * e]), h1 = bf16_round(x[2 * e + 1]);
+    hi[e] = pack_bf16(h0, h1);
+    lo[e] = pack_bf16(x[2 * e] - h0, x[2 * e + 1] - h1);
+  }
+}
+// Phi_q row: [hi | lo | hi | 0];  Phi_k row: [hi | hi | lo | 0]  => Pq.Pk = qh kh + ql kh + qh kl
+__device__ __forceinline__ void write_phi_q(uint32_t buf, int r, const float* phi) {
+  uint32_t b[4][4];
+  split8(phi, b[0], b[1]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[2][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, r, b);
+}
+__device__ __forceinline__ void write_phi_k(uint32_t buf, int r, const float* phi) {
+  uint32_t b[4][4];
+  split8(phi, b[0], b[2]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[1][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, r, b);
+}
+// S operand row c (B of num = Phi_q S): [S_hi | S_hi | S_lo | 0] over f
+__device__ __forceinline__ void write_sop(uint32_t buf, int c, const float* s) {
+  uint32_t b[4][4];
+  split8(s, b[0], b[2]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[1][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, c, b);
+}
+
+// block-wide sum of 8 values over the 128 compute threads, fixed order
+__device__ __forceinline__ void csum8(float* v, float* scratch) {
+#pragma unroll
+  for (int f = 0; f < FP; ++f) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
+  }
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int f = 0; f < FP; ++f) scratch[(warp_id() & 3) * FP + f] = v[f];
+  }
+  compute_bar();
+#pragma unroll
+  for (int f = 0; f < FP; ++f) v[f] = ((scratch[f] + scratch[FP + f]) + scratch[2 * FP + f]) + scratch[3 * FP + f];
+  compute_bar();
+}
+
+// write one [128 x 128] fp32 row (from TMEM) as bf16 into a SW128 staging tile
+__device__ __forceinline__ void stage_row_bf16(uint32_t tile, int r, const float* v, int c0) {
+  // v holds columns [c0, c0 + 32)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int chunk = (c0 >> 3) + j;  // 8-element chunk index 0..15
+    const uint32_t off = (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
+    st_shared_v4(tile + off, pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                 pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+  }
+}
+
+// ===========================================================================
+// K1: key-side aggregation per segment (non-causal tables / causal segment totals)
+// ===========================================================================
+namespace agg {
+constexpr int STAGES = 3;
+constexpr int STAGE_BYTES = 2 * TILE;  // K, V
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_W = STAGES * STAGE_BYTES;
+constexpr int OFF_PHI = OFF_W + WOP;         // 2 buffers
+constexpr int OFF_BAR = OFF_PHI + 2 * PHI;
+constexpr int SMEM = OFF_BAR + 256 + 1024;   // + alignment slack
+}  // namespace agg
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_aggregate(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+  using namespace agg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;               // [STAGES]
+  uint64_t* empty = bars + STAGES;     // [STAGES]
+  uint64_t* proj_full = bars + 2 * STAGES;
+  uint64_t* phi_full = proj_full + 1;
+  uint64_t* phi_empty = phi_full + 1;  // [2]
+  uint64_t* wready = phi_empty + 2;
+  uint64_t* acc_full = wready + 1;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  float* scratch = reinterpret_cast<float*>(tslot + 4);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 128);
+    mbar_init(&phi_empty[0], 1);
+    mbar_init(&phi_empty[1], 1);
+    mbar_init(wready, 128);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<64>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t nitems = a.BH * a.nseg;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      const uint64_t pol = policy_evict_first();
+      uint32_t gc = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item m = item_of(a, it);
+        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+          const int s = gc % STAGES;
+          const uint32_t u = gc / STAGES;
+          mbar_wait(&empty[s], (u & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+          for (int h = 0; h < 2; ++h) {
+            tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, int(t), int(m.bh), pol);
+            tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, int(t), int(m.bh), pol);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      mbar_wait(wready, ni & 1);
+      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
+      tc_fence_after();
+      bool first = true;
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_commit(proj_full);
+        }
+        __syncwarp();
+        mbar_wait(phi_full, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + TILE, kk), desc_phi_mn(phib, kk), ID_STATE,
+                      (!first || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+          umma_commit(&phi_empty[gc & 1]);
+          if (t + CH >= m.t1) umma_commit(acc_full);
+        }
+        __syncwarp();
+        first = false;
+      }
+    }
+  } else {
+    // ------------------------------ compute warps
+    const int r = crow();
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      build_wop(a, m.bh, sb + OFF_W);
+      fence_proxy_async();
+      mbar_arrive(wready);
+      float asum[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) asum[f] = 0.f;
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
+        mbar_wait(proj_full, gc & 1);
+        tc_fence_after();
+        float proj[16];
+        tmem_ld16(tmem + lane_base() + TM_PROJK, proj);
+        tmem_ld_wait();
+        float phi[FP];
+        row_features<P>(a, proj, inv, t + r < m.t1, phi);
+#pragma unroll
+        for (int f = 0; f < FP; ++f) asum[f] += phi[f];
+        if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
+        write_phi_k(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+      }
+      // item done: read S^T (lane r = value column r) and write the partial table
+      mbar_wait(acc_full, ni & 1);
+      tc_fence_after();
+      float acc[32];
+      tmem_ld32(tmem + lane_base() + TM_SACC, acc);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      csum8(asum, scratch);
+      const int F = a.T << a.P;
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+      if (r < F) out[r * LDS_T + DH] = asum[r];
+      // bump past the phi_empty phases consumed by this item's last chunks (tracked via gc)
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<64>(tmem);
+}
+
+// ===========================================================================
+// K2: non-causal query-side readout  O = Phi_q S_v / (Phi_q A), den = D / T
+// ===========================================================================
+namespace rdo {
+constexpr int STAGES = 3;
+constexpr int STAGE_BYTES = TILE;  // Q, reused as O staging
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_W = STAGES * STAGE_BYTES;
+constexpr int OFF_PHI = OFF_W + WOP;   // 2 buffers
+constexpr int OFF_SOP = OFF_PHI + 2 * PHI;
+constexpr int OFF_BAR = OFF_SOP + PHI;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+}  // namespace rdo
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_readout(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
+  using namespace rdo;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* proj_full = bars + 2 * STAGES;
+  uint64_t* phi_full = proj_full + 1;
+  uint64_t* phi_empty = phi_full + 1;  // [2]
+  uint64_t* wready = phi_empty + 2;
+  uint64_t* num_full = wready + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(num_full + 1);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 128);
+    mbar_init(&phi_empty[0], 1);
+    mbar_init(&phi_empty[1], 1);
+    mbar_init(wready, 128);
+    mbar_init(num_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t nitems = a.BH * a.nseg;
+  constexpr uint32_t TM_NUM_R = 128;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmO);
+      const uint64_t pol = policy_evict_first();
+      uint32_t gc = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item m = item_of(a, it);
+        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+          const int s = gc % STAGES;
+          mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, int(t), int(m.bh), pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      mbar_wait(wready, ni & 1);
+      tc_fence_after();
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_commit(proj_full);
+        }
+        __syncwarp();
+        mbar_wait(phi_full, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_NUM_R, desc_phi_k(phib, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
+          umma_commit(num_full);
+          umma_commit(&phi_empty[gc & 1]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int r = crow();
+    const float invT = 1.f / float(a.T);
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      const int F = a.T << a.P;
+      const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
+      // previous item's last num read is complete (program order); rebuild W' and S operand
+      build_wop(a, m.bh, sb + OFF_W);
+      float srow[FP], A[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) {
+        srow[f] = f < F ? tab[f * LDS_T + r] : 0.f;
+        A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
+      }
+      write_sop(sb + OFF_SOP, r, srow);
+      fence_proxy_async();
+      mbar_arrive(wready);
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
+        mbar_wait(proj_full, gc & 1);
+        tc_fence_after();
+        float proj[16];
+        tmem_ld16(tmem + lane_base() + TM_PROJQ, proj);
+        tmem_ld_wait();
+        const bool valid = t + r < m.t1;
+        float phi[FP];
+        row_features<P>(a, proj, inv, valid, phi);
+        float D = 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
+        if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
+        write_phi_q(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+        if (valid) a.den[m.bh * a.N + t + r] = D * invT;
+        const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+        mbar_wait(num_full, gc & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base() + TM_NUM_R + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= rD;
+          stage_row_bf16(stage, r, v, c0);  // Q tile is dead: reuse as O staging
+        }
+        tc_fence_before();
+        fence_proxy_async();
+        compute_bar();
+        if (threadIdx.x == 64) {
+          for (int h = 0; h < 2; ++h) tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + h * SUB),
+                                                  h * 64, int(t), int(m.bh));
+          tma_store_commit();
+          tma_store_wait_read<0>();
+          mbar_arrive(&empty[s]);
+        }
+      }
+    }
+    if (threadIdx.x == 64) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+// ===========================================================================
+// K3: causal forward, chunked scan with carry-in per segment
+//   num_c = Phi_q,c S_<c + tril(Phi_q,c Phi_k,c^T) V_c,   S_<c+1 = S_<c + Phi_k,c^T [V_c | 1]
+// ===========================================================================
+namespace cfw {
+constexpr int STAGES = 2;
+constexpr int STAGE_BYTES = 3 * TILE;  // Q (-> P~), K (-> O staging), V
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_W = STAGES * STAGE_BYTES;
+constexpr int OFF_PHIQ = OFF_W + WOP;
+constexpr int OFF_PHIK = OFF_PHIQ + PHI;
+constexpr int OFF_SOP = OFF_PHIK + PHI;
+constexpr int OFF_BAR = OFF_SOP + PHI;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+}  // namespace cfw
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_causal_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Args a) {
+  using namespace cfw;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;                 // [2]
+  uint64_t* empty = bars + 2;            // [2]  (MMA commit + store-read arrive)
+  uint64_t* proj_full = bars + 4;
+  uint64_t* phi_full = bars + 5;
+  uint64_t* pm_full = bars + 6;
+  uint64_t* pt_full = bars + 7;
+  uint64_t* num_full = bars + 8;
+  uint64_t* wready = bars + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+  float* scratch = reinterpret_cast<float*>(tslot + 4);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 2); }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 128);
+    mbar_init(pm_full, 1);
+    mbar_init(pt_full, 128);
+    mbar_init(num_full, 1);
+    mbar_init(wready, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t nitems = a.BH * a.nseg;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmO);
+      const uint64_t pol = policy_evict_first();
+      uint32_t gc = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item m = item_of(a, it);
+        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+          const int s = gc & 1;
+          mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+          for (int h = 0; h < 2; ++h) {
+            tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, int(t), int(m.bh), pol);
+            tma_load_3d(st + TILE + h * SUB, &tmK, &full[s], h * 64, int(t), int(m.bh), pol);
+            tma_load_3d(st + 2 * TILE + h * SUB, &tmV, &full[s], h * 64, int(t), int(m.bh), pol);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      mbar_wait(wready, ni & 1);
+      tc_fence_after();
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc & 1;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          }
+          umma_commit(proj_full);
+        }
+        __syncwarp();
+        mbar_wait(phi_full, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_PM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), ID_PM, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + 2 * TILE, kk), desc_phi_mn(sb + OFF_PHIK, kk), ID_STATE, 1u);
+          umma_commit(pm_full);
+        }
+        __syncwarp();
+        mbar_wait(pt_full, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_NUM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_NUM, desc_tile_k(stage, kk), desc_tile_mn(stage + 2 * TILE, kk), ID_NUMB, 1u);
+          umma_commit(num_full);
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int r = crow();
+    const float invT = 1.f / float(a.T);
+    const int F = a.T << a.P;
+    uint32_t gc = 0, ni = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
+      const Item m = item_of(a, it);
+      const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      build_wop(a, m.bh, sb + OFF_W);
+      float srow[FP], A[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) {
+        srow[f] = f < F ? car[f * LDS_T + r] : 0.f;
+        A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
+      }
+      // S accumulator (lane r = value column r): cols 0..7 = S_in, the rest 0
+      {
+        float z[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = j < FP ? srow[j] : 0.f;
+        tmem_st16(tmem + lane_base() + TM_SACC, z);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = 0.f;
+        tmem_st16(tmem + lane_base() + TM_SACC + 16, z);
+        tmem_st_wait();
+      }
+      write_sop(sb + OFF_SOP, r, srow);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(wready);
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc & 1;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc >> 1) & 1);
+        const float invq = inv_scale(tile_row_sumsq(stage, r), a.normalize);
+        const float invk = inv_scale(tile_row_sumsq(stage + TILE, r), a.normalize);
+        const bool valid = t + r < m.t1;
+        mbar_wait(proj_full, gc & 1);
+        tc_fence_after();
+        float pq[16], pk[16];
+        tmem_ld16(tmem + lane_base() + TM_PROJQ, pq);
+        tmem_ld16(tmem + lane_base() + TM_PROJK, pk);
+        tmem_ld_wait();
+        float phq[FP], phk[FP];
+        row_features<P>(a, pq, invq, valid, phq);
+        row_features<P>(a, pk, invk, valid, phk);
+        write_phi_q(sb + OFF_PHIQ, r, phq);
+        write_phi_k(sb + OFF_PHIK, r, phk);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+        float D = 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
+        csum8(phk, scratch);  // chunk total of phi_k (identical in every thread)
+        // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 into the dead Q tile
+        mbar_wait(pm_full, gc & 1);
+        tc_fence_after();
+        float rs = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < CH; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base() + TM_PM + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = (c0 + j <= r) ? v[j] : 0.f;
+            rs += v[j];
+          }
+          stage_row_bf16(stage, r, v, c0);
+        }
+        D += rs;
+        float sacc[32];
+        tmem_ld32(tmem + lane_base() + TM_SACC, sacc);  // S_<=c (value column r)
+        tmem_ld_wait();
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(pt_full);
+        if (valid) a.den[m.bh * a.N + t + r] = D * invT;
+        const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) A[f] += phk[f];
+        // ---- numerator -> O (staged in the dead K tile), then next chunk's S operand
+        mbar_wait(num_full, gc & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base() + TM_NUM + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= rD;
+          stage_row_bf16(stage + TILE, r, v, c0);
+        }
+        float snext[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
+        write_sop(sb + OFF_SOP, r, snext);
+        fence_proxy_async();
+        tc_fence_before();
+        compute_bar();
+        if (threadIdx.x == 64) {
+          for (int h = 0; h < 2; ++h)
+            tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + TILE + h * SUB), h * 64,
+                         int(t), int(m.bh));
+          tma_store_commit();
+          tma_store_wait_read<0>();
+          mbar_arrive(&empty[s]);
+        }
+      }
+    }
+    if (threadIdx.x == 64) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [BH, N, 128] bf16 viewed as 3-D {128, N, BH}; box {64, 128, 1}; SW128
+bool make_map(CUtensorMap* m, const void* ptr, const Geo& g) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t(DH), cuuint64_t(g.N), cuuint64_t(g.BH)};
+  cuuint64_t strides[2] = {cuuint64_t(DH) * 2, cuuint64_t(g.N) * DH * 2};
+  cuuint32_t box[3] = {64, CH, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+Args make_args(const Geo& g) {
+  Args a{};
+  a.BH = g.BH;
+  a.H = g.H;
+  a.N = g.N;
+  a.nseg = g.nseg;
+  a.seg_tokens = g.seg_tokens;
+  a.P = g.P;
+  a.T = g.T;
+  a.TP = g.T * g.P;
+  a.beta = g.beta;
+  a.normalize = g.normalize;
+  a.w_per_head = g.w_per_head;
+  return a;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+unsigned grid_for(const Geo& g) {
+  const int64_t items = g.BH * g.nseg;
+  return unsigned(items < num_sms() ? items : num_sms());
+}
+
+template <typename K, typename... Ts>
+cudaError_t launch(K kernel, int smem, unsigned grid, cudaStream_t st, Ts... args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, NTHREADS, smem, st>>>(args...);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace tcfast
+
+// ---- entry points used by race_abi.cu --------------------------------------
+bool tc_supported(const Geo& g) {
+  const char* off = getenv("RACE_DISABLE_FAST_PATH");  // read per call: tests flip it
+  if (off && off[0] == '1') return false;
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return false;
+  const int F = g.T << g.P;
+  return g.dtype == 1 && g.d == 128 && g.dv == 128 && F <= tcfast::FP && g.T * g.P <= 5 && g.P <= 3 && g.N > 0 &&
+         g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 && tcfast::encode_fn() != nullptr;
+}
+
+cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st) {
+  using namespace tcfast;
+  CUtensorMap mk, mv;
+  if (!make_map(&mk, k, g) || !make_map(&mv, v, g)) return cudaErrorInvalidValue;
+  Args a = make_args(g);
+  a.w = w;
+  a.tout = part;
+  switch (g.P) {
+    case 1: return launch(k_aggregate<1>, agg::SMEM, grid_for(g), st, mk, mv, a);
+    case 2: return launch(k_aggregate<2>, agg::SMEM, grid_for(g), st, mk, mv, a);
+    default: return launch(k_aggregate<3>, agg::SMEM, grid_for(g), st, mk, mv, a);
+  }
+}
+
+cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
+                       cudaStream_t st) {
+  using namespace tcfast;
+  CUtensorMap mq, mo;
+  if (!make_map(&mq, q, g) || !make_map(&mo, o, g)) return cudaErrorInvalidValue;
+  Args a = make_args(g);
+  a.w = w;
+  a.tin = tab;
+  a.den = den;
+  switch (g.P) {
+    case 1: return launch(k_readout<1>, rdo::SMEM, grid_for(g), st, mq, mo, a);
+    case 2: return launch(k_readout<2>, rdo::SMEM, grid_for(g), st, mq, mo, a);
+    default: return launch(k_readout<3>, rdo::SMEM, grid_for(g), st, mq, mo, a);
+  }
+}
+
+cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
+                          const float* car, void* o, float* den, cudaStream_t st) {
+  using namespace tcfast;
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mo, o, g))
+    return cudaErrorInvalidValue;
+  Args a = make_args(g);
+  a.w = w;
+  a.tin = car;
+  a.den = den;
+  switch (g.P) {
+    case 1: return launch(k_causal_fwd<1>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    case 2: return launch(k_causal_fwd<2>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    default: return launch(k_causal_fwd<3>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+  }
+}
+
 }  // namespace race

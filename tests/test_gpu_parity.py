@@ -278,3 +278,41 @@ def test_workers_invariance():
     cfg = rb.SketchConfig(hyperplanes=2, tables=3, ensembles=2, seed=777, causal=True)
     a, b = rb.race_attention(inp, cfg), rb.race_attention(inp, cfg, workers=4)
     assert np.array_equal(a.o, b.o) and np.array_equal(a.den, b.den)
+
+
+# ---------------------------------------------------------------------------
+# sm_100a fast path (tcgen05/TMA) against the generic CUDA kernels and the oracle
+# ---------------------------------------------------------------------------
+def _both_paths(fn):
+    import os
+
+    os.environ["RACE_DISABLE_FAST_PATH"] = "1"
+    try:
+        slow = fn()
+    finally:
+        os.environ.pop("RACE_DISABLE_FAST_PATH", None)
+    fast = fn()
+    return fast, slow
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("n", [128, 1000, 4096, 70000])
+@pytest.mark.parametrize("pl", [(2, 2), (1, 3), (3, 1)], ids=["P2L2", "P1L3", "P3L1"])
+def test_fast_path_forward(causal, n, pl):
+    q, k, v, g, w, p = _big(n=n, causal=causal)
+    P, L = pl
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=3, causal=causal)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(q.device)
+    p = cfg.params()
+    from paper_2510_04008_b200.functional import Problem
+
+    assert _lib.fast_path(Problem(q, k, v, w, p).desc)
+    (o_f, den_f, st_f), (o_s, den_s, st_s) = _both_paths(lambda: rb.race_forward(q, k, v, w, p))
+    assert rel_err(st_f.cpu(), st_s.cpu()) <= 1e-4
+    assert rel_err(den_f.cpu(), den_s.cpu()) <= 1e-4
+    assert rel_err(o_f.float().cpu(), o_s.float().cpu()) <= TOL_BF16
+    if n <= 4096:  # and against the oracle, head 0
+        qh, kh, vh = (t[0, 0].double().cpu().numpy() for t in (q, k, v))
+        o_r, den_r, _ = ro.forward(qh, kh, vh, w[0].double().cpu().numpy(), cfg.beta, causal)
+        assert rel_err(o_f[0, 0].float().cpu(), o_r) <= TOL_BF16
+        assert rel_err(den_f[0, 0].cpu(), den_r) <= TOL_F32
