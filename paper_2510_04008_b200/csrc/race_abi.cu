@@ -20,6 +20,10 @@ bool tc_supported(const Geo& g);
 cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st);
 cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
                        cudaStream_t st);
+cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
+                     float* dpart, cudaStream_t st);
+cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
+                     void* dv, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
                           const float* car, void* o, float* den, cudaStream_t st);
 }  // namespace race
@@ -219,6 +223,8 @@ int race_bwd_qside(const race_desc_t* desc, const void* q, const void* d_o, cons
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_bwd_q(g, q, d_o, w, tables, dq, dpart, S(stream)), "tc_bwd_qside");
   return cuda_status(race::simt_bwd_q(g, q, d_o, w, tables, dq, dpart, S(stream)), "bwd_qside");
 }
 
@@ -228,6 +234,8 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v, const 
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_bwd_k(g, k, v, w, dtables, dk, dv, S(stream)), "tc_bwd_kside");
   return cuda_status(race::simt_bwd_k(g, k, v, w, dtables, dk, dv, S(stream)), "bwd_kside");
 }
 

@@ -1,0 +1,520 @@
+// tc_fast.cuh -- shared pieces of the sm_100a fast-path kernels (race_tc.cu,
+// race_tc_bwd.cu): geometry, work items, UMMA descriptors for the fixed
+// operand layouts, and the per-row feature / VJP math of the compute warps.
+#pragma once
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "race_common.cuh"
+#include "race_internal.h"
+#include "tc_common.cuh"
+
+namespace race {
+namespace tcfast {
+
+using namespace tc;
+
+constexpr int CH = 128;              // tokens per chunk (= MMA M)
+constexpr int DH = 128;              // d = dv
+constexpr int SUB = CH * 64 * 2;     // one [128 x 64] bf16 SW128 sub-tile (16 KB)
+constexpr int TILE = 2 * SUB;        // [128 x 128] bf16 tile (32 KB)
+constexpr int WOP = 2 * 16 * 128;    // W' operand: [16 x 128] bf16, 2 SW128 sub-tiles of 2 KB
+constexpr int PHI = CH * 64;         // [128 x 32] bf16 K-major SW64 (8 KB)
+constexpr int NTHREADS = 192;
+constexpr int FP = 8;                // padded feature count
+constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
+
+// TMEM column map
+constexpr uint32_t TM_PROJQ = 0, TM_PROJK = 16, TM_SACC = 32, TM_PM = 64, TM_NUM = 256;
+
+struct Args {
+  unsigned* dbg;  // optional host-mapped progress words (RACE_DEBUG_PROGRESS=1), [grid][256]
+  int64_t BH, H, N, nseg, seg_tokens;
+  int P, T, TP;
+  float beta;
+  int normalize, w_per_head;
+  const float* w;
+  const float* tin;   // tables / carries
+  float* tout;        // partial tables
+  float* den;
+};
+
+#define RACE_DBG(a_, slot_, val_)                                                        \
+  do {                                                                                   \
+    if ((a_).dbg) *(volatile unsigned*)&(a_).dbg[blockIdx.x * 256 + (slot_)] = (val_);   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// role helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int crow() { return ((warp_id() & 3) << 5) | lane_id(); }       // compute row
+__device__ __forceinline__ uint32_t lane_base() { return uint32_t((warp_id() & 3) * 32) << 16; }
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
+struct Item {
+  int64_t bh, seg, t0, t1;  // tokens [t0, t1) of sequence bh
+};
+__device__ __forceinline__ Item item_of(const Args& a, int64_t it) {
+  Item r;
+  r.bh = it / a.nseg;
+  r.seg = it % a.nseg;
+  r.t0 = r.seg * a.seg_tokens;
+  r.t1 = r.t0 + a.seg_tokens < a.N ? r.t0 + a.seg_tokens : a.N;
+  return r;
+}
+
+// operand descriptors ------------------------------------------------------
+// [128 x 128] bf16 tile from TMA (two SW128 sub-tiles), K-major, K-step kk of 16
+__device__ __forceinline__ uint64_t desc_tile_k(uint32_t base, int kk) {
+  return smem_desc(base + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024, kSw128);
+}
+// same tile used MN-major (rows = K = tokens, 128 MN = 2 sub-tiles at LBO = SUB)
+__device__ __forceinline__ uint64_t desc_tile_mn(uint32_t base, int kk) {
+  return smem_desc(base + kk * 2048, SUB, 1024, kSw128);
+}
+// W' [16 x 128] K-major SW128 (sub-tiles of 16 rows x 128 B)
+__device__ __forceinline__ uint64_t desc_w(uint32_t base, int kk) {
+  return smem_desc(base + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024, kSw128);
+}
+// [128 x 32] K-major SW64 (Phi / S operand), K-step kk in {0, 1}
+__device__ __forceinline__ uint64_t desc_phi_k(uint32_t base, int kk) {
+  return smem_desc(base + kk * 32, 16, 512, kSw64);
+}
+// same buffer used MN-major: N = 32 columns, K = 128 tokens
+__device__ __forceinline__ uint64_t desc_phi_mn(uint32_t base, int kk) {
+  return smem_desc(base + kk * 1024, 8192, 512, kSw64);
+}
+
+constexpr uint32_t ID_PROJ = idesc_bf16(128, 16, 0, 0);
+constexpr uint32_t ID_PM = idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t ID_STATE = idesc_bf16(128, 32, 1, 1);
+constexpr uint32_t ID_NUMA = idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t ID_NUMB = idesc_bf16(128, 128, 0, 1);
+
+// ---------------------------------------------------------------------------
+// compute-thread building blocks
+// ---------------------------------------------------------------------------
+// sum of squares of row r of a [128 x 128] SW128 tile
+__device__ __forceinline__ float tile_row_sumsq(uint32_t tile, int r) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint4 v = ld_shared_v4(tile + h * SUB + r * 128 + ((j ^ (r & 7)) << 4));
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float a = bf16_lo(w4[q]), b = bf16_hi(w4[q]);
+        s0 = fmaf(a, a, s0);
+        s1 = fmaf(b, b, s1);
+      }
+    }
+  }
+  return s0 + s1;
+}
+
+// per-row inverse scale (1/||x|| or 1 for pass-through / unnormalised rows)
+__device__ __forceinline__ float inv_scale(float sumsq, int normalize) {
+  if (!normalize) return 1.f;
+  const float nrm = sqrtf(sumsq);
+  return nrm < kZeroRowEps ? 1.f : 1.f / nrm;
+}
+
+// W' rows 3j, 3j+1, 3j+2 = W_hi[j], W_mid[j], W_lo[j] (W to 24 bits), K-major SW128
+__device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wop) {
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  for (int idx = threadIdx.x - 64; idx < 16 * 16; idx += 128) {
+    const int n = idx >> 4, j = idx & 15;  // row n, 8-element chunk j
+    const int hp = n / 3, piece = n % 3;
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v = 0.f;
+        if (hp < a.TP) {
+          const float x = w[hp * DH + j * 8 + e * 2 + h];
+          const float hi = bf16_round(x);
+          const float mid = bf16_round(x - hi);
+          v = piece == 0 ? hi : piece == 1 ? mid : bf16_round(x - hi - mid);
+        }
+        v2[h] = v;
+      }
+      pk[e] = pack_bf16(v2[0], v2[1]);
+    }
+    const uint32_t off = (j >> 3) * 2048 + n * 128 + (((j & 7) ^ (n & 7)) << 4);
+    st_shared_v4(wop + off, pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// features of one row from its 16 projection columns (P compile-time, T <= 8 >> P)
+template <int P>
+__device__ __forceinline__ void row_features(const Args& a, const float* proj, float inv, bool valid, float* phi) {
+  constexpr int R = 1 << P;
+  constexpr int TMAX = FP / R;
+#pragma unroll
+  for (int f = 0; f < FP; ++f) phi[f] = 0.f;
+#pragma unroll
+  for (int tau = 0; tau < TMAX; ++tau) {
+    if (tau < a.T && valid) {
+      float e[P], z = 1.f;
+      bool neg[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int j = tau * P + p;
+        const float u = tanhf((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
+        e[p] = expf(-2.f * a.beta * fabsf(u));
+        neg[p] = u < 0.f;
+        z *= 1.f + e[p];
+      }
+      const float rz = 1.f / z;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float prod = rz;
+#pragma unroll
+        for (int p = 0; p < P; ++p) prod *= (((rr >> p) & 1) == int(neg[p])) ? 1.f : e[p];
+        phi[tau * R + rr] = prod;
+      }
+    }
+  }
+}
+
+// row r of a [128 x 32] SW64 operand: four 8-element bf16 blocks
+__device__ __forceinline__ void write_row32(uint32_t buf, int r, const uint32_t (*blk)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+    st_shared_v4(buf + off, blk[j][0], blk[j][1], blk[j][2], blk[j][3]);
+  }
+}
+__device__ __forceinline__ void split8(const float* x, uint32_t* hi, uint32_t* lo) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float h0 = bf16_round(x[2 * e]), h1 = bf16_round(x[2 * e + 1]);
+    hi[e] = pack_bf16(h0, h1);
+    lo[e] = pack_bf16(x[2 * e] - h0, x[2 * e + 1] - h1);
+  }
+}
+// Phi_q row: [hi | lo | hi | 0];  Phi_k row: [hi | hi | lo | 0]  => Pq.Pk = qh kh + ql kh + qh kl
+__device__ __forceinline__ void write_phi_q(uint32_t buf, int r, const float* phi) {
+  uint32_t b[4][4];
+  split8(phi, b[0], b[1]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[2][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, r, b);
+}
+__device__ __forceinline__ void write_phi_k(uint32_t buf, int r, const float* phi) {
+  uint32_t b[4][4];
+  split8(phi, b[0], b[2]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[1][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, r, b);
+}
+// S operand row c (B of num = Phi_q S): [S_hi | S_hi | S_lo | 0] over f
+__device__ __forceinline__ void write_sop(uint32_t buf, int c, const float* s) {
+  uint32_t b[4][4];
+  split8(s, b[0], b[2]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { b[1][e] = b[0][e]; b[3][e] = 0u; }
+  write_row32(buf, c, b);
+}
+
+// block-wide sum of 8 values over the 128 compute threads, fixed order
+__device__ __forceinline__ void csum8(float* v, float* scratch) {
+#pragma unroll
+  for (int f = 0; f < FP; ++f) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
+  }
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int f = 0; f < FP; ++f) scratch[(warp_id() & 3) * FP + f] = v[f];
+  }
+  compute_bar();
+#pragma unroll
+  for (int f = 0; f < FP; ++f) v[f] = ((scratch[f] + scratch[FP + f]) + scratch[2 * FP + f]) + scratch[3 * FP + f];
+  compute_bar();
+}
+
+// write one [128 x 128] fp32 row (from TMEM) as bf16 into a SW128 staging tile
+__device__ __forceinline__ void stage_row_bf16(uint32_t tile, int r, const float* v, int c0) {
+  // v holds columns [c0, c0 + 32)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int chunk = (c0 >> 3) + j;  // 8-element chunk index 0..15
+    const uint32_t off = (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
+    st_shared_v4(tile + off, pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                 pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// backward helpers
+// ---------------------------------------------------------------------------
+// W'' = [W_hi; W_hi; W_lo; 0] (blocks of 8 K-rows, hyperplane j in row 8b + j) as an
+// MN-major SW128 [32 x 128] operand: B of dx^ = dProj . W with dProj = [hi | lo | hi | 0]
+constexpr int W2OP = 2 * 32 * 128;  // 8 KB
+__device__ __forceinline__ uint64_t desc_w2(uint32_t base, int kk) {
+  return smem_desc(base + kk * 2048, 4096, 1024, kSw128);
+}
+__device__ __forceinline__ void build_w2(const Args& a, int64_t bh, uint32_t w2) {
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  for (int idx = threadIdx.x - 64; idx < 32 * 16; idx += 128) {
+    const int k = idx >> 4, j = idx & 15;  // K-row k, 8-element column chunk j
+    const int blk = k >> 3, hp = k & 7;
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v = 0.f;
+        if (blk < 3 && hp < a.TP) {
+          const float x = w[hp * DH + j * 8 + e * 2 + h];
+          const float hi = bf16_round(x);
+          v = blk == 2 ? x - hi : hi;
+        }
+        v2[h] = v;
+      }
+      pk[e] = pack_bf16(v2[0], v2[1]);
+    }
+    const uint32_t off = (j >> 3) * 4096 + k * 128 + (((j & 7) ^ (k & 7)) << 4);
+    st_shared_v4(w2 + off, pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// S^T operand [16 x 128] K-major SW128 (rows f = S_hi[f], 8 + f = S_lo[f]; K = value
+// column): B of y = dO . S_v^T.  Thread c owns value column c.
+__device__ __forceinline__ void write_sopT(uint32_t buf, int c, const float* s) {
+  const uint32_t sub = (c >> 6) * 2048;
+  const uint32_t inrow = (c & 63) * 2;
+#pragma unroll
+  for (int f = 0; f < 8; ++f) {
+    const float hi = bf16_round(s[f]);
+    const __nv_bfloat16 bh = __float2bfloat16_rn(hi), bl = __float2bfloat16_rn(s[f] - hi);
+    const uint32_t o1 = f * 128 + inrow, o2 = (8 + f) * 128 + inrow;
+    const uint32_t p1 = sub + (o1 ^ (((o1 >> 7) & 7) << 4)), p2 = sub + (o2 ^ (((o2 >> 7) & 7) << 4));
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + p1), "h"(*reinterpret_cast<const unsigned short*>(&bh)) : "memory");
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + p2), "h"(*reinterpret_cast<const unsigned short*>(&bl)) : "memory");
+  }
+}
+
+// features + the tanh values u_j (j < TP) kept for the VJP
+template <int P>
+__device__ __forceinline__ void row_features_u(const Args& a, const float* proj, float inv, bool valid, float* phi,
+                                               float* u) {
+  constexpr int R = 1 << P;
+  constexpr int TMAX = FP / R;
+#pragma unroll
+  for (int f = 0; f < FP; ++f) phi[f] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) u[j] = 0.f;
+#pragma unroll
+  for (int tau = 0; tau < TMAX; ++tau) {
+    if (tau < a.T && valid) {
+      float e[P], z = 1.f;
+      bool neg[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int j = tau * P + p;
+        const float uu = tanhf((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
+        u[j] = uu;
+        e[p] = expf(-2.f * a.beta * fabsf(uu));
+        neg[p] = uu < 0.f;
+        z *= 1.f + e[p];
+      }
+      const float rz = 1.f / z;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float prod = rz;
+#pragma unroll
+        for (int p = 0; p < P; ++p) prod *= (((rr >> p) & 1) == int(neg[p])) ? 1.f : e[p];
+        phi[tau * R + rr] = prod;
+      }
+    }
+  }
+}
+
+// softmax-over-corners + tanh VJP (ra/backward.py:53-90): dphi -> dproj_j, j < TP
+template <int P>
+__device__ __forceinline__ void row_feature_vjp(const Args& a, const float* u, const float* phi, const float* dphi,
+                                                float* dproj) {
+  constexpr int R = 1 << P;
+  constexpr int TMAX = FP / R;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) dproj[j] = 0.f;
+#pragma unroll
+  for (int tau = 0; tau < TMAX; ++tau) {
+    if (tau < a.T) {
+      float s = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) s = fmaf(dphi[tau * R + rr], phi[tau * R + rr], s);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        float du = 0.f;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const float dl = phi[tau * R + rr] * (dphi[tau * R + rr] - s);
+          du += ((rr >> p) & 1) ? -dl : dl;
+        }
+        const float uu = u[tau * P + p];
+        dproj[tau * P + p] = a.beta * du * (1.f - uu * uu);
+      }
+    }
+  }
+}
+
+// dProj row (A of dx^ = dProj . W''): [hi | lo | hi | 0]
+__device__ __forceinline__ void write_dproj(uint32_t buf, int r, const float* dproj) { write_phi_q(buf, r, dproj); }
+
+struct Scale {
+  float inv;     // 1/||x|| (or 1)
+  bool tangent;  // apply the sphere-tangent projection (normalised, non-zero row)
+};
+__device__ __forceinline__ Scale row_scale(float sumsq, int normalize) {
+  if (!normalize) return {1.f, false};
+  const float nrm = sqrtf(sumsq);
+  if (nrm < kZeroRowEps) return {1.f, false};
+  return {1.f / nrm, true};
+}
+
+// dx = (dx^ - (dx^.x^) x^) / ||x|| from TMEM columns [col, col+128) (lane = row r),
+// x = row r of the SW128 tile; the bf16 result overwrites row r of the same tile.
+__device__ __forceinline__ void tangent_row_inplace(uint32_t tmem_col, uint32_t tile, int r, Scale sc) {
+  // tcgen05.ld is warp-collective (.sync.aligned): every lane runs both passes,
+  // rows without the tangent step (zero / padded rows) just discard the dot.
+  float dot = 0.f;
+  {
+#pragma unroll
+    for (int c0 = 0; c0 < DH; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem_col + c0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int chunk = (c0 >> 3) + j;
+        const uint4 x = ld_shared_v4(tile + (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4));
+        const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          dot = fmaf(v[8 * j + 2 * q], bf16_lo(xw[q]), dot);
+          dot = fmaf(v[8 * j + 2 * q + 1], bf16_hi(xw[q]), dot);
+        }
+      }
+    }
+  }
+  const float cx = sc.tangent ? dot * sc.inv * sc.inv : 0.f;  // (dx^.x^) / ||x|| per unit of raw x
+#pragma unroll
+  for (int c0 = 0; c0 < DH; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem_col + c0, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int chunk = (c0 >> 3) + j;
+      const uint32_t addr = tile + (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
+      uint32_t o[4];
+      if (sc.tangent) {
+        const uint4 x = ld_shared_v4(addr);
+        const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = pack_bf16((v[8 * j + 2 * q] - cx * bf16_lo(xw[q])) * sc.inv,
+                           (v[8 * j + 2 * q + 1] - cx * bf16_hi(xw[q])) * sc.inv);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = pack_bf16(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
+      }
+      st_shared_v4(addr, o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [BH, N, 128] bf16 viewed as 3-D {128, N, BH}; box {64, 128, 1}; SW128
+inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t(DH), cuuint64_t(g.N), cuuint64_t(g.BH)};
+  cuuint64_t strides[2] = {cuuint64_t(DH) * 2, cuuint64_t(g.N) * DH * 2};
+  cuuint32_t box[3] = {64, CH, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+unsigned* debug_progress_device();  // race_tc.cu
+inline Args make_args(const Geo& g) {
+  Args a{};
+  a.dbg = debug_progress_device();
+  a.BH = g.BH;
+  a.H = g.H;
+  a.N = g.N;
+  a.nseg = g.nseg;
+  a.seg_tokens = g.seg_tokens;
+  a.P = g.P;
+  a.T = g.T;
+  a.TP = g.T * g.P;
+  a.beta = g.beta;
+  a.normalize = g.normalize;
+  a.w_per_head = g.w_per_head;
+  return a;
+}
+
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+inline unsigned grid_for(const Geo& g) {
+  const int64_t items = g.BH * g.nseg;
+  return unsigned(items < num_sms() ? items : num_sms());
+}
+
+template <typename K, typename... Ts>
+cudaError_t launch(K kernel, int smem, unsigned grid, cudaStream_t st, Ts... args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, NTHREADS, smem, st>>>(args...);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace tcfast
+}  // namespace race

@@ -316,3 +316,27 @@ def test_fast_path_forward(causal, n, pl):
         o_r, den_r, _ = ro.forward(qh, kh, vh, w[0].double().cpu().numpy(), cfg.beta, causal)
         assert rel_err(o_f[0, 0].float().cpu(), o_r) <= TOL_BF16
         assert rel_err(den_f[0, 0].cpu(), den_r) <= TOL_F32
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("n", [128, 1000, 4096, 70000])
+@pytest.mark.parametrize("pl", [(2, 2), (1, 3), (3, 1)], ids=["P2L2", "P1L3", "P3L1"])
+def test_fast_path_backward(causal, n, pl):
+    q, k, v, g, w, p = _big(n=n, causal=causal)
+    P, L = pl
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=5, causal=causal)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(q.device)
+    p = cfg.params()
+
+    def run():
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        return rb.race_backward(q, k, v, w, g, p, state=st)
+
+    fast, slow = _both_paths(run)
+    for x, y in zip(fast, slow):
+        assert rel_err(x.float().cpu(), y.float().cpu()) <= TOL_BF16
+    if n <= 4096:
+        qh, kh, vh, gh = (t[0, 1].double().cpu().numpy() for t in (q, k, v, g))
+        ref = ro.vjp(qh, kh, vh, w[1].double().cpu().numpy(), cfg.beta, gh, causal)
+        errs = grad_errs([t[0, 1].float().cpu().numpy() for t in fast], ref, GRAD_FLOOR)
+        assert max(errs) <= TOL_BF16, errs
