@@ -24,6 +24,12 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
                      float* dpart, cudaStream_t st);
 cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
                      void* dv, cudaStream_t st);
+cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                            const float* w, const float* car, void* dq, float* rden, float* gden, float* dpart,
+                            cudaStream_t st);
+cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
+                            const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
+                            void* dv, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
                           const float* car, void* o, float* den, cudaStream_t st);
 }  // namespace race
@@ -246,6 +252,9 @@ int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k, con
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_bwd_causal_q(g, q, k, v, d_o, w, carries, dq, rden, gden, dpart, S(stream)),
+                       "tc_bwd_causal_q");
   return cuda_status(race::simt_bwd_causal_q(g, q, k, v, d_o, w, carries, dq, rden, gden, dpart, S(stream)),
                      "bwd_causal_q");
 }
@@ -257,6 +266,9 @@ int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, con
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, dk, dv, S(stream)),
+                       "tc_bwd_causal_k");
   return cuda_status(race::simt_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, dk, dv, S(stream)),
                      "bwd_causal_k");
 }
