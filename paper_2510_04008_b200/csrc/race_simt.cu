@@ -657,26 +657,50 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restric
   }
 }
 
-// Fixed-order segment reduction (see race_combine in race_b200.h).
-__global__ void k_combine(int64_t BH, int64_t nseg, int64_t E, int mode, const float* __restrict__ part,
-                          const float* __restrict__ carry, float* __restrict__ out) {
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// Fixed-order segment reduction (see race_combine in race_b200.h).  Block =
+// 32 table elements x CG segment groups: each thread sums its group's
+// segments in order, the group totals are combined in group order through
+// shared memory, then each thread emits its group's prefixes/suffixes.  The
+// association is fixed by (nseg, CG), so results are bit-reproducible.
+constexpr int CG = 16;
+__global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, int64_t E, int mode,
+                                                     const float* __restrict__ part, const float* __restrict__ carry,
+                                                     float* __restrict__ out) {
+  __shared__ float gs[CG][33];
+  const int lx = threadIdx.x & 31, gy = threadIdx.x >> 5;
+  const int64_t e = int64_t(blockIdx.x) * 32 + lx;
   const int64_t bh = blockIdx.y;
-  if (e >= E) return;
+  const int64_t per = (nseg + CG - 1) / CG;
+  const int64_t s0 = gy * per, s1 = s0 + per < nseg ? s0 + per : nseg;
+  const bool ok = e < E;
   const float* p = part + bh * nseg * E + e;
-  float s = carry ? carry[bh * E + e] : 0.f;
+  float sum = 0.f;
+  if (ok)
+    for (int64_t i = s0; i < s1; ++i) sum += p[i * E];
+  gs[gy][lx] = sum;
+  __syncthreads();
+  const float c = (ok && carry) ? carry[bh * E + e] : 0.f;
   if (mode == 0) {
-    for (int64_t i = 0; i < nseg; ++i) s += p[i * E];
-    out[bh * E + e] = s;
-  } else if (mode == 1) {
-    for (int64_t i = 0; i < nseg; ++i) {
-      out[(bh * nseg + i) * E + e] = s;
-      s += p[i * E];
+    if (gy == 0 && ok) {
+      float tot = c;
+      for (int g = 0; g < CG; ++g) tot += gs[g][lx];
+      out[bh * E + e] = tot;
+    }
+    return;
+  }
+  if (!ok) return;
+  float base = c;
+  if (mode == 1) {
+    for (int g = 0; g < gy; ++g) base += gs[g][lx];
+    for (int64_t i = s0; i < s1; ++i) {
+      out[(bh * nseg + i) * E + e] = base;
+      base += p[i * E];
     }
   } else {
-    for (int64_t i = nseg - 1; i >= 0; --i) {
-      out[(bh * nseg + i) * E + e] = s;
-      s += p[i * E];
+    for (int g = CG - 1; g > gy; --g) base += gs[g][lx];
+    for (int64_t i = s1 - 1; i >= s0; --i) {
+      out[(bh * nseg + i) * E + e] = base;
+      base += p[i * E];
     }
   }
 }
@@ -785,8 +809,8 @@ cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const 
 }
 cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st) {
   const int64_t E = int64_t(g.T << g.P) * (g.dv + 1);
-  dim3 grid(unsigned((E + 255) / 256), unsigned(g.BH));
-  simt::k_combine<<<grid, 256, 0, st>>>(g.BH, g.nseg, E, mode, part, carry, out);
+  dim3 grid(unsigned((E + 31) / 32), unsigned(g.BH));
+  simt::k_combine<<<grid, 32 * simt::CG, 0, st>>>(g.BH, g.nseg, E, mode, part, carry, out);
   note_launch();
   return cudaGetLastError();
 }

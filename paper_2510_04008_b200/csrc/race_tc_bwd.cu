@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld16(tmem + lane_base() + TM_P, proj);
         tmem_ld16(tmem + lane_base() + TM_Y, yv);
         tmem_ld_wait();
-        float phi[FP], u[5];
-        row_features_u<P>(a, proj, sc.inv, valid, phi, u);
+        float phi[FP], u[5], ph[5];
+        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
         float y[FP], D = 0.f, num = 0.f;
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_arrive(ready);
         mbar_wait(c2, gc & 1);
         tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc);
+        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc, dot_from_proj(dproj, ph));
         tc_fence_before();
         fence_proxy_async();
         compute_bar();
@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld16(tmem + lane_base() + TM_P, proj);
         tmem_ld16(tmem + lane_base() + TM_Z, zv);
         tmem_ld_wait();
-        float phi[FP], u[5], dphi[FP];
-        row_features_u<P>(a, proj, sc.inv, valid, phi, u);
+        float phi[FP], u[5], ph[5], dphi[FP];
+        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
 #pragma unroll
         for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
         float dproj[8];
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld_wait();
           stage_row_bf16(stage + TILE, r, v, c0);  // dV over the dead V row
         }
-        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc);
+        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc, dot_from_proj(dproj, ph));
         tc_fence_before();
         fence_proxy_async();
         compute_bar();

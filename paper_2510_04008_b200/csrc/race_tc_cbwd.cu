@@ -250,9 +250,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld16(tmem + lane_base() + TM_PK, pk);
         tmem_ld16(tmem + lane_base() + TM_Y, yv);
         tmem_ld_wait();
-        float phq[FP], uq[5], phk[FP], uk[5];
-        row_features_u<P>(a, pq, scq.inv, valid, phq, uq);
-        row_features_u<P>(a, pk, sck.inv, valid, phk, uk);
+        float phq[FP], uq[5], hq[5], phk[FP], uk[5], hk[5];
+        row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+        row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
         write_phi_q(sb + OFF_PHIQ, r, phq);
         write_phi_k(sb + OFF_PHIK, r, phk);
         fence_proxy_async();
@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
         float dproj[8];
         row_feature_vjp<P>(a, uq, phq, dphi, dproj);
+        const float dotq = dot_from_proj(dproj, hq);
         write_dproj(sb + OFF_DPROJ, r, dproj);
         fence_proxy_async();
         tc_fence_before();
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ---- dq in place of q, then store
         mbar_wait(c4, par);
         tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_Q, r, scq);
+        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_Q, r, scq, dotq);
         tc_fence_before();
         fence_proxy_async();
         compute_bar();
@@ -583,13 +584,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool valid = t + r < m.t1;
         // per-query-token normaliser terms of this chunk (rg is free: the previous
         // chunk finished reading it before its final compute_bar)
-        rg[r] = valid ? rden[m.bh * a.N + t + r] : 0.f;
-        rg[128 + r] = valid ? gden[m.bh * a.N + t + r] : 0.f;
+        const float rd_ld = valid ? rden[m.bh * a.N + t + r] : 0.f;
+        const float gd_ld = valid ? gden[m.bh * a.N + t + r] : 0.f;
         mbar_wait(fullQ, par);
         mbar_wait(fullK, par);
         const Scale scq = row_scale(tile_row_sumsq(sb + OFF_Q, r), a.normalize);
         const Scale sck = row_scale(tile_row_sumsq(sb + OFF_K, r), a.normalize);
         mbar_arrive(emptyQ);
+        rg[r] = rd_ld;
+        rg[128 + r] = gd_ld;
         mbar_wait(c1, par);
         tc_fence_after();
         float pq[16], pk[16], zv[16];
@@ -597,9 +600,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld16(tmem + lane_base() + TM_PK, pk);
         tmem_ld16(tmem + lane_base() + TM_ZV, zv);
         tmem_ld_wait();
-        float phq[FP], phk[FP], uk[5], uq[5];
-        row_features_u<P>(a, pq, scq.inv, valid, phq, uq);
-        row_features_u<P>(a, pk, sck.inv, valid, phk, uk);
+        float phq[FP], phk[FP], uk[5], uq[5], hq[5], hk[5];
+        row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+        row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
         write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
         write_phi_q(sb + OFF_PHIK, r, phk);  // [hi|lo|hi|0]
         fence_proxy_async();
@@ -649,6 +652,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
         float dproj[8];
         row_feature_vjp<P>(a, uk, phk, dphi, dproj);
+        const float dotk = dot_from_proj(dproj, hk);
         write_dproj(sb + OFF_DPROJ, r, dproj);
         float dsa[32];
         tmem_ld32(tmem + lane_base() + TM_DS, dsa);
@@ -674,7 +678,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ---- dk in place of k, then store dK, dV
         mbar_wait(c4, par);
         tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_K, r, sck);
+        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_K, r, sck, dotk);
         tc_fence_before();
         fence_proxy_async();
         compute_bar();

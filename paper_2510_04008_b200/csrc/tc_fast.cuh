@@ -315,13 +315,13 @@ __device__ __forceinline__ void write_sopT(uint32_t buf, int c, const float* s) 
 // features + the tanh values u_j (j < TP) kept for the VJP
 template <int P>
 __device__ __forceinline__ void row_features_u(const Args& a, const float* proj, float inv, bool valid, float* phi,
-                                               float* u) {
+                                               float* u, float* phat) {
   constexpr int R = 1 << P;
   constexpr int TMAX = FP / R;
 #pragma unroll
   for (int f = 0; f < FP; ++f) phi[f] = 0.f;
 #pragma unroll
-  for (int j = 0; j < 5; ++j) u[j] = 0.f;
+  for (int j = 0; j < 5; ++j) u[j] = phat[j] = 0.f;
 #pragma unroll
   for (int tau = 0; tau < TMAX; ++tau) {
     if (tau < a.T && valid) {
@@ -330,7 +330,9 @@ __device__ __forceinline__ void row_features_u(const Args& a, const float* proj,
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const int j = tau * P + p;
-        const float uu = tanhf((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
+        const float ph = (proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv;
+        const float uu = tanhf(ph);
+        phat[j] = ph;
         u[j] = uu;
         e[p] = expf(-2.f * a.beta * fabsf(uu));
         neg[p] = uu < 0.f;
@@ -380,6 +382,14 @@ __device__ __forceinline__ void row_feature_vjp(const Args& a, const float* u, c
 // dProj row (A of dx^ = dProj . W''): [hi | lo | hi | 0]
 __device__ __forceinline__ void write_dproj(uint32_t buf, int r, const float* dproj) { write_phi_q(buf, r, dproj); }
 
+// dx^.x^ = sum_j dproj_j phat_j
+__device__ __forceinline__ float dot_from_proj(const float* dproj, const float* phat) {
+  float d = 0.f;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) d = fmaf(dproj[j], phat[j], d);
+  return d;
+}
+
 struct Scale {
   float inv;     // 1/||x|| (or 1)
   bool tangent;  // apply the sphere-tangent projection (normalised, non-zero row)
@@ -393,30 +403,11 @@ __device__ __forceinline__ Scale row_scale(float sumsq, int normalize) {
 
 // dx = (dx^ - (dx^.x^) x^) / ||x|| from TMEM columns [col, col+128) (lane = row r),
 // x = row r of the SW128 tile; the bf16 result overwrites row r of the same tile.
-__device__ __forceinline__ void tangent_row_inplace(uint32_t tmem_col, uint32_t tile, int r, Scale sc) {
-  // tcgen05.ld is warp-collective (.sync.aligned): every lane runs both passes,
-  // rows without the tangent step (zero / padded rows) just discard the dot.
-  float dot = 0.f;
-  {
-#pragma unroll
-    for (int c0 = 0; c0 < DH; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem_col + c0, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int chunk = (c0 >> 3) + j;
-        const uint4 x = ld_shared_v4(tile + (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4));
-        const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          dot = fmaf(v[8 * j + 2 * q], bf16_lo(xw[q]), dot);
-          dot = fmaf(v[8 * j + 2 * q + 1], bf16_hi(xw[q]), dot);
-        }
-      }
-    }
-  }
-  const float cx = sc.tangent ? dot * sc.inv * sc.inv : 0.f;  // (dx^.x^) / ||x|| per unit of raw x
+// dot_hat = dx^.x^ = sum_j dproj_j (x^.w_j): computed by the caller from the
+// projections, so one pass over dx^ suffices.
+__device__ __forceinline__ void tangent_row_inplace(uint32_t tmem_col, uint32_t tile, int r, Scale sc,
+                                                    float dot_hat) {
+  const float cx = sc.tangent ? dot_hat * sc.inv : 0.f;  // (dx^.x^) / ||x|| per unit of raw x
 #pragma unroll
   for (int c0 = 0; c0 < DH; c0 += 32) {
     float v[32];
