@@ -282,6 +282,7 @@ def run_ours(args, world, rank, local_rank):
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     rden = torch.empty((pr.bh, n), device=dev)
     gden = torch.empty_like(rden)
+    norms = torch.empty((pr.bh, n, 2), device=dev)
     S = _stream()
     ptr = _vp
     if causal:
@@ -289,12 +290,14 @@ def run_ours(args, world, rank, local_rank):
             ("kside_partials", lambda: L.race_kside_partials(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(part), ptr(ws), S)),
             ("combine", lambda: L.race_combine(pr.dref, 1, ptr(part), None, ptr(tabs), S)),
             ("fwd_causal", lambda: L.race_fwd_causal(pr.dref, ptr(q), ptr(k), ptr(v), ptr(pr.w), ptr(tabs), ptr(o),
-                                                     ptr(den), ptr(ws), S)),
+                                                     ptr(den), ptr(norms), ptr(ws), S)),
             ("bwd_causal_q", lambda: L.race_bwd_causal_q(pr.dref, ptr(q), ptr(k), ptr(v), ptr(g), ptr(pr.w), ptr(tabs),
-                                                         ptr(dq), ptr(rden), ptr(gden), ptr(dpart), ptr(ws), S)),
+                                                         ptr(norms), ptr(dq), ptr(rden), ptr(gden), ptr(dpart),
+                                                         ptr(ws), S)),
             ("combine_d", lambda: L.race_combine(pr.dref, 2, ptr(dpart), None, ptr(dtabs), S)),
             ("bwd_causal_k", lambda: L.race_bwd_causal_k(pr.dref, ptr(q), ptr(k), ptr(v), ptr(g), ptr(pr.w), ptr(rden),
-                                                         ptr(gden), ptr(dtabs), ptr(dk), ptr(dv), ptr(ws), S)),
+                                                         ptr(gden), ptr(dtabs), ptr(norms), ptr(dk), ptr(dv),
+                                                         ptr(ws), S)),
         ]
     else:
         calls = [

@@ -93,7 +93,9 @@ int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens);
 int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
 
 /* Elements (float32) of the state race_fwd saves for race_bwd:
- * non-causal: tables [BH, F, dv+1];  causal: carries [BH, nseg, F, dv+1]. */
+ * non-causal: tables [BH, F, dv+1];
+ * causal: carries [BH, nseg, F, dv+1] followed by rownorms [BH, N, 2]
+ *         (sum of squares of each q and k row, reused by the backward).    */
 int race_state_elems(const race_desc_t* desc, int64_t* elems);
 
 /* ---- monolithic single-device entry points ---------------------------- */
@@ -136,10 +138,12 @@ int race_fwd_readout(const race_desc_t* desc, const void* q, const float* w,
                      void* workspace, void* stream);
 
 /* Causal chunked scan given per-segment carry-in tables
- * (ra/forward.py:100-121).                                                */
+ * (ra/forward.py:100-121).  rownorms (may be NULL) receives [BH, N, 2]
+ * float32: the sum of squares of each q and k row.                        */
 int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k,
                     const void* v, const float* w, const float* carries,
-                    void* o, float* den, void* workspace, void* stream);
+                    void* o, float* den, float* rownorms, void* workspace,
+                    void* stream);
 
 /* Non-causal backward, query side: dq and per-segment partial dS
  * (ra/backward.py:109-118 + the d_num/d_den prologue 201-209).           */
@@ -154,11 +158,12 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v,
 
 /* Causal backward, forward-direction scan: dq, per-token normaliser terms
  * rden = 1/(T*den), gden = -(dO.O)/(T*den), and per-segment dS totals
- * (ra/backward.py:142-168).                                               */
+ * (ra/backward.py:142-168).  rownorms (may be NULL = recompute) is what
+ * race_fwd_causal wrote.                                                  */
 int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k,
                       const void* v, const void* d_o, const float* w,
-                      const float* carries, void* dq, float* rden,
-                      float* gden, float* dpart, void* workspace,
+                      const float* carries, const float* rownorms, void* dq,
+                      float* rden, float* gden, float* dpart, void* workspace,
                       void* stream);
 
 /* Causal backward, reverse-direction scan given per-segment suffix dS
@@ -166,8 +171,8 @@ int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k,
 int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k,
                       const void* v, const void* d_o, const float* w,
                       const float* rden, const float* gden,
-                      const float* dcarries, void* dk, void* dv,
-                      void* workspace, void* stream);
+                      const float* dcarries, const float* rownorms, void* dk,
+                      void* dv, void* workspace, void* stream);
 
 #ifdef __cplusplus
 }

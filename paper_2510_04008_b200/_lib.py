@@ -75,11 +75,11 @@ _SIGS = {
     "race_kside_partials": ([_P] * 7, ctypes.c_int),
     "race_combine": ([_P, ctypes.c_int32, _P, _P, _P, _P], ctypes.c_int),
     "race_fwd_readout": ([_P] * 8, ctypes.c_int),
-    "race_fwd_causal": ([_P] * 10, ctypes.c_int),
+    "race_fwd_causal": ([_P] * 11, ctypes.c_int),
     "race_bwd_qside": ([_P] * 9, ctypes.c_int),
     "race_bwd_kside": ([_P] * 9, ctypes.c_int),
-    "race_bwd_causal_q": ([_P] * 13, ctypes.c_int),
-    "race_bwd_causal_k": ([_P] * 13, ctypes.c_int),
+    "race_bwd_causal_q": ([_P] * 14, ctypes.c_int),
+    "race_bwd_causal_k": ([_P] * 14, ctypes.c_int),
 }
 
 

@@ -25,13 +25,13 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
 cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
                      void* dv, cudaStream_t st);
 cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
-                            const float* w, const float* car, void* dq, float* rden, float* gden, float* dpart,
-                            cudaStream_t st);
+                            const float* w, const float* car, const float* nrm, void* dq, float* rden, float* gden,
+                            float* dpart, cudaStream_t st);
 cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
-                            const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
-                            void* dv, cudaStream_t st);
+                            const float* w, const float* rden, const float* gden, const float* dcar,
+                            const float* nrm, void* dk, void* dv, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                          const float* car, void* o, float* den, cudaStream_t st);
+                          const float* car, void* o, float* den, float* nrm, cudaStream_t st);
 }  // namespace race
 
 namespace race {
@@ -172,7 +172,7 @@ int race_workspace_bytes(const race_desc_t* desc, size_t* bytes) {
 int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
-  *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g);
+  *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g) + (g.causal ? 2 * g.BH * g.N : 0);
   return RACE_OK;
 }
 
@@ -213,14 +213,14 @@ int race_fwd_readout(const race_desc_t* desc, const void* q, const float* w, con
 }
 
 int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w,
-                    const float* carries, void* o, float* den, void* workspace, void* stream) {
+                    const float* carries, void* o, float* den, float* rownorms, void* workspace, void* stream) {
   (void)workspace;
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
   if (race::tc_supported(g))
-    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, S(stream)), "tc_causal_fwd");
-  return cuda_status(race::simt_causal_fwd(g, q, k, v, w, carries, o, den, S(stream)), "causal_fwd");
+    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, S(stream)), "tc_causal_fwd");
+  return cuda_status(race::simt_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, S(stream)), "causal_fwd");
 }
 
 int race_bwd_qside(const race_desc_t* desc, const void* q, const void* d_o, const float* w, const float* tables,
@@ -246,28 +246,28 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v, const 
 }
 
 int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k, const void* v, const void* d_o,
-                      const float* w, const float* carries, void* dq, float* rden, float* gden, float* dpart,
-                      void* workspace, void* stream) {
+                      const float* w, const float* carries, const float* rownorms, void* dq, float* rden,
+                      float* gden, float* dpart, void* workspace, void* stream) {
   (void)workspace;
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
   if (race::tc_supported(g))
-    return cuda_status(race::tc_bwd_causal_q(g, q, k, v, d_o, w, carries, dq, rden, gden, dpart, S(stream)),
+    return cuda_status(race::tc_bwd_causal_q(g, q, k, v, d_o, w, carries, rownorms, dq, rden, gden, dpart, S(stream)),
                        "tc_bwd_causal_q");
   return cuda_status(race::simt_bwd_causal_q(g, q, k, v, d_o, w, carries, dq, rden, gden, dpart, S(stream)),
                      "bwd_causal_q");
 }
 
 int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, const void* v, const void* d_o,
-                      const float* w, const float* rden, const float* gden, const float* dcarries, void* dk,
-                      void* dv, void* workspace, void* stream) {
+                      const float* w, const float* rden, const float* gden, const float* dcarries,
+                      const float* rownorms, void* dk, void* dv, void* workspace, void* stream) {
   (void)workspace;
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
   if (race::tc_supported(g))
-    return cuda_status(race::tc_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, dk, dv, S(stream)),
+    return cuda_status(race::tc_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, rownorms, dk, dv, S(stream)),
                        "tc_bwd_causal_k");
   return cuda_status(race::simt_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, dk, dv, S(stream)),
                      "bwd_causal_k");
@@ -287,7 +287,8 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     return race_fwd_readout(desc, q, w, tabs, o, den, workspace, stream);
   }
   if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
-  return race_fwd_causal(desc, q, k, v, w, tabs, o, den, workspace, stream);
+  float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
+  return race_fwd_causal(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
 }
 
 int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, const void* d_o,
@@ -310,10 +311,12 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     if (int rc = race_combine(desc, RACE_COMBINE_TOTAL, ws.dpart, nullptr, ws.dtables, stream)) return rc;
     return race_bwd_kside(desc, k, v, w, ws.dtables, dk, dv, workspace, stream);
   }
-  if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, dq, ws.rden, ws.gden, ws.dpart, workspace, stream))
+  const float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
+  if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, nrm, dq, ws.rden, ws.gden, ws.dpart, workspace,
+                                 stream))
     return rc;
   if (int rc = race_combine(desc, RACE_COMBINE_SUFFIX, ws.dpart, nullptr, ws.dtables, stream)) return rc;
-  return race_bwd_causal_k(desc, q, k, v, d_o, w, ws.rden, ws.gden, ws.dtables, dk, dv, workspace, stream);
+  return race_bwd_causal_k(desc, q, k, v, d_o, w, ws.rden, ws.gden, ws.dtables, nrm, dk, dv, workspace, stream);
 }
 
 }  // extern "C"

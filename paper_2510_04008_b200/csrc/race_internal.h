@@ -25,7 +25,7 @@ cudaError_t simt_aggregate(const Geo& g, const void* k, const void* v, const flo
 cudaError_t simt_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
                          cudaStream_t st);
 cudaError_t simt_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                            const float* car, void* o, float* den, cudaStream_t st);
+                            const float* car, void* o, float* den, float* nrm, cudaStream_t st);
 cudaError_t simt_bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
                        float* dpart, cudaStream_t st);
 cudaError_t simt_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,

@@ -335,7 +335,8 @@ __global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict_
                                                    const Tin* __restrict__ k, const Tin* __restrict__ v,
                                                    const float* __restrict__ w,
                                                    const float* __restrict__ carries,
-                                                   Tin* __restrict__ o, float* __restrict__ den) {
+                                                   Tin* __restrict__ o, float* __restrict__ den,
+                                                   float* __restrict__ nrm) {
   const Plan pl(g, kW | kS | kXq | kXk | kV | kPhq | kPhk | kPm);
   float* sm = reinterpret_cast<float*>(smem_f4);
   float* ws = sm + pl.oW; float* S = sm + pl.oS; float* xq = sm + pl.oXq; float* xk = sm + pl.oXk;
@@ -356,6 +357,13 @@ __global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict_
     __syncthreads();
     tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
     tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    if (nrm) {  // row sums of squares for the backward (same meaning as the fast path's)
+      for (int r = threadIdx.x; r < rows; r += NT) {
+        const float sq = rowv[kScQ * TILE + r], sk = rowv[kScK * TILE + r];
+        nrm[(bh * g.N + t0 + r) * 2 + 0] = sq > 0.f ? sq * sq : 0.f;
+        nrm[(bh * g.N + t0 + r) * 2 + 1] = sk > 0.f ? sk * sk : 0.f;
+      }
+    }
     __syncthreads();
     for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
       const int r = it / TILE, j = it % TILE;
@@ -737,9 +745,9 @@ struct Launch {
     RACE_LAUNCH(k_readout<Tin>, kW | kS | kXq | kPhq, (const Tin*)q, w, tab, (Tin*)o, den);
   }
   static cudaError_t causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                                const float* car, void* o, float* den, cudaStream_t st) {
+                                const float* car, void* o, float* den, float* nrm, cudaStream_t st) {
     RACE_LAUNCH(k_causal_fwd<Tin>, kW | kS | kXq | kXk | kV | kPhq | kPhk | kPm, (const Tin*)q, (const Tin*)k,
-                (const Tin*)v, w, car, (Tin*)o, den);
+                (const Tin*)v, w, car, (Tin*)o, den, nrm);
   }
   static cudaError_t bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
                            float* dpart, cudaStream_t st) {
@@ -786,8 +794,8 @@ cudaError_t simt_readout(const Geo& g, const void* q, const float* w, const floa
   return RACE_DISPATCH(readout, g, q, w, tab, o, den, st);
 }
 cudaError_t simt_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                            const float* car, void* o, float* den, cudaStream_t st) {
-  return RACE_DISPATCH(causal_fwd, g, q, k, v, w, car, o, den, st);
+                            const float* car, void* o, float* den, float* nrm, cudaStream_t st) {
+  return RACE_DISPATCH(causal_fwd, g, q, k, v, w, car, o, den, nrm, st);
 }
 cudaError_t simt_bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
                        float* dpart, cudaStream_t st) {

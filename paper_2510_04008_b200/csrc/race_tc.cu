@@ -522,9 +522,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int s = gc & 1;
         const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
         mbar_wait(&full[s], (gc >> 1) & 1);
-        const float invq = inv_scale(tile_row_sumsq(stage, r), a.normalize);
-        const float invk = inv_scale(tile_row_sumsq(stage + TILE, r), a.normalize);
+        const float sqq = tile_row_sumsq(stage, r), sqk = tile_row_sumsq(stage + TILE, r);
+        const float invq = inv_scale(sqq, a.normalize);
+        const float invk = inv_scale(sqk, a.normalize);
         const bool valid = t + r < m.t1;
+        if (a.nrm_out && valid)
+          *reinterpret_cast<float2*>(a.nrm_out + (m.bh * a.N + t + r) * 2) = make_float2(sqq, sqk);
         mbar_wait(proj_full, gc & 1);
         tc_fence_after();
         float pq[16], pk[16];
@@ -547,9 +550,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(pm_full, gc & 1);
         tc_fence_after();
         float rs = 0.f;
+        const int qw = warp & 3;  // rows 32qw..: column blocks > qw are above the diagonal
 #pragma unroll
         for (int c0 = 0; c0 < CH; c0 += 32) {
           float v[32];
+          if ((c0 >> 5) > qw) {  // warp-uniform
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            stage_row_bf16(stage, r, v, c0);
+            continue;
+          }
           tmem_ld32(tmem + lane_base() + TM_PM + c0, v);
           tmem_ld_wait();
 #pragma unroll
@@ -669,7 +679,7 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
 }
 
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                          const float* car, void* o, float* den, cudaStream_t st) {
+                          const float* car, void* o, float* den, float* nrm, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mo, o, g))
@@ -678,6 +688,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.w = w;
   a.tin = car;
   a.den = den;
+  a.nrm_out = nrm;
   switch (g.P) {
     case 1: return launch(k_causal_fwd<1>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
     case 2: return launch(k_causal_fwd<2>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);

@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int64_t nitems = a.BH * a.nseg;
+  if (warp >= 2) {  // masked blocks of E~ are never written: zero them once
+    for (int i = threadIdx.x - 64; i < TILE / 16; i += 128)
+      reinterpret_cast<uint4*>(smem + OFF_ET)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
 
   if (warp == 0) {
     if (elect_one()) {
@@ -238,10 +243,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
         const uint32_t par = gc & 1;
         const bool valid = t + r < m.t1;
+        float2 sq2 = make_float2(0.f, 0.f);
+        if (a.nrm_in && valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
         mbar_wait(fullQ, par);
         mbar_wait(fullK, par);
-        const Scale scq = row_scale(tile_row_sumsq(sb + OFF_Q, r), a.normalize);
-        const Scale sck = row_scale(tile_row_sumsq(sb + OFF_K, r), a.normalize);
+        if (!a.nrm_in) sq2 = make_float2(tile_row_sumsq(sb + OFF_Q, r), tile_row_sumsq(sb + OFF_K, r));
+        const Scale scq = row_scale(sq2.x, a.normalize);
+        const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_arrive(emptyK);
         mbar_wait(c1, par);
         tc_fence_after();
@@ -270,8 +278,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(c2, par);
         tc_fence_after();
         float rs = 0.f, nd = 0.f;
+        const int qw = warp & 3;  // this warp's rows are 32qw..32qw+31: column blocks > qw are masked out
 #pragma unroll
         for (int c0 = 0; c0 < CH; c0 += 32) {
+          if ((c0 >> 5) > qw) continue;  // warp-uniform: the whole block is above the diagonal
           float pm[32], e[32];
           tmem_ld32(tmem + lane_base() + TM_PMC + c0, pm);
           tmem_ld32(tmem + lane_base() + TM_E + c0, e);
@@ -290,6 +300,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // E~ = tril(E - rho) -> bf16 A operand
 #pragma unroll
         for (int c0 = 0; c0 < CH; c0 += 32) {
+          if ((c0 >> 5) > qw) continue;  // stays zero from the kernel prologue
           float e[32];
           tmem_ld32(tmem + lane_base() + TM_E + c0, e);
           tmem_ld_wait();
@@ -447,6 +458,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int64_t nitems = a.BH * a.nseg;
+  if (warp >= 2) {  // masked blocks of EG~ are never written: zero them once
+    for (int i = threadIdx.x - 64; i < TILE / 16; i += 128)
+      reinterpret_cast<uint4*>(smem + OFF_EG)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
 
   if (warp == 0) {
     if (elect_one()) {
@@ -586,10 +602,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // chunk finished reading it before its final compute_bar)
         const float rd_ld = valid ? rden[m.bh * a.N + t + r] : 0.f;
         const float gd_ld = valid ? gden[m.bh * a.N + t + r] : 0.f;
+        float2 sq2 = make_float2(0.f, 0.f);
+        if (a.nrm_in && valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
         mbar_wait(fullQ, par);
         mbar_wait(fullK, par);
-        const Scale scq = row_scale(tile_row_sumsq(sb + OFF_Q, r), a.normalize);
-        const Scale sck = row_scale(tile_row_sumsq(sb + OFF_K, r), a.normalize);
+        if (!a.nrm_in) sq2 = make_float2(tile_row_sumsq(sb + OFF_Q, r), tile_row_sumsq(sb + OFF_K, r));
+        const Scale scq = row_scale(sq2.x, a.normalize);
+        const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_arrive(emptyQ);
         rg[r] = rd_ld;
         rg[128 + r] = gd_ld;
@@ -613,8 +632,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ---- EG~ (from E^T) and P~^T (from Pm^T), masked t >= i
         mbar_wait(c2, par);
         tc_fence_after();
+        const int qw = warp & 3;  // rows 32qw..32qw+31: column blocks < qw are masked out (t < i)
 #pragma unroll
         for (int c0 = 0; c0 < CH; c0 += 32) {
+          if ((c0 >> 5) < qw) {  // warp-uniform: EG~ block stays zero from the prologue
+            float z[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] = 0.f;
+            stage_row_bf16(sb + OFF_V, r, z, c0);
+            continue;
+          }
           float e[32], pm[32];
           tmem_ld32(tmem + lane_base() + TM_E + c0, e);
           tmem_ld32(tmem + lane_base() + TM_PMC + c0, pm);
@@ -705,8 +732,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // ---- entry points ------------------------------------------------------------
 cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
-                            const float* w, const float* car, void* dq, float* rden, float* gden, float* dpart,
-                            cudaStream_t st) {
+                            const float* w, const float* car, const float* nrm, void* dq, float* rden, float* gden,
+                            float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdq;
   if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mdo, d_o, g) ||
@@ -716,6 +743,7 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.w = w;
   a.tin = car;
   a.tout = dpart;
+  a.nrm_in = nrm;
   switch (g.P) {
     case 1: return launch(k_bwd_causal_q<1>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
     case 2: return launch(k_bwd_causal_q<2>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
@@ -724,8 +752,8 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
 }
 
 cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
-                            const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
-                            void* dv, cudaStream_t st) {
+                            const float* w, const float* rden, const float* gden, const float* dcar,
+                            const float* nrm, void* dk, void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
   if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mdo, d_o, g) ||
@@ -734,6 +762,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   Args a = make_args(g);
   a.w = w;
   a.tin = dcar;
+  a.nrm_in = nrm;
   switch (g.P) {
     case 1: return launch(k_bwd_causal_k<1>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);
     case 2: return launch(k_bwd_causal_k<2>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);

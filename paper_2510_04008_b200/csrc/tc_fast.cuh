@@ -39,6 +39,8 @@ struct Args {
   const float* tin;   // tables / carries
   float* tout;        // partial tables
   float* den;
+  const float* nrm_in;  // [BH, N, 2] row sums of squares (q, k) saved by the causal forward, or null
+  float* nrm_out;
 };
 
 #define RACE_DBG(a_, slot_, val_)                                                        \
@@ -432,6 +434,274 @@ __device__ __forceinline__ void tangent_row_inplace(uint32_t tmem_col, uint32_t 
       st_shared_v4(addr, o[0], o[1], o[2], o[3]);
     }
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// 8-compute-warp helpers (warps 2..9): warp w and w+4 share TMEM lane quarter
+// w % 4 (rows), and split the 128 columns into halves h = 0 / 1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int chalf() { return warp_id() >= 6 ? 1 : 0; }
+__device__ __forceinline__ void cbar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void hbar128(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
+
+// sum of squares over columns [64h, 64h + 64) of row r (= SW128 sub-tile h)
+__device__ __forceinline__ float half_row_sumsq(uint32_t tile, int r, int h) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 v = ld_shared_v4(tile + h * SUB + r * 128 + ((j ^ (r & 7)) << 4));
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = bf16_lo(w4[q]), b = bf16_hi(w4[q]);
+      s0 = fmaf(a, a, s0);
+      s1 = fmaf(b, b, s1);
+    }
+  }
+  return s0 + s1;
+}
+
+// copy half h of row r between two SW128 tiles (same swizzle => same offsets)
+__device__ __forceinline__ void copy_half_row(uint32_t dst, uint32_t src, int r, int h) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t off = h * SUB + r * 128 + (j << 4);
+    const uint4 v = ld_shared_v4(src + off);
+    st_shared_v4(dst + off, v.x, v.y, v.z, v.w);
+  }
+}
+
+// sum of 8 values over the 128 threads of half h (4 warps), fixed order; all get the total
+__device__ __forceinline__ void hsum8(float* v, float* scratch, int h) {
+#pragma unroll
+  for (int f = 0; f < FP; ++f) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
+  }
+  float* sc = scratch + h * 4 * FP;
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int f = 0; f < FP; ++f) sc[(warp_id() & 3) * FP + f] = v[f];
+  }
+  hbar128(h);
+#pragma unroll
+  for (int f = 0; f < FP; ++f) v[f] = ((sc[f] + sc[FP + f]) + sc[2 * FP + f]) + sc[3 * FP + f];
+}
+
+// one-pass tangent VJP for columns [64h, 64h + 64) of row r; bf16 result straight to global
+__device__ __forceinline__ void tangent_half_to_global(uint32_t tmem_col, uint32_t tile, int r, int h, Scale sc,
+                                                       float dot_hat, __nv_bfloat16* grow, bool store) {
+  const float cx = sc.tangent ? dot_hat * sc.inv : 0.f;
+#pragma unroll
+  for (int c0 = 0; c0 < 64; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem_col + 64 * h + c0, v);
+    tmem_ld_wait();
+    uint32_t o[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int chunk = 8 * h + (c0 >> 3) + j;
+      const uint4 x = ld_shared_v4(tile + h * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4));
+      const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float a = sc.tangent ? (v[8 * j + 2 * q] - cx * bf16_lo(xw[q])) * sc.inv : v[8 * j + 2 * q];
+        const float b = sc.tangent ? (v[8 * j + 2 * q + 1] - cx * bf16_hi(xw[q])) * sc.inv : v[8 * j + 2 * q + 1];
+        o[4 * j + q] = pack_bf16(a, b);
+      }
+    }
+    if (store) {
+      uint4* dst = reinterpret_cast<uint4*>(grow + 64 * h + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+    }
+  }
+}
+
+// TMEM columns [64h, 64h + 64) of row r -> bf16 global row
+__device__ __forceinline__ void tmem_half_to_global(uint32_t tmem_col, int h, float scale, __nv_bfloat16* grow,
+                                                    bool store) {
+#pragma unroll
+  for (int c0 = 0; c0 < 64; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem_col + 64 * h + c0, v);
+    tmem_ld_wait();
+    if (store) {
+      uint4* dst = reinterpret_cast<uint4*>(grow + 64 * h + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        dst[j] = make_uint4(pack_bf16(v[8 * j] * scale, v[8 * j + 1] * scale),
+                            pack_bf16(v[8 * j + 2] * scale, v[8 * j + 3] * scale),
+                            pack_bf16(v[8 * j + 4] * scale, v[8 * j + 5] * scale),
+                            pack_bf16(v[8 * j + 6] * scale, v[8 * j + 7] * scale));
+    }
+  }
+}
+
+// W' / W'' builds spread over the 256 compute threads
+__device__ __forceinline__ void build_ops_256(const Args& a, int64_t bh, uint32_t wop, uint32_t w2) {
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  const int tid = threadIdx.x - 64;
+  for (int idx = tid; idx < 16 * 16 + 32 * 16; idx += 256) {
+    uint32_t pk[4];
+    uint32_t off, base;
+    if (idx < 256) {  // W' row n = 3j + piece
+      const int n = idx >> 4, j = idx & 15, hp = n / 3, piece = n % 3;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v2[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float v = 0.f;
+          if (hp < a.TP) {
+            const float x = w[hp * DH + j * 8 + e * 2 + hh];
+            const float hi = bf16_round(x);
+            const float mid = bf16_round(x - hi);
+            v = piece == 0 ? hi : piece == 1 ? mid : bf16_round(x - hi - mid);
+          }
+          v2[hh] = v;
+        }
+        pk[e] = pack_bf16(v2[0], v2[1]);
+      }
+      off = (j >> 3) * 2048 + n * 128 + (((j & 7) ^ (n & 7)) << 4);
+      base = wop;
+    } else {  // W'' K-row k = 8 blk + hp
+      const int i2 = idx - 256, k = i2 >> 4, j = i2 & 15, blk = k >> 3, hp = k & 7;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v2[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float v = 0.f;
+          if (blk < 3 && hp < a.TP) {
+            const float x = w[hp * DH + j * 8 + e * 2 + hh];
+            const float hi = bf16_round(x);
+            v = blk == 2 ? x - hi : hi;
+          }
+          v2[hh] = v;
+        }
+        pk[e] = pack_bf16(v2[0], v2[1]);
+      }
+      off = (j >> 3) * 4096 + k * 128 + (((j & 7) ^ (k & 7)) << 4);
+      base = w2;
+    }
+    st_shared_v4(base + off, pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// S^T operand column c, only f in [f0, f0 + 4) (the two halves split the 8 rows)
+__device__ __forceinline__ void write_sopT_half(uint32_t buf, int c, const float* s, int f0) {
+  const uint32_t sub = (c >> 6) * 2048;
+  const uint32_t inrow = (c & 63) * 2;
+#pragma unroll
+  for (int ff = 0; ff < 4; ++ff) {
+    const int f = f0 + ff;
+    const float hi = bf16_round(s[f]);
+    const __nv_bfloat16 bh = __float2bfloat16_rn(hi), bl = __float2bfloat16_rn(s[f] - hi);
+    const uint32_t o1 = f * 128 + inrow, o2 = (8 + f) * 128 + inrow;
+    const uint32_t p1 = sub + (o1 ^ (((o1 >> 7) & 7) << 4)), p2 = sub + (o2 ^ (((o2 >> 7) & 7) << 4));
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + p1), "h"(*reinterpret_cast<const unsigned short*>(&bh)) : "memory");
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + p2), "h"(*reinterpret_cast<const unsigned short*>(&bl)) : "memory");
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// pointer-based variants of the row helpers: plain C++ shared-memory accesses
+// (LDS/STS the compiler may batch and reorder), for the hot loops
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int chunk) {
+  return reinterpret_cast<uint4*>(tile + (chunk >> 3) * SUB + r * 128 + (((chunk & 7) ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ float half_row_sumsq_p(uint8_t* tile, int r, int h) {
+  uint4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = *tile_chunk(tile, r, 8 * h + j);
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = bf16_lo(w4[q]), b = bf16_hi(w4[q]);
+      s0 = fmaf(a, a, s0);
+      s1 = fmaf(b, b, s1);
+    }
+  }
+  return s0 + s1;
+}
+__device__ __forceinline__ void copy_half_row_p(uint8_t* dst, uint8_t* src, int r, int h) {
+  uint4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = *tile_chunk(src, r, 8 * h + j);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) *tile_chunk(dst, r, 8 * h + j) = v[j];
+}
+// 32 fp32 values (columns [c0, c0 + 32)) -> bf16 into row r of a SW128 tile
+__device__ __forceinline__ void stage32_p(uint8_t* tile, int r, const float* v, int c0) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *tile_chunk(tile, r, (c0 >> 3) + j) =
+        make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                   pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+}
+// tangent VJP on 32 columns [c0, c0 + 32) given the dx^ values v; x from the tile
+__device__ __forceinline__ void tangent32(const float* v, uint8_t* tile, int r, int c0, Scale sc, float cx,
+                                          uint32_t* o) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 x = *tile_chunk(tile, r, (c0 >> 3) + j);
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = sc.tangent ? (v[8 * j + 2 * q] - cx * bf16_lo(xw[q])) * sc.inv : v[8 * j + 2 * q];
+      const float b = sc.tangent ? (v[8 * j + 2 * q + 1] - cx * bf16_hi(xw[q])) * sc.inv : v[8 * j + 2 * q + 1];
+      o[4 * j + q] = pack_bf16(a, b);
+    }
+  }
+}
+__device__ __forceinline__ void st_global16(__nv_bfloat16* dst, const uint32_t* o) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) d[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+}
+// columns [64h, 64h + 64): dx = tangent(dx^) straight to global (TMEM loads double-buffered)
+__device__ __forceinline__ void tangent_half_p(uint32_t tmem_col, uint8_t* tile, int r, int h, Scale sc,
+                                               float dot_hat, __nv_bfloat16* grow, bool store) {
+  const float cx = sc.tangent ? dot_hat * sc.inv : 0.f;
+  float v0[32], v1[32];
+  uint32_t o[16];
+  tmem_ld32(tmem_col + 64 * h, v0);
+  tmem_ld_wait();
+  tmem_ld32(tmem_col + 64 * h + 32, v1);
+  tangent32(v0, tile, r, 64 * h, sc, cx, o);
+  if (store) st_global16(grow + 64 * h, o);
+  tmem_ld_wait();
+  tangent32(v1, tile, r, 64 * h + 32, sc, cx, o);
+  if (store) st_global16(grow + 64 * h + 32, o);
+}
+// TMEM columns [64h, 64h + 64) -> bf16 global row (double-buffered TMEM loads)
+__device__ __forceinline__ void tmem_half_to_global_p(uint32_t tmem_col, int h, __nv_bfloat16* grow, bool store) {
+  float v0[32], v1[32];
+  uint32_t o[16];
+  tmem_ld32(tmem_col + 64 * h, v0);
+  tmem_ld_wait();
+  tmem_ld32(tmem_col + 64 * h + 32, v1);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j] = pack_bf16(v0[2 * j], v0[2 * j + 1]);
+  if (store) st_global16(grow + 64 * h, o);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j] = pack_bf16(v1[2 * j], v1[2 * j + 1]);
+  if (store) st_global16(grow + 64 * h + 32, o);
+}
+// row r of a [128 x 32] SW64 operand from four 8-element blocks
+__device__ __forceinline__ void write_row32_p(uint8_t* buf, int r, const uint32_t (*blk)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<uint4*>(buf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+        make_uint4(blk[j][0], blk[j][1], blk[j][2], blk[j][3]);
 }
 
 // ---------------------------------------------------------------------------

@@ -99,12 +99,13 @@ def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
                                           _stream()), "race_fwd_readout")
         return o, den, tables.view(pr.state_shape())
     carry = comm.carry(local, "prefix")
-    carries = torch.empty((pr.bh, pr.nseg, E), dtype=torch.float32, device=dev)
+    state = torch.empty(pr.state_shape(), dtype=torch.float32, device=dev)
+    carries, norms = pr.split_causal_state(state)
     if pr.n:
         _combine(pr, _lib.COMBINE_PREFIX, part, carry, carries)
         _lib.check(L.race_fwd_causal(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(carries), _vp(o), _vp(den),
-                                     _vp(ws), _stream()), "race_fwd_causal")
-    return o, den, carries.view(pr.state_shape())
+                                     _vp(norms), _vp(ws), _stream()), "race_fwd_causal")
+    return o, den, state
 
 
 def sharded_backward(q, k, v, w, d_o, p: SketchParams, state, group=None, comm=None):
@@ -131,9 +132,10 @@ def sharded_backward(q, k, v, w, d_o, p: SketchParams, state, group=None, comm=N
         return dq, dk, dv
     rden = torch.empty((pr.bh, max(pr.n, 1)), dtype=torch.float32, device=dev)
     gden = torch.empty_like(rden)
+    carries, norms = pr.split_causal_state(state)
     if pr.n:
-        _lib.check(L.race_bwd_causal_q(pr.dref, _vp(q), _vp(k), _vp(v), _vp(d_o), _vp(pr.w), _vp(state),
-                                       _vp(dq), _vp(rden), _vp(gden), _vp(dpart), _vp(ws), _stream()),
+        _lib.check(L.race_bwd_causal_q(pr.dref, _vp(q), _vp(k), _vp(v), _vp(d_o), _vp(pr.w), _vp(carries),
+                                       _vp(norms), _vp(dq), _vp(rden), _vp(gden), _vp(dpart), _vp(ws), _stream()),
                    "race_bwd_causal_q")
         _combine(pr, _lib.COMBINE_TOTAL, dpart, None, local)
     carry = comm.carry(local, "suffix")
@@ -141,7 +143,7 @@ def sharded_backward(q, k, v, w, d_o, p: SketchParams, state, group=None, comm=N
         dcar = torch.empty((pr.bh, pr.nseg, E), dtype=torch.float32, device=dev)
         _combine(pr, _lib.COMBINE_SUFFIX, dpart, carry, dcar)
         _lib.check(L.race_bwd_causal_k(pr.dref, _vp(q), _vp(k), _vp(v), _vp(d_o), _vp(pr.w), _vp(rden),
-                                       _vp(gden), _vp(dcar), _vp(dk), _vp(dv), _vp(ws), _stream()),
+                                       _vp(gden), _vp(dcar), _vp(norms), _vp(dk), _vp(dv), _vp(ws), _stream()),
                    "race_bwd_causal_k")
     return dq, dk, dv
 
