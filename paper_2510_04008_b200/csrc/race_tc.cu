@@ -616,6 +616,410 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// K3, pipelined 8-compute-warp version (the one launched).
+//
+// Warps: 0 = TMA producer AND O-store issuer, 1 = MMA issuer, 2..9 = compute.
+// Warp w and w + 4 share TMEM lane quarter w % 4 (token rows) and split each
+// 128-column pass into halves h = chalf(): h = 0 owns the q-row norm and
+// columns 0..63; h = 1 the k-row norm, columns 64..127, the S operand and the
+// chunk total of phi_k.
+//
+// Each CTA walks a CONTIGUOUS range of (b*h, segment) items, so the bucket
+// state S / A simply continues in TMEM / registers from one segment to the
+// next; carries are loaded only when the range starts or crosses into a new
+// sequence.
+//
+// Buffer recycling is what bounds this kernel, so each tile is released as
+// early as possible: the Q and K tiles of chunk c only feed the projection MMA
+// and the row norms (computed one chunk ahead, while the previous numerator
+// MMA runs), so they are refilled with chunk c + 2 right after proj(c); the
+// intra-chunk weights P~ = tril(Phi_q Phi_k^T) go to TMEM and enter the
+// numerator MMA as its A operand (tcgen05.mma [d], [a], b); O is staged in
+// the V tile once the numerator MMA has consumed it, and the producer issues
+// the TMA store itself just before refilling that tile.
+// ---------------------------------------------------------------------------
+namespace cfw8 {
+using cfw::STAGES;
+using cfw::STAGE_BYTES;
+using cfw::OFF_STAGE;
+using cfw::OFF_W;
+using cfw::OFF_PHIQ;
+using cfw::OFF_PHIK;
+using cfw::OFF_SOP;
+constexpr int OFF_X = cfw::OFF_BAR;  // [2 parity] x { sq[2][128], rs[2][128], kp[4][8] } floats
+constexpr int XPAR = 256 + 256 + 32;
+constexpr int OFF_BAR = OFF_X + 2 * XPAR * 4;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr uint32_t TM_PA = 192;  // P~ as bf16 pairs: 128 lanes x 64 columns
+static_assert(SMEM <= 232448, "k_causal_fwd8 shared memory");
+}  // namespace cfw8
+
+// contiguous item range of this CTA: [i0, i1)
+__device__ __forceinline__ void cta_range(int64_t nitems, int64_t& i0, int64_t& i1) {
+  i0 = int64_t(blockIdx.x) * nitems / gridDim.x;
+  i1 = int64_t(blockIdx.x + 1) * nitems / gridDim.x;
+}
+// chunk cursor over a CTA's item range
+struct Cursor {
+  int64_t it, i1, t;
+  Item m;
+  __device__ __forceinline__ void start(const Args& a, int64_t i0, int64_t i1_) {
+    it = i0;
+    i1 = i1_;
+    if (it < i1) {
+      m = item_of(a, it);
+      t = m.t0;
+    }
+  }
+  __device__ __forceinline__ bool ok() const { return it < i1; }
+  __device__ __forceinline__ void next(const Args& a) {
+    t += CH;
+    if (t >= m.t1) {
+      ++it;
+      if (it < i1) {
+        m = item_of(a, it);
+        t = m.t0;
+      }
+    }
+  }
+};
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_causal_fwd8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Args a) {
+  using namespace cfw8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* fullqk = bars;       // [2]  Q, K bytes landed
+  uint64_t* fullv = bars + 2;    // [2]  V bytes landed
+  uint64_t* emptyqk = bars + 4;  // [2]  proj MMA done (commit) + row norms done (1 arrive)
+  uint64_t* ostaged = bars + 6;  // [2]  O staged in the V tile (256 arrivals)
+  uint64_t* proj_full = bars + 8;
+  uint64_t* phi_full = bars + 9;
+  uint64_t* pm_full = bars + 10;
+  uint64_t* pt_full = bars + 11;
+  uint64_t* num_full = bars + 12;
+  uint64_t* wready = bars + 13;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&fullqk[i], 1);
+      mbar_init(&fullv[i], 1);
+      mbar_init(&emptyqk[i], 2);
+      mbar_init(&ostaged[i], 256);
+    }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 256);
+    mbar_init(pm_full, 1);
+    mbar_init(pt_full, 256);
+    mbar_init(num_full, 1);
+    mbar_init(wready, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmO);
+      const uint64_t pol = policy_evict_first();
+      int64_t ot0 = 0, ob0 = 0, ot1 = 0, ob1 = 0;  // coordinates of the O tile held by each stage
+      auto store_o = [&](uint32_t j) {             // O of chunk j (V tile of stage j & 1)
+        const int s = j & 1;
+        mbar_wait(&ostaged[s], (j >> 1) & 1);
+        const int ot = int(s ? ot1 : ot0), ob = int(s ? ob1 : ob0);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE + h * SUB),
+                       h * 64, ot, ob);
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc & 1;
+        uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&emptyqk[s], ((gc >> 1) & 1) ^ 1);
+        RACE_TRACE(a, 0, gc);
+        mbar_arrive_expect_tx(&fullqk[s], 2 * TILE);
+        for (int h = 0; h < 2; ++h) {
+          tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+          tma_load_3d(st + TILE + h * SUB, &tmK, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+        }
+        if (gc >= 2) {
+          store_o(gc - 2);
+          tma_store_wait_read<0>();
+        }
+        RACE_TRACE(a, 9, gc);
+        mbar_arrive_expect_tx(&fullv[s], TILE);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(st + 2 * TILE + h * SUB, &tmV, &fullv[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+        if (s) { ot1 = cur.t; ob1 = cur.m.bh; } else { ot0 = cur.t; ob0 = cur.m.bh; }
+      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_o(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0;
+    int64_t prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {  // compute warps (re)built W, S, A for this sequence
+        prev_bh = m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+        tc_fence_after();
+      }
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc & 1;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&fullqk[s], (gc >> 1) & 1);
+        RACE_TRACE(a, 1, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          }
+          umma_commit(proj_full);
+          umma_commit(&emptyqk[s]);
+        }
+        __syncwarp();
+        mbar_wait(phi_full, gc & 1);
+        RACE_TRACE(a, 2, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_PM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), ID_PM, kk > 0);
+        }
+        __syncwarp();
+        mbar_wait(&fullv[s], (gc >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + 2 * TILE, kk), desc_phi_mn(sb + OFF_PHIK, kk), ID_STATE, 1u);
+          umma_commit(pm_full);
+        }
+        __syncwarp();
+        mbar_wait(pt_full, gc & 1);
+        RACE_TRACE(a, 3, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_NUM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts(tmem + TM_NUM, tmem + TM_PA + kk * 8, desc_tile_mn(stage + 2 * TILE, kk), ID_NUMB, 1u);
+          umma_commit(num_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const int qw = warp & 3;  // lane quarter: rows 32qw..32qw+31
+    const uint32_t lb = lane_base();
+    const float invT = 1.f / float(a.T);
+    const int F = a.T << a.P;
+    float* xbase = reinterpret_cast<float*>(smem + OFF_X);
+    {  // P~ blocks above the diagonal are never written: zero the A operand once
+      uint32_t z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0u;
+      tmem_st16u(tmem + lb + TM_PA + 32 * h, z);
+      tmem_st16u(tmem + lb + TM_PA + 32 * h + 16, z);
+      tmem_st_wait();
+    }
+    float A[FP], snext[FP];
+    float sqq = 0.f, sqk = 0.f;  // row norms^2 of the current chunk
+    uint32_t gc = 0;
+    int64_t prev_bh = -1;
+    Cursor cur;
+    cur.start(a, i0, i1);
+    if (cur.ok()) {  // norms of the very first chunk
+      mbar_wait(&fullqk[0], 0);
+      const float sq = tile_row_sumsq(sb + OFF_STAGE + h * TILE, r);
+      xbase[h * 128 + r] = sq;
+      if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
+      compute_bar256();
+      if (threadIdx.x == 64) mbar_arrive(&emptyqk[0]);
+      sqq = xbase[r];
+      sqk = xbase[128 + r];
+    }
+    for (; cur.ok(); ++gc) {
+      const Item m = cur.m;
+      const int64_t t = cur.t;
+      const int s = gc & 1;
+      const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+      float* xpar = xbase + (gc & 1) * XPAR;
+      const bool valid = t + r < m.t1;
+      if (m.bh != prev_bh) {  // (re)load the sequence state: W', S_in (TMEM + S operand), A_in
+        prev_bh = m.bh;
+        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
+        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        float srow[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
+          srow[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
+        }
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        if (h == 1) {  // S accumulator (lane r = value column r): cols 0..7 = S_in, the rest 0
+          float z[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = j < FP ? srow[j] : 0.f;
+          tmem_st16(tmem + lb + TM_SACC, z);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = 0.f;
+          tmem_st16(tmem + lb + TM_SACC + 16, z);
+          tmem_st_wait();
+          write_sop(sb + OFF_SOP, r, srow);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(wready);
+        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
+      }
+      const float invq = inv_scale(sqq, a.normalize);
+      const float invk = inv_scale(sqk, a.normalize);
+      mbar_wait(proj_full, gc & 1);
+      if (threadIdx.x == 64) RACE_TRACE(a, 5, gc);
+      tc_fence_after();
+      float phq[FP];
+      if (h == 0) {
+        float pq[16];
+        tmem_ld16(tmem + lb + TM_PROJQ, pq);
+        tmem_ld_wait();
+        row_features<P>(a, pq, invq, valid, phq);
+        write_phi_q(sb + OFF_PHIQ, r, phq);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+      } else {
+        float pq[16], pk[16], phk[FP];
+        tmem_ld16(tmem + lb + TM_PROJK, pk);
+        tmem_ld16(tmem + lb + TM_PROJQ, pq);
+        tmem_ld_wait();
+        row_features<P>(a, pk, invk, valid, phk);
+        write_phi_k(sb + OFF_PHIK, r, phk);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+        // chunk total of phi_k: warp butterfly, per-quarter partials
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) phk[f] += __shfl_xor_sync(0xffffffffu, phk[f], o);
+        }
+        if (lane_id() == 0) {
+#pragma unroll
+          for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
+        }
+        row_features<P>(a, pq, invq, valid, phq);
+      }
+      float D = 0.f;
+#pragma unroll
+      for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
+      // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 pairs into TMEM (my 64 columns)
+      mbar_wait(pm_full, gc & 1);
+      if (threadIdx.x == 64) RACE_TRACE(a, 6, gc);
+      tc_fence_after();
+      float rs = 0.f;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 64 * h + 32 * b;
+        if ((c0 >> 5) <= qw) {  // warp-uniform; blocks above the diagonal stay zero
+          float v[32];
+          uint32_t u[16];
+          tmem_ld32(tmem + lb + TM_PM + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = (c0 + j <= r) ? v[j] : 0.f;
+            rs += v[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) u[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+          tmem_st16u(tmem + lb + TM_PA + (c0 >> 1), u);
+        }
+      }
+      xpar[256 + h * 128 + r] = rs;
+      if (h == 1) {
+        float sacc[32];
+        tmem_ld32(tmem + lb + TM_SACC, sacc);  // S_<=c (value column r)
+        tmem_ld_wait();
+#pragma unroll
+        for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(pt_full);
+      // ---- while the numerator MMA runs: row norms of the next chunk
+      cur.next(a);
+      if (cur.ok()) {
+        const int sn = (gc + 1) & 1;
+        mbar_wait(&fullqk[sn], ((gc + 1) >> 1) & 1);
+        const float sq = tile_row_sumsq(sb + OFF_STAGE + sn * STAGE_BYTES + h * TILE, r);
+        xpar[h * 128 + r] = sq;
+        if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
+      }
+      compute_bar256();
+      if (threadIdx.x == 64 && cur.ok()) mbar_arrive(&emptyqk[(gc + 1) & 1]);
+      sqq = xpar[r];
+      sqk = xpar[128 + r];
+      D += xpar[256 + r] + xpar[384 + r];
+      if (h == 0 && valid) a.den[m.bh * a.N + t + r] = D * invT;
+      const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
+      // ---- numerator -> O (my 64 columns, staged in the consumed V tile), next S operand
+      mbar_wait(num_full, gc & 1);
+      if (threadIdx.x == 64) RACE_TRACE(a, 7, gc);
+      tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 64 * h + 32 * b;
+        float v[32];
+        tmem_ld32(tmem + lb + TM_NUM + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= rD;
+        stage_row_bf16(stage + 2 * TILE, r, v, c0);
+      }
+      if (h == 1) write_sop(sb + OFF_SOP, r, snext);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&ostaged[s]);
+      if (threadIdx.x == 64) RACE_TRACE(a, 8, gc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+
 static unsigned* g_dbg_host = nullptr;
 static unsigned* g_dbg_dev = nullptr;
 unsigned* debug_progress_device() {
@@ -689,6 +1093,14 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.tin = car;
   a.den = den;
   a.nrm_out = nrm;
+  const char* v1 = getenv("RACE_FWD_V1");
+  if (!(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch_nt(k_causal_fwd8<1>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+      case 2: return launch_nt(k_causal_fwd8<2>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+      default: return launch_nt(k_causal_fwd8<3>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_causal_fwd<1>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
     case 2: return launch(k_causal_fwd<2>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);

@@ -23,6 +23,7 @@ constexpr int TILE = 2 * SUB;        // [128 x 128] bf16 tile (32 KB)
 constexpr int WOP = 2 * 16 * 128;    // W' operand: [16 x 128] bf16, 2 SW128 sub-tiles of 2 KB
 constexpr int PHI = CH * 64;         // [128 x 32] bf16 K-major SW64 (8 KB)
 constexpr int NTHREADS = 192;
+constexpr int NTHREADS8 = 320;      // 8-compute-warp kernels: warps 2..9 compute
 constexpr int FP = 8;                // padded feature count
 constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
 
@@ -48,6 +49,25 @@ struct Args {
     if ((a_).dbg) *(volatile unsigned*)&(a_).dbg[blockIdx.x * 256 + (slot_)] = (val_);   \
   } while (0)
 
+// timeline trace of CTA 0 (RACE_DEBUG_PROGRESS=1): slot ev * 32 + chunk holds clock()
+#define RACE_TRACE(a_, ev_, gc_)                                                         \
+  do {                                                                                   \
+    if ((a_).dbg && blockIdx.x == 0 && (gc_) < 32u)                                      \
+      *(volatile unsigned*)&(a_).dbg[(ev_) * 32 + (gc_)] = (unsigned)clock();            \
+  } while (0)
+
+// per-CTA start / end (globaltimer, ns) in the last 2 * 148 words of the debug buffer
+__device__ __forceinline__ unsigned gtimer_lo() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return unsigned(t);
+}
+#define RACE_CTA_TIME(a_, which_)                                                        \
+  do {                                                                                   \
+    if ((a_).dbg && blockIdx.x < 148)                                                    \
+      *(volatile unsigned*)&(a_).dbg[148 * 256 - 2 * 148 + 2 * blockIdx.x + (which_)] = gtimer_lo(); \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // role helpers
 // ---------------------------------------------------------------------------
@@ -55,6 +75,7 @@ __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int crow() { return ((warp_id() & 3) << 5) | lane_id(); }       // compute row
 __device__ __forceinline__ uint32_t lane_base() { return uint32_t((warp_id() & 3) * 32) << 16; }
+__device__ __forceinline__ void compute_bar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -134,9 +155,10 @@ __device__ __forceinline__ float inv_scale(float sumsq, int normalize) {
 }
 
 // W' rows 3j, 3j+1, 3j+2 = W_hi[j], W_mid[j], W_lo[j] (W to 24 bits), K-major SW128
+template <int NTC = 128>
 __device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wop) {
   const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
-  for (int idx = threadIdx.x - 64; idx < 16 * 16; idx += 128) {
+  for (int idx = threadIdx.x - 64; idx < 16 * 16; idx += NTC) {
     const int n = idx >> 4, j = idx & 15;  // row n, 8-element chunk j
     const int hp = n / 3, piece = n % 3;
     uint32_t pk[4];
@@ -272,9 +294,10 @@ constexpr int W2OP = 2 * 32 * 128;  // 8 KB
 __device__ __forceinline__ uint64_t desc_w2(uint32_t base, int kk) {
   return smem_desc(base + kk * 2048, 4096, 1024, kSw128);
 }
+template <int NTC = 128>
 __device__ __forceinline__ void build_w2(const Args& a, int64_t bh, uint32_t w2) {
   const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
-  for (int idx = threadIdx.x - 64; idx < 32 * 16; idx += 128) {
+  for (int idx = threadIdx.x - 64; idx < 32 * 16; idx += NTC) {
     const int k = idx >> 4, j = idx & 15;  // K-row k, 8-element column chunk j
     const int blk = k >> 3, hp = k & 7;
     uint32_t pk[4];
@@ -768,6 +791,14 @@ inline unsigned grid_for(const Geo& g) {
   return unsigned(items < num_sms() ? items : num_sms());
 }
 
+template <typename K, typename... Ts>
+cudaError_t launch_nt(K kernel, int nthreads, int smem, unsigned grid, cudaStream_t st, Ts... args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, nthreads, smem, st>>>(args...);
+  note_launch();
+  return cudaGetLastError();
+}
 template <typename K, typename... Ts>
 cudaError_t launch(K kernel, int smem, unsigned grid, cudaStream_t st, Ts... args) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -57,9 +57,12 @@ __global__ void __launch_bounds__(128) k_selftest(int M, int N, int K, int a_mn,
 
   for (int i = tid; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  for (int i = tid; i < M * K; i += 128) {
-    const int m = i / K, k = i % K;
-    *reinterpret_cast<__nv_bfloat16*>(sa + canon_off(m, k, M, K, a_mn, a_sw)) = A[i];
+  const bool a_tmem = a_sw == 0;  // A from TMEM (columns 128.. of the allocation)
+  if (!a_tmem) {
+    for (int i = tid; i < M * K; i += 128) {
+      const int m = i / K, k = i % K;
+      *reinterpret_cast<__nv_bfloat16*>(sa + canon_off(m, k, M, K, a_mn, a_sw)) = A[i];
+    }
   }
   for (int i = tid; i < N * K; i += 128) {
     const int n = i / K, k = i % K;
@@ -75,11 +78,31 @@ __global__ void __launch_bounds__(128) k_selftest(int M, int N, int K, int a_mn,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (a_tmem) {  // thread = row: pack row tid of A into 32-bit cells (k even in the low half)
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t u[16];
+      for (int j = 0; j < 16; ++j) {
+        const int k = 2 * (c0 + j);
+        const __nv_bfloat16 lo = k < K ? A[tid * K + k] : __float2bfloat16(0.f);
+        const __nv_bfloat16 hi = k + 1 < K ? A[tid * K + k + 1] : __float2bfloat16(0.f);
+        u[j] = uint32_t(*reinterpret_cast<const unsigned short*>(&lo)) |
+               (uint32_t(*reinterpret_cast<const unsigned short*>(&hi)) << 16);
+      }
+      tmem_st16u(tmem + (uint32_t(warp * 32) << 16) + 128 + c0, u);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
   if (tid == 0) {
-    const uint32_t idesc = idesc_bf16(M, N, a_mn, b_mn);
+    const uint32_t idesc = idesc_bf16(M, N, a_tmem ? 0 : a_mn, b_mn);
     for (int kk = 0; kk < K / 16; ++kk) {
-      umma_bf16(tmem, operand_desc(smem_u32(sa), kk, M, K, a_mn, a_sw), operand_desc(smem_u32(sb), kk, N, K, b_mn, b_sw),
-                idesc, kk > 0);
+      if (a_tmem)
+        umma_bf16_ts(tmem, tmem + 128 + kk * 8, operand_desc(smem_u32(sb), kk, N, K, b_mn, b_sw), idesc, kk > 0);
+      else
+        umma_bf16(tmem, operand_desc(smem_u32(sa), kk, M, K, a_mn, a_sw),
+                  operand_desc(smem_u32(sb), kk, N, K, b_mn, b_sw), idesc, kk > 0);
     }
     umma_commit(bar);
   }
@@ -102,7 +125,7 @@ __global__ void __launch_bounds__(128) k_selftest(int M, int N, int K, int a_mn,
 
 extern "C" int tc_selftest_gemm(int M, int N, int K, int a_mn, int b_mn, int a_sw, int b_sw, const void* A,
                                 const void* B, float* D, void* stream) {
-  if (M != 128 || N % 16 || N < 16 || N > 256 || K % 16 || K > 128) return 1;
+  if (M != 128 || N % 16 || N < 16 || N > 128 || K % 16 || K > 128) return 1;
   if (M * K * 2 > 32768 || N * K * 2 > 32768) return 1;
   const size_t smem = 65536 + 128;
   cudaFuncSetAttribute(k_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

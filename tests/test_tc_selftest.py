@@ -28,11 +28,13 @@ COMBOS = [
     (128, 128, 0, 0, 128, 128),  # dO V^T (bwd)
     (32, 128, 1, 1, 128, 128),   # dO^T x Phi~ with Phi in SW128 rows
     (64, 64, 1, 0, 128, 128),
+    (128, 128, 0, 1, 0, 128),    # P~ (A from TMEM) x V (causal forward, tcgen05.mma [d], [a], b)
+    (128, 32, 0, 0, 0, 64),      # A from TMEM x K-major SW64 B
 ]
 
 
-@pytest.mark.parametrize("combo", COMBOS, ids=lambda c: "N%d_K%d_a%s%d_b%s%d" % (
-    c[0], c[1], "MN" if c[2] else "K", c[4], "MN" if c[3] else "K", c[5]))
+@pytest.mark.parametrize("combo", COMBOS, ids=lambda c: "N%d_K%d_a%s%s_b%s%d" % (
+    c[0], c[1], "MN" if c[2] else "K", c[4] or "tmem", "MN" if c[3] else "K", c[5]))
 def test_umma_layouts(combo):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA")
