@@ -30,6 +30,7 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
 cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
                             const float* w, const float* rden, const float* gden, const float* dcar,
                             const float* nrm, void* dk, void* dv, cudaStream_t st);
+cudaError_t tc_rownorms(const Geo& g, const void* q, const void* k, float* nrm, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
                           const float* car, void* o, float* den, float* nrm, cudaStream_t st);
 }  // namespace race
@@ -116,6 +117,7 @@ struct WsLayout {
   float* dtables;  // [BH, nseg, E]
   float* rden;
   float* gden;
+  float* nrm;      // [BH, N, 2] row norms when the caller has no forward state
   size_t bytes;
 };
 
@@ -134,6 +136,7 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
   w.dtables = take(segE);
   w.rden = take(tok);
   w.gden = take(tok);
+  w.nrm = take(2 * tok);
   w.bytes = off;
   return w;
 }
@@ -248,13 +251,19 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v, const 
 int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k, const void* v, const void* d_o,
                       const float* w, const float* carries, const float* rownorms, void* dq, float* rden,
                       float* gden, float* dpart, void* workspace, void* stream) {
-  (void)workspace;
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
-  if (race::tc_supported(g))
+  if (race::tc_supported(g)) {
+    if (!rownorms) {  // recompute the forward's row norms (same summation order)
+      if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
+      float* nrm = ws_layout(g, workspace).nrm;
+      if (int rc = cuda_status(race::tc_rownorms(g, q, k, nrm, S(stream)), "tc_rownorms")) return rc;
+      rownorms = nrm;
+    }
     return cuda_status(race::tc_bwd_causal_q(g, q, k, v, d_o, w, carries, rownorms, dq, rden, gden, dpart, S(stream)),
                        "tc_bwd_causal_q");
+  }
   return cuda_status(race::simt_bwd_causal_q(g, q, k, v, d_o, w, carries, dq, rden, gden, dpart, S(stream)),
                      "bwd_causal_q");
 }
@@ -262,13 +271,19 @@ int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k, con
 int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, const void* v, const void* d_o,
                       const float* w, const float* rden, const float* gden, const float* dcarries,
                       const float* rownorms, void* dk, void* dv, void* workspace, void* stream) {
-  (void)workspace;
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
-  if (race::tc_supported(g))
+  if (race::tc_supported(g)) {
+    if (!rownorms) {
+      if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
+      float* nrm = ws_layout(g, workspace).nrm;
+      if (int rc = cuda_status(race::tc_rownorms(g, q, k, nrm, S(stream)), "tc_rownorms")) return rc;
+      rownorms = nrm;
+    }
     return cuda_status(race::tc_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, rownorms, dk, dv, S(stream)),
                        "tc_bwd_causal_k");
+  }
   return cuda_status(race::simt_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, dk, dv, S(stream)),
                      "bwd_causal_k");
 }
@@ -312,6 +327,10 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     return race_bwd_kside(desc, k, v, w, ws.dtables, dk, dv, workspace, stream);
   }
   const float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
+  if (!nrm && race::tc_supported(g)) {  // once for both passes
+    if (int rc = cuda_status(race::tc_rownorms(g, q, k, ws.nrm, S(stream)), "tc_rownorms")) return rc;
+    nrm = ws.nrm;
+  }
   if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, nrm, dq, ws.rden, ws.gden, ws.dpart, workspace,
                                  stream))
     return rc;

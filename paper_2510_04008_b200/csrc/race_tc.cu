@@ -655,36 +655,6 @@ constexpr uint32_t TM_PA = 192;  // P~ as bf16 pairs: 128 lanes x 64 columns
 static_assert(SMEM <= 232448, "k_causal_fwd8 shared memory");
 }  // namespace cfw8
 
-// contiguous item range of this CTA: [i0, i1)
-__device__ __forceinline__ void cta_range(int64_t nitems, int64_t& i0, int64_t& i1) {
-  i0 = int64_t(blockIdx.x) * nitems / gridDim.x;
-  i1 = int64_t(blockIdx.x + 1) * nitems / gridDim.x;
-}
-// chunk cursor over a CTA's item range
-struct Cursor {
-  int64_t it, i1, t;
-  Item m;
-  __device__ __forceinline__ void start(const Args& a, int64_t i0, int64_t i1_) {
-    it = i0;
-    i1 = i1_;
-    if (it < i1) {
-      m = item_of(a, it);
-      t = m.t0;
-    }
-  }
-  __device__ __forceinline__ bool ok() const { return it < i1; }
-  __device__ __forceinline__ void next(const Args& a) {
-    t += CH;
-    if (t >= m.t1) {
-      ++it;
-      if (it < i1) {
-        m = item_of(a, it);
-        t = m.t0;
-      }
-    }
-  }
-};
-
 template <int P>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_causal_fwd8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -1020,6 +990,31 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 }
 
 
+// row sums of squares of q and k ([BH, N, 2]) in exactly the order the
+// forward's tile_row_sumsq accumulates them, for backward calls without state
+__global__ void __launch_bounds__(256) k_rownorms(const uint4* __restrict__ q, const uint4* __restrict__ k,
+                                                  float* __restrict__ nrm, int64_t rows) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+#pragma unroll
+  for (int which = 0; which < 2; ++which) {
+    const uint4* x = (which ? k : q) + i * 16;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const uint4 v = x[c];
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = bf16_lo(w4[e]), hi = bf16_hi(w4[e]);
+        s0 = fmaf(lo, lo, s0);
+        s1 = fmaf(hi, hi, s1);
+      }
+    }
+    nrm[i * 2 + which] = s0 + s1;
+  }
+}
+
 static unsigned* g_dbg_host = nullptr;
 static unsigned* g_dbg_dev = nullptr;
 unsigned* debug_progress_device() {
@@ -1080,6 +1075,15 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
     case 2: return launch(k_readout<2>, rdo::SMEM, grid_for(g), st, mq, mo, a);
     default: return launch(k_readout<3>, rdo::SMEM, grid_for(g), st, mq, mo, a);
   }
+}
+
+cudaError_t tc_rownorms(const Geo& g, const void* q, const void* k, float* nrm, cudaStream_t st) {
+  const int64_t rows = g.BH * g.N;
+  if (rows == 0) return cudaSuccess;
+  tcfast::k_rownorms<<<unsigned((rows + 255) / 256), 256, 0, st>>>(static_cast<const uint4*>(q),
+                                                                  static_cast<const uint4*>(k), nrm, rows);
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,

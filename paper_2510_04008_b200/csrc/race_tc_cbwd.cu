@@ -13,6 +13,8 @@
 //     dphi_k,i = [v_i | 1] dS_>c^T + sum_{t>=i} (G_t . [v_i | 1]) phi_q,t
 //     dV_i     = phi_k,i dS_>c,v + sum_{t>=i} Pm_ti dO_t / D_t
 // followed by the feature / tanh / sphere-tangent VJPs (shared with race_tc_bwd.cu).
+#include <cstdlib>
+
 #include "tc_fast.cuh"
 
 namespace race {
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int64_t nitems = a.BH * a.nseg;
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
   if (warp >= 2) {  // masked blocks of E~ are never written: zero them once
     for (int i = threadIdx.x - 64; i < TILE / 16; i += 128)
       reinterpret_cast<uint4*>(smem + OFF_ET)[i] = make_uint4(0, 0, 0, 0);
@@ -122,15 +125,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t par = (gc & 1) ^ 1;
           // tiles free up in this order within a chunk: K, V, dO, Q
           mbar_wait(emptyK, par);
+          RACE_TRACE(a, 0, gc);
           mbar_arrive_expect_tx(fullK, TILE);
           for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, int(t), int(m.bh), pol);
           mbar_wait(emptyV, par);
+          RACE_TRACE(a, 1, gc);
           mbar_arrive_expect_tx(fullV, TILE);
           for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, int(t), int(m.bh), pol);
           mbar_wait(emptyO, par);
+          RACE_TRACE(a, 2, gc);
           mbar_arrive_expect_tx(fullO, TILE);
           for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, int(t), int(m.bh), pol);
           mbar_wait(emptyQ, par);
+          RACE_TRACE(a, 3, gc);
           mbar_arrive_expect_tx(fullQ, TILE);
           for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, int(t), int(m.bh), pol);
         }
@@ -148,6 +155,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t par = gc & 1;
         mbar_wait(fullQ, par);
         mbar_wait(fullK, par);
+        RACE_TRACE(a, 4, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -160,6 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         __syncwarp();
         mbar_wait(fullV, par);
         mbar_wait(fullO, par);
+        RACE_TRACE(a, 5, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -171,6 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         __syncwarp();
         mbar_wait(phi_ready, par);
+        RACE_TRACE(a, 6, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -184,6 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         __syncwarp();
         mbar_wait(et_ready, par);
+        RACE_TRACE(a, 7, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -198,6 +209,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         __syncwarp();
         mbar_wait(dp_ready, par);
+        RACE_TRACE(a, 8, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -252,6 +264,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_arrive(emptyK);
         mbar_wait(c1, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
         tc_fence_after();
         float pq[16], pk[16], yv[16];
         tmem_ld16(tmem + lane_base() + TM_PQ, pq);
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         csum8(phk, scratch);  // chunk total of phi_k
         // ---- row statistics from Pm and E
         mbar_wait(c2, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
         tc_fence_after();
         float rs = 0.f, nd = 0.f;
         const int qw = warp & 3;  // this warp's rows are 32qw..32qw+31: column blocks > qw are masked out
@@ -332,6 +346,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         // ---- dphi_q -> dproj
         mbar_wait(c3, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
         tc_fence_after();
         float zz[32];
         tmem_ld32(tmem + lane_base() + TM_Z, zz);
@@ -350,16 +365,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < FP; ++f) A[f] += phk[f];
         // ---- dq in place of q, then store
         mbar_wait(c4, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
         tc_fence_after();
         tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_Q, r, scq, dotq);
         tc_fence_before();
         fence_proxy_async();
         compute_bar();
         if (threadIdx.x == 64) {
+          RACE_TRACE(a, 13, gc);
           for (int h = 0; h < 2; ++h)
             tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + h * SUB), h * 64, int(t), int(m.bh));
           tma_store_commit();
           tma_store_wait_read<0>();
+          RACE_TRACE(a, 14, gc);
           mbar_arrive(emptyQ);
         }
       }
@@ -384,6 +402,460 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ===========================================================================
+// causal backward, query side -- pipelined 8-compute-warp version (launched)
+//
+// Same math as k_bwd_causal_q above; the structure follows k_causal_fwd8:
+// contiguous CTA ranges (S, A continue across segments, dS / dA totals are
+// emitted per segment), compute warps 2..9 split every 128-column pass into
+// halves, E~ = tril(E - rho) lives in TMEM as the A operand of Z = E~ Phi_k,
+// the Q tile is double-buffered and dQ is staged in place and TMA-stored by
+// the producer right before that buffer is refilled.  Row norms come from
+// the forward (rownorms is required).
+// ===========================================================================
+namespace cq8 {
+constexpr int OFF_Q = 0;  // two buffers
+constexpr int OFF_K = 2 * TILE, OFF_V = 3 * TILE, OFF_DO = 4 * TILE;
+constexpr int OFF_W = 5 * TILE;
+constexpr int OFF_W2 = OFF_W + WOP;
+constexpr int OFF_SOPT = OFF_W2 + W2OP;
+constexpr int OFF_PHIQ = OFF_SOPT + WOP;
+constexpr int OFF_PHIK = OFF_PHIQ + PHI;
+constexpr int OFF_PHIT = OFF_PHIK + PHI;
+constexpr int OFF_DPROJ = OFF_PHIT + PHI;
+constexpr int OFF_X = OFF_DPROJ + PHI;  // [2 parity] x { rs[2][128], nd[2][128], kp[4][8] }, then da[4][8]
+constexpr int XPAR = 256 + 256 + 32;
+constexpr int OFF_BAR = OFF_X + (2 * XPAR + 32) * 4;
+constexpr int SMEM = OFF_BAR + 512 + 1024;
+static_assert(SMEM <= 232448, "k_bwd_causal_q8 shared memory");
+constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_ET = 144, TM_PMC = 256,
+                   TM_E = 384, TM_DX = 256;
+}  // namespace cq8
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const __grid_constant__ CUtensorMap tmDQ, Args a, float* __restrict__ rden,
+                    float* __restrict__ gden) {
+  using namespace cq8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* fullQ = bars + 0;     // [2]
+  uint64_t* dqstaged = bars + 2;  // [2] dQ staged in Q buffer (256 arrivals)
+  uint64_t* fullK = bars + 4;
+  uint64_t* fullV = bars + 5;
+  uint64_t* fullO = bars + 6;
+  uint64_t* emptyK = bars + 7;
+  uint64_t* emptyV = bars + 8;
+  uint64_t* emptyO = bars + 9;
+  uint64_t* c1 = bars + 10;
+  uint64_t* c2 = bars + 11;
+  uint64_t* c3 = bars + 12;
+  uint64_t* c4 = bars + 13;
+  uint64_t* phi_ready = bars + 14;
+  uint64_t* et_ready = bars + 15;
+  uint64_t* dp_ready = bars + 16;
+  uint64_t* wready = bars + 17;
+  uint64_t* acc_full = bars + 18;
+  uint64_t* acc_empty = bars + 19;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&fullQ[i], 1);
+      mbar_init(&dqstaged[i], 256);
+    }
+    for (int i = 4; i < 14; ++i) mbar_init(&bars[i], 1);
+    mbar_init(phi_ready, 256);
+    mbar_init(et_ready, 256);
+    mbar_init(dp_ready, 256);
+    mbar_init(wready, 256);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmDO);
+      tma_prefetch_desc(&tmDQ);
+      const uint64_t pol = policy_evict_first();
+      int64_t qt0 = 0, qb0 = 0, qt1 = 0, qb1 = 0;
+      auto store_dq = [&](uint32_t j) {
+        const int s = j & 1;
+        mbar_wait(&dqstaged[s], (j >> 1) & 1);
+        const int qt = int(s ? qt1 : qt0), qb = int(s ? qb1 : qb0);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + s * TILE + h * SUB), h * 64, qt, qb);
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const uint32_t par = (gc & 1) ^ 1;
+        const int s = gc & 1;
+        const int t = int(cur.t), bh = int(cur.m.bh);
+        if (gc >= 2) {
+          store_dq(gc - 2);
+          tma_store_wait_read<0>();
+        }
+        RACE_TRACE(a, 3, gc);
+        mbar_arrive_expect_tx(&fullQ[s], TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + s * TILE + h * SUB, &tmQ, &fullQ[s], h * 64, t, bh, pol);
+        if (s) { qt1 = t; qb1 = bh; } else { qt0 = t; qb0 = bh; }
+        mbar_wait(emptyK, par);
+        RACE_TRACE(a, 0, gc);
+        mbar_arrive_expect_tx(fullK, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
+        mbar_wait(emptyV, par);
+        RACE_TRACE(a, 1, gc);
+        mbar_arrive_expect_tx(fullV, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
+        mbar_wait(emptyO, par);
+        RACE_TRACE(a, 2, gc);
+        mbar_arrive_expect_tx(fullO, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
+      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dq(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0, ni = 0;
+    int64_t prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ni) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
+      tc_fence_after();
+      bool first = true;
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const uint32_t par = gc & 1;
+        const int s = gc & 1;
+        mbar_wait(&fullQ[s], (gc >> 1) & 1);
+        mbar_wait(fullK, par);
+        RACE_TRACE(a, 4, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+            umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          }
+          umma_commit(emptyK);
+        }
+        __syncwarp();
+        mbar_wait(fullV, par);
+        mbar_wait(fullO, par);
+        RACE_TRACE(a, 5, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_DO, kk), desc_tile_k(sb + OFF_V, kk), IDC_E, kk > 0);
+            umma_bf16(tmem + TM_Y, desc_tile_k(sb + OFF_DO, kk), desc_w(sb + OFF_SOPT, kk), IDC_Y, kk > 0);
+          }
+          umma_commit(c1);
+        }
+        __syncwarp();
+        mbar_wait(phi_ready, par);
+        RACE_TRACE(a, 6, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_PMC, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), IDC_PM, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_S, desc_tile_mn(sb + OFF_V, kk), desc_phi_mn(sb + OFF_PHIK, kk), IDC_ST, 1u);
+          umma_commit(c2);
+          umma_commit(emptyV);
+        }
+        __syncwarp();
+        mbar_wait(et_ready, par);
+        RACE_TRACE(a, 7, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16_ts(tmem + TM_Z, tmem + TM_ET + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
+            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST,
+                      (!first || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(c3);
+          umma_commit(emptyO);
+          if (t + CH >= m.t1) umma_commit(acc_full);
+        }
+        __syncwarp();
+        mbar_wait(dp_ready, par);
+        RACE_TRACE(a, 8, gc);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
+          umma_commit(c4);
+        }
+        __syncwarp();
+        first = false;
+      }
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const int qw = warp & 3;
+    const uint32_t lb = lane_base();
+    const float invT = 1.f / float(a.T);
+    const int F = a.T << a.P;
+    float* xbase = reinterpret_cast<float*>(smem + OFF_X);
+    float* xda = xbase + 2 * XPAR;
+    {  // E~ blocks above the diagonal are never written: zero the A operand once
+      uint32_t z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0u;
+      tmem_st16u(tmem + lb + TM_ET + 32 * h, z);
+      tmem_st16u(tmem + lb + TM_ET + 32 * h + 16, z);
+      tmem_st_wait();
+    }
+    float A[FP], dA[FP];
+    uint32_t gc = 0, ni = 0;
+    int64_t prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ni) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {  // (re)load the sequence state
+        prev_bh = m.bh;
+        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        float scol[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
+          scol[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
+        }
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        build_w2<256>(a, m.bh, sb + OFF_W2);
+        if (h == 1) {
+          float z[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = j < FP ? scol[j] : 0.f;
+          tmem_st16(tmem + lb + TM_S, z);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = 0.f;
+          tmem_st16(tmem + lb + TM_S + 16, z);
+          tmem_st_wait();
+          write_sopT(sb + OFF_SOPT, r, scol);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(wready);
+      }
+#pragma unroll
+      for (int f = 0; f < FP; ++f) dA[f] = 0.f;
+      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
+        const uint32_t par = gc & 1;
+        const int s = gc & 1;
+        uint8_t* qtile = smem + OFF_Q + s * TILE;
+        float* xpar = xbase + par * XPAR;
+        const bool valid = t + r < m.t1;
+        float2 sq2 = make_float2(0.f, 0.f);
+        if (valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
+        const Scale scq = row_scale(sq2.x, a.normalize);
+        const Scale sck = row_scale(sq2.y, a.normalize);
+        mbar_wait(c1, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
+        tc_fence_after();
+        float pq[16], yv[16];
+        float phq[FP], uq[5], hq[5];
+        if (h == 0) {
+          tmem_ld16(tmem + lb + TM_PQ, pq);
+          tmem_ld16(tmem + lb + TM_Y, yv);
+          tmem_ld_wait();
+          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+          write_phi_q(sb + OFF_PHIQ, r, phq);
+          fence_proxy_async();
+          tc_fence_before();
+          mbar_arrive(phi_ready);
+        } else {
+          float pk[16], phk[FP], uk[5], hk[5];
+          tmem_ld16(tmem + lb + TM_PK, pk);
+          tmem_ld16(tmem + lb + TM_PQ, pq);
+          tmem_ld16(tmem + lb + TM_Y, yv);
+          tmem_ld_wait();
+          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
+          write_phi_k(sb + OFF_PHIK, r, phk);
+          fence_proxy_async();
+          tc_fence_before();
+          mbar_arrive(phi_ready);
+#pragma unroll
+          for (int f = 0; f < FP; ++f) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) phk[f] += __shfl_xor_sync(0xffffffffu, phk[f], o);
+          }
+          if (lane_id() == 0) {
+#pragma unroll
+            for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
+          }
+          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+        }
+        float y[FP], Dint = 0.f, ydot = 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          y[f] = yv[f] + yv[8 + f];
+          Dint = fmaf(phq[f], A[f], Dint);
+          ydot = fmaf(phq[f], y[f], ydot);
+        }
+        // ---- row statistics from Pm and E over my 64 columns
+        mbar_wait(c2, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
+        tc_fence_after();
+        float rs = 0.f, nd = 0.f;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int c0 = 64 * h + 32 * b;
+          if ((c0 >> 5) <= qw) {  // warp-uniform
+            float pm[32], e[32];
+            tmem_ld32(tmem + lb + TM_PMC + c0, pm);
+            tmem_ld32(tmem + lb + TM_E + c0, e);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float pmj = (c0 + j <= r) ? pm[j] : 0.f;
+              rs += pmj;
+              nd = fmaf(pmj, e[j], nd);
+            }
+          }
+        }
+        xpar[h * 128 + r] = rs;
+        xpar[256 + h * 128 + r] = nd;
+        compute_bar256();
+        const float D = Dint + (xpar[r] + xpar[128 + r]);
+        const float ndt = xpar[256 + r] + xpar[384 + r];
+        const bool live = valid && D * invT > kDegenerateDenEps;
+        const float rD = live ? 1.f / D : 0.f;
+        const float rho = (ydot + ndt) * rD;
+        // E~ = tril(E - rho) -> bf16 pairs into TMEM (A of Z)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int c0 = 64 * h + 32 * b;
+          if ((c0 >> 5) <= qw) {
+            float e[32];
+            uint32_t u[16];
+            tmem_ld32(tmem + lb + TM_E + c0, e);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              u[j] = pack_bf16((c0 + 2 * j <= r) ? e[2 * j] - rho : 0.f,
+                               (c0 + 2 * j + 1 <= r) ? e[2 * j + 1] - rho : 0.f);
+            tmem_st16u(tmem + lb + TM_ET + (c0 >> 1), u);
+          }
+        }
+        if (h == 1) {
+          float pht[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) pht[f] = phq[f] * rD;
+          write_phi_k(sb + OFF_PHIT, r, pht);
+          // S_<=c for the next chunk's y (the Y MMA of this chunk completed at c1)
+          float sacc[32];
+          tmem_ld32(tmem + lb + TM_S, sacc);
+          tmem_ld_wait();
+          float snext[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
+          write_sopT(sb + OFF_SOPT, r, snext);
+        } else {
+#pragma unroll
+          for (int f = 0; f < FP; ++f) dA[f] = fmaf(phq[f], -rho * rD, dA[f]);
+        }
+        tmem_st_wait();
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(et_ready);
+        if (h == 0 && valid) {
+          rden[m.bh * a.N + t + r] = rD;
+          gden[m.bh * a.N + t + r] = -rho * rD;
+        }
+        // ---- dphi_q -> dproj
+        mbar_wait(c3, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
+        tc_fence_after();
+        float zz[32];
+        tmem_ld32(tmem + lb + TM_Z, zz);
+        tmem_ld_wait();
+        float dphi[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
+        float dproj[8];
+        row_feature_vjp<P>(a, uq, phq, dphi, dproj);
+        const float dotq = dot_from_proj(dproj, hq);
+        if (h == 0) write_dproj(sb + OFF_DPROJ, r, dproj);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(dp_ready);
+#pragma unroll
+        for (int f = 0; f < FP; ++f)
+          A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
+        // ---- dq (my 64 columns) in place of q; the producer stores it
+        mbar_wait(c4, par);
+        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
+        tc_fence_after();
+        tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(&dqstaged[s]);
+        if (threadIdx.x == 64) RACE_TRACE(a, 13, gc);
+      }
+      // ---- segment done: dS total (TMEM) and dA total (block reduction)
+      mbar_wait(acc_full, ni & 1);
+      tc_fence_after();
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      if (h == 1) {
+        float acc[32];
+        tmem_ld32(tmem + lb + TM_DS, acc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int f = 0; f < FP; ++f)
+          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+      } else {
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dA[f] += __shfl_xor_sync(0xffffffffu, dA[f], o);
+        }
+        if (lane_id() == 0) {
+#pragma unroll
+          for (int f = 0; f < FP; ++f) xda[qw * FP + f] = dA[f];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      compute_bar256();
+      if (h == 0 && r < F) out[r * LDS_T + DH] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -728,6 +1200,415 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ===========================================================================
+// causal backward, key side -- pipelined 8-compute-warp version (launched)
+//
+// Same math as k_bwd_causal_k above.  Each CTA walks its contiguous item
+// range BACKWARDS (the key side is a suffix scan), so dS_>c and dA continue
+// across segments; compute warps split the column passes into halves; EG~ and
+// P~^T live in TMEM as the A operands of Z = EG~ Phi_q and dV += P~^T dO; the
+// K tile is double-buffered (dK staged in place, TMA-stored by the producer);
+// dV goes straight from TMEM to global memory.  Row norms are required.
+// ===========================================================================
+namespace ck8 {
+constexpr int OFF_K = 0;  // two buffers
+constexpr int OFF_Q = 2 * TILE, OFF_V = 3 * TILE, OFF_DO = 4 * TILE;
+constexpr int OFF_W = 5 * TILE;
+constexpr int OFF_W2 = OFF_W + WOP;
+constexpr int OFF_DSOPT = OFF_W2 + W2OP;   // [16 x 128] B of z = V dS_v^T
+constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // [128 x 32] B of dV_a = Phi_k dS_v
+constexpr int OFF_PHIQ = OFF_DSOP + PHI;   // [hi|hi|lo|0]  B of Pm^T (K) and of Z (MN)
+constexpr int OFF_PHIK = OFF_PHIQ + PHI;   // [hi|lo|hi|0]  A of Pm^T and dV_a
+constexpr int OFF_PHIT = OFF_PHIK + PHI;   // phi_q / D     B of dS (MN)
+constexpr int OFF_DPROJ = OFF_PHIT + PHI;
+constexpr int OFF_X = OFF_DPROJ + PHI;     // [2 parity] x { rd[128], gd[128], dac[4][8] }
+constexpr int XPAR = 256 + 32;
+constexpr int OFF_BAR = OFF_X + 2 * XPAR * 4;
+constexpr int SMEM = OFF_BAR + 512 + 1024;
+static_assert(SMEM <= 232448, "k_bwd_causal_k8 shared memory");
+constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_EG = 128, TM_PT = 192, TM_E = 256,
+                   TM_DX = 256, TM_PMC = 384, TM_DV = 384;
+}  // namespace ck8
+
+// reverse chunk cursor over a CTA's item range (last item, last chunk first)
+struct RCursor {
+  int64_t it, i0, t;
+  Item m;
+  __device__ __forceinline__ void start(const Args& a, int64_t i0_, int64_t i1) {
+    i0 = i0_;
+    it = i1 - 1;
+    if (it >= i0) {
+      m = item_of(a, it);
+      t = m.t0 + ((m.t1 - m.t0 - 1) / CH) * CH;
+    }
+  }
+  __device__ __forceinline__ bool ok() const { return it >= i0; }
+  __device__ __forceinline__ void next(const Args& a) {
+    t -= CH;
+    if (t < m.t0) {
+      --it;
+      if (it >= i0) {
+        m = item_of(a, it);
+        t = m.t0 + ((m.t1 - m.t0 - 1) / CH) * CH;
+      }
+    }
+  }
+};
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const __grid_constant__ CUtensorMap tmDK, Args a, const float* __restrict__ rden,
+                    const float* __restrict__ gden, __nv_bfloat16* __restrict__ dvout) {
+  using namespace ck8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* fullK = bars + 0;     // [2]
+  uint64_t* dkstaged = bars + 2;  // [2]
+  uint64_t* fullQ = bars + 4;
+  uint64_t* fullV = bars + 5;
+  uint64_t* fullO = bars + 6;
+  uint64_t* emptyQ = bars + 7;
+  uint64_t* emptyV = bars + 8;
+  uint64_t* emptyO = bars + 9;
+  uint64_t* projf = bars + 10;
+  uint64_t* c1 = bars + 11;
+  uint64_t* c2 = bars + 12;
+  uint64_t* c3 = bars + 13;
+  uint64_t* c4 = bars + 14;
+  uint64_t* phi_ready = bars + 15;
+  uint64_t* pt_ready = bars + 16;
+  uint64_t* dp_ready = bars + 17;
+  uint64_t* dxfree = bars + 18;
+  uint64_t* wready = bars + 19;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&fullK[i], 1);
+      mbar_init(&dkstaged[i], 256);
+    }
+    for (int i = 4; i < 15; ++i) mbar_init(&bars[i], 1);
+    mbar_init(phi_ready, 256);
+    mbar_init(pt_ready, 256);
+    mbar_init(dp_ready, 256);
+    mbar_init(dxfree, 256);
+    mbar_init(wready, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmDO);
+      tma_prefetch_desc(&tmDK);
+      const uint64_t pol = policy_evict_first();
+      int64_t kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
+      auto store_dk = [&](uint32_t j) {
+        const int s = j & 1;
+        mbar_wait(&dkstaged[s], (j >> 1) & 1);
+        const int kt = int(s ? kt1 : kt0), kb = int(s ? kb1 : kb0);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + s * TILE + h * SUB), h * 64, kt, kb);
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      RCursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const uint32_t par = (gc & 1) ^ 1;
+        const int s = gc & 1;
+        const int t = int(cur.t), bh = int(cur.m.bh);
+        if (gc >= 2) {
+          store_dk(gc - 2);
+          tma_store_wait_read<0>();
+        }
+        mbar_arrive_expect_tx(&fullK[s], TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + s * TILE + h * SUB, &tmK, &fullK[s], h * 64, t, bh, pol);
+        if (s) { kt1 = t; kb1 = bh; } else { kt0 = t; kb0 = bh; }
+        mbar_wait(emptyQ, par);
+        mbar_arrive_expect_tx(fullQ, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, t, bh, pol);
+        mbar_wait(emptyV, par);
+        mbar_arrive_expect_tx(fullV, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
+        mbar_wait(emptyO, par);
+        mbar_arrive_expect_tx(fullO, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
+      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dk(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0;
+    int64_t prev_bh = -1;
+    RCursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      const uint32_t par = gc & 1;
+      const int s = gc & 1;
+      if (cur.m.bh != prev_bh) {
+        prev_bh = cur.m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+        tc_fence_after();
+      }
+      mbar_wait(fullQ, par);
+      mbar_wait(&fullK[s], (gc >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        }
+        umma_commit(projf);
+        umma_commit(emptyQ);
+      }
+      __syncwarp();
+      if (gc > 0) mbar_wait(dxfree, (gc - 1) & 1);  // E aliases the previous chunk's dX
+      mbar_wait(fullV, par);
+      mbar_wait(fullO, par);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + TM_ZV, desc_tile_k(sb + OFF_V, kk), desc_w(sb + OFF_DSOPT, kk), IDC_Y, kk > 0);
+          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
+        }
+        umma_commit(c1);
+        umma_commit(emptyV);
+      }
+      __syncwarp();
+      mbar_wait(phi_ready, par);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+          umma_bf16(tmem + TM_PMC, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_PHIQ, kk), IDC_PM, kk > 0);
+        umma_commit(c2);
+      }
+      __syncwarp();
+      mbar_wait(pt_ready, par);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+          umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), IDC_DVA, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16_ts(tmem + TM_Z, tmem + TM_EG + kk * 8, desc_phi_mn(sb + OFF_PHIQ, kk), IDC_Z, kk > 0);
+          umma_bf16_ts(tmem + TM_DV, tmem + TM_PT + kk * 8, desc_tile_mn(sb + OFF_DO, kk), IDC_DVB, 1u);
+          umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
+        }
+        umma_commit(c3);
+        umma_commit(emptyO);
+      }
+      __syncwarp();
+      mbar_wait(dp_ready, par);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+          umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
+        umma_commit(c4);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const int qw = warp & 3;
+    const uint32_t lb = lane_base();
+    const int F = a.T << a.P;
+    float* xbase = reinterpret_cast<float*>(smem + OFF_X);
+    {  // EG~ / P~^T blocks below the diagonal are never written: zero both A operands once
+      uint32_t z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0u;
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) tmem_st16u(tmem + lb + TM_EG + 64 * h + c, z);
+      tmem_st_wait();
+    }
+    float dA[FP];
+    uint32_t gc = 0;
+    int64_t prev_bh = -1;
+    RCursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      const Item m = cur.m;
+      const int64_t t = cur.t;
+      const uint32_t par = gc & 1;
+      const int s = gc & 1;
+      float* xpar = xbase + par * XPAR;
+      const bool valid = t + r < m.t1;
+      if (m.bh != prev_bh) {  // (re)load the suffix state dS_>seg, dA_>seg and W', W''
+        prev_bh = m.bh;
+        const float* dcar = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        float dcol[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          dcol[f] = f < F ? dcar[f * LDS_T + r] : 0.f;
+          dA[f] = f < F ? dcar[f * LDS_T + DH] : 0.f;
+        }
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        build_w2<256>(a, m.bh, sb + OFF_W2);
+        if (h == 1) {
+          float z[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = j < FP ? dcol[j] : 0.f;
+          tmem_st16(tmem + lb + TM_DS, z);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = 0.f;
+          tmem_st16(tmem + lb + TM_DS + 16, z);
+          tmem_st_wait();
+          write_sopT(sb + OFF_DSOPT, r, dcol);
+          write_sop(sb + OFF_DSOP, r, dcol);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(wready);
+      }
+      // per-query-token normaliser terms of this chunk
+      const float rdr = valid ? rden[m.bh * a.N + t + r] : 0.f;
+      const float gdr = valid ? gden[m.bh * a.N + t + r] : 0.f;
+      float2 sq2 = make_float2(0.f, 0.f);
+      if (valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
+      const Scale scq = row_scale(sq2.x, a.normalize);
+      const Scale sck = row_scale(sq2.y, a.normalize);
+      xpar[h * 128 + r] = h ? gdr : rdr;
+      mbar_wait(projf, par);
+      tc_fence_after();
+      float phq[FP], uq[5], hq[5], phk[FP], uk[5], hk[5];
+      {
+        float pq[16], pk[16];
+        tmem_ld16(tmem + lb + TM_PQ, pq);
+        tmem_ld16(tmem + lb + TM_PK, pk);
+        tmem_ld_wait();
+        if (h == 0) {
+          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+          write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
+        } else {
+          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
+          write_phi_q(sb + OFF_PHIK, r, phk);  // [hi|lo|hi|0]
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_ready);
+        if (h == 0) {
+          float pht[FP], dac[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) {
+            pht[f] = phq[f] * rdr;
+            dac[f] = phq[f] * gdr;
+          }
+          write_phi_k(sb + OFF_PHIT, r, pht);
+#pragma unroll
+          for (int f = 0; f < FP; ++f) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dac[f] += __shfl_xor_sync(0xffffffffu, dac[f], o);
+          }
+          if (lane_id() == 0) {
+#pragma unroll
+            for (int f = 0; f < FP; ++f) xpar[256 + qw * FP + f] = dac[f];
+          }
+          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);  // for dk (off the MMA path)
+        }
+      }
+      compute_bar256();  // rd / gd of every query token, dA partials
+      // ---- EG~ (from E^T) and P~^T (from Pm^T), t >= i, my 64 columns -> TMEM A operands
+      mbar_wait(c1, par);
+      mbar_wait(c2, par);
+      tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 64 * h + 32 * b;
+        if ((c0 >> 5) >= qw) {  // warp-uniform; blocks below the diagonal stay zero
+          float e[32], pm[32];
+          tmem_ld32(tmem + lb + TM_E + c0, e);
+          tmem_ld32(tmem + lb + TM_PMC + c0, pm);
+          tmem_ld_wait();
+          uint32_t ue[16], up[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float ee[2], pp[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int tq = c0 + 2 * j + q;
+              const bool keep = tq >= r;
+              const float rdt = xpar[tq];
+              ee[q] = keep ? fmaf(e[2 * j + q], rdt, xpar[128 + tq]) : 0.f;
+              pp[q] = keep ? pm[2 * j + q] * rdt : 0.f;
+            }
+            ue[j] = pack_bf16(ee[0], ee[1]);
+            up[j] = pack_bf16(pp[0], pp[1]);
+          }
+          tmem_st16u(tmem + lb + TM_EG + (c0 >> 1), ue);
+          tmem_st16u(tmem + lb + TM_PT + (c0 >> 1), up);
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(pt_ready);
+      // ---- dphi_k, dV, next dS operands
+      mbar_wait(c3, par);
+      tc_fence_after();
+      float zz[32], zv[16];
+      tmem_ld32(tmem + lb + TM_Z, zz);
+      tmem_ld16(tmem + lb + TM_ZV, zv);
+      tmem_ld_wait();
+      float dphi[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
+      float dproj[8];
+      row_feature_vjp<P>(a, uk, phk, dphi, dproj);
+      const float dotk = dot_from_proj(dproj, hk);
+      if (h == 1) {
+        write_dproj(sb + OFF_DPROJ, r, dproj);
+        float dsa[32];
+        tmem_ld32(tmem + lb + TM_DS, dsa);
+        tmem_ld_wait();
+        float dsn[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) dsn[f] = dsa[f] + dsa[16 + f];
+        write_sopT(sb + OFF_DSOPT, r, dsn);
+        write_sop(sb + OFF_DSOP, r, dsn);
+      }
+      tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, valid);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(dp_ready);
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
+      // ---- dk (my 64 columns) in place of k; the producer stores it
+      mbar_wait(c4, par);
+      tc_fence_after();
+      tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&dkstaged[s]);
+      mbar_arrive(dxfree);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace tcfast
 
 // ---- entry points ------------------------------------------------------------
@@ -744,6 +1625,14 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.tin = car;
   a.tout = dpart;
   a.nrm_in = nrm;
+  const char* v1 = getenv("RACE_BWDQ_V1");
+  if (nrm && !(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
+      case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
+      default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_bwd_causal_q<1>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
     case 2: return launch(k_bwd_causal_q<2>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
@@ -763,6 +1652,15 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.w = w;
   a.tin = dcar;
   a.nrm_in = nrm;
+  const char* v1 = getenv("RACE_BWDK_V1");
+  if (nrm && !(v1 && v1[0] == '1')) {
+    __nv_bfloat16* dvp = static_cast<__nv_bfloat16*>(dv);
+    switch (g.P) {
+      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
+      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
+      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_bwd_causal_k<1>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);
     case 2: return launch(k_bwd_causal_k<2>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);

@@ -96,6 +96,36 @@ __device__ __forceinline__ Item item_of(const Args& a, int64_t it) {
   return r;
 }
 
+// contiguous item range of this CTA: [i0, i1)
+__device__ __forceinline__ void cta_range(int64_t nitems, int64_t& i0, int64_t& i1) {
+  i0 = int64_t(blockIdx.x) * nitems / gridDim.x;
+  i1 = int64_t(blockIdx.x + 1) * nitems / gridDim.x;
+}
+// chunk cursor over a CTA's item range
+struct Cursor {
+  int64_t it, i1, t;
+  Item m;
+  __device__ __forceinline__ void start(const Args& a, int64_t i0, int64_t i1_) {
+    it = i0;
+    i1 = i1_;
+    if (it < i1) {
+      m = item_of(a, it);
+      t = m.t0;
+    }
+  }
+  __device__ __forceinline__ bool ok() const { return it < i1; }
+  __device__ __forceinline__ void next(const Args& a) {
+    t += CH;
+    if (t >= m.t1) {
+      ++it;
+      if (it < i1) {
+        m = item_of(a, it);
+        t = m.t0;
+      }
+    }
+  }
+};
+
 // operand descriptors ------------------------------------------------------
 // [128 x 128] bf16 tile from TMA (two SW128 sub-tiles), K-major, K-step kk of 16
 __device__ __forceinline__ uint64_t desc_tile_k(uint32_t base, int kk) {
@@ -703,6 +733,24 @@ __device__ __forceinline__ void tangent_half_p(uint32_t tmem_col, uint8_t* tile,
   tmem_ld_wait();
   tangent32(v1, tile, r, 64 * h + 32, sc, cx, o);
   if (store) st_global16(grow + 64 * h + 32, o);
+}
+// columns [64h, 64h + 64): dx = tangent(dx^) written back over x in the SW128 tile
+__device__ __forceinline__ void tangent_half_inplace(uint32_t tmem_col, uint8_t* tile, int r, int h, Scale sc,
+                                                     float dot_hat) {
+  const float cx = sc.tangent ? dot_hat * sc.inv : 0.f;
+  float v0[32], v1[32];
+  uint32_t o[16];
+  tmem_ld32(tmem_col + 64 * h, v0);
+  tmem_ld_wait();
+  tmem_ld32(tmem_col + 64 * h + 32, v1);
+  tangent32(v0, tile, r, 64 * h, sc, cx, o);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) *tile_chunk(tile, r, 8 * h + j) = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  tmem_ld_wait();
+  tangent32(v1, tile, r, 64 * h + 32, sc, cx, o);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *tile_chunk(tile, r, 8 * h + 4 + j) = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
 }
 // TMEM columns [64h, 64h + 64) -> bf16 global row (double-buffered TMEM loads)
 __device__ __forceinline__ void tmem_half_to_global_p(uint32_t tmem_col, int h, __nv_bfloat16* grow, bool store) {

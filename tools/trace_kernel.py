@@ -32,11 +32,16 @@ q, k, v, do = (torch.randn(1, 4, args.n, 128, generator=g, device=dev).to(torch.
 L = _lib.lib()
 L.race_debug_progress_buffer.restype = ctypes.c_void_p
 buf = (ctypes.c_uint * (148 * 256)).from_address(L.race_debug_progress_buffer())
+o, den, st = rb.race_forward(q, k, v, w, p)
+torch.cuda.synchronize()
 for rep in range(3):
     for i in range(148 * 256):
         buf[i] = 0
-    o, den, st = rb.race_forward(q, k, v, w, p)
-    if args.kernel != "fwd":
+    torch.cuda.synchronize()
+    if args.kernel == "fwd":
+        o, den, st = rb.race_forward(q, k, v, w, p)
+    else:  # the backward launches bwd_q then bwd_k: trace only the one asked for
+        os.environ["RACE_TRACE_KERNEL"] = args.kernel
         rb.race_backward(q, k, v, w, do, p, state=st)
     torch.cuda.synchronize()
 vals = [[buf[e * 32 + c] for c in range(32)] for e in range(args.events)]
