@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       xbase[h * 128 + r] = sq;
       if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
       compute_bar256();
-      if (threadIdx.x == 64) mbar_arrive(&emptyqk[0]);
+      if (threadIdx.x == CT0) mbar_arrive(&emptyqk[0]);
       sqq = xbase[r];
       sqk = xbase[128 + r];
     }
@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const bool valid = t + r < m.t1;
       if (m.bh != prev_bh) {  // (re)load the sequence state: W', S_in (TMEM + S operand), A_in
         prev_bh = m.bh;
-        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
         const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
         float srow[FP];
 #pragma unroll
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
           srow[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
         }
-        build_wop<256>(a, m.bh, sb + OFF_W);
+        build_wop<256, CT0>(a, m.bh, sb + OFF_W);
         if (h == 1) {  // S accumulator (lane r = value column r): cols 0..7 = S_in, the rest 0
           float z[16];
 #pragma unroll
@@ -867,12 +867,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(wready);
-        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
       }
       const float invq = inv_scale(sqq, a.normalize);
       const float invk = inv_scale(sqk, a.normalize);
       mbar_wait(proj_full, gc & 1);
-      if (threadIdx.x == 64) RACE_TRACE(a, 5, gc);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 5, gc);
       tc_fence_after();
       float phq[FP];
       if (h == 0) {
@@ -911,7 +911,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
       // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 pairs into TMEM (my 64 columns)
       mbar_wait(pm_full, gc & 1);
-      if (threadIdx.x == 64) RACE_TRACE(a, 6, gc);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 6, gc);
       tc_fence_after();
       float rs = 0.f;
 #pragma unroll
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
       }
       compute_bar256();
-      if (threadIdx.x == 64 && cur.ok()) mbar_arrive(&emptyqk[(gc + 1) & 1]);
+      if (threadIdx.x == CT0 && cur.ok()) mbar_arrive(&emptyqk[(gc + 1) & 1]);
       sqq = xpar[r];
       sqk = xpar[128 + r];
       D += xpar[256 + r] + xpar[384 + r];
@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
       // ---- numerator -> O (my 64 columns, staged in the consumed V tile), next S operand
       mbar_wait(num_full, gc & 1);
-      if (threadIdx.x == 64) RACE_TRACE(a, 7, gc);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 7, gc);
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&ostaged[s]);
-      if (threadIdx.x == 64) RACE_TRACE(a, 8, gc);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 8, gc);
     }
   }
   tc_fence_before();
@@ -1097,6 +1097,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.tin = car;
   a.den = den;
   a.nrm_out = nrm;
+  a.dbg = trace_for("fwd");
   const char* v1 = getenv("RACE_FWD_V1");
   if (!(v1 && v1[0] == '1')) {
     switch (g.P) {

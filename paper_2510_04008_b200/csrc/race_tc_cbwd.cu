@@ -548,7 +548,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(wready, nr & 1);
         ++nr;
       }
-      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
       tc_fence_after();
       bool first = true;
       for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
@@ -596,6 +595,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         __syncwarp();
         mbar_wait(et_ready, par);
         RACE_TRACE(a, 7, gc);
+        if (first && ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);  // dS of the previous segment read out
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -653,8 +653,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
           scol[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
         }
-        build_wop<256>(a, m.bh, sb + OFF_W);
-        build_w2<256>(a, m.bh, sb + OFF_W2);
+        build_wop<256, CT0>(a, m.bh, sb + OFF_W);
+        build_w2<256, CT0>(a, m.bh, sb + OFF_W2);
         if (h == 1) {
           float z[16];
 #pragma unroll
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const Scale scq = row_scale(sq2.x, a.normalize);
         const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_wait(c1, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
         tc_fence_after();
         float pq[16], yv[16];
         float phq[FP], uq[5], hq[5];
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- row statistics from Pm and E over my 64 columns
         mbar_wait(c2, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
         tc_fence_after();
         float rs = 0.f, nd = 0.f;
 #pragma unroll
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- dphi_q -> dproj
         mbar_wait(c3, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
         tc_fence_after();
         float zz[32];
         tmem_ld32(tmem + lb + TM_Z, zz);
@@ -817,13 +817,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
         // ---- dq (my 64 columns) in place of q; the producer stores it
         mbar_wait(c4, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
         tc_fence_after();
         tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
-        if (threadIdx.x == 64) RACE_TRACE(a, 13, gc);
+        if (threadIdx.x == CT0) RACE_TRACE(a, 13, gc);
       }
       // ---- segment done: dS total (TMEM) and dA total (block reduction)
       mbar_wait(acc_full, ni & 1);
@@ -1336,16 +1336,20 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           store_dk(gc - 2);
           tma_store_wait_read<0>();
         }
+        RACE_TRACE(a, 3, gc);
         mbar_arrive_expect_tx(&fullK[s], TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + s * TILE + h * SUB, &tmK, &fullK[s], h * 64, t, bh, pol);
         if (s) { kt1 = t; kb1 = bh; } else { kt0 = t; kb0 = bh; }
         mbar_wait(emptyQ, par);
+        RACE_TRACE(a, 0, gc);
         mbar_arrive_expect_tx(fullQ, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, t, bh, pol);
         mbar_wait(emptyV, par);
+        RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
         mbar_wait(emptyO, par);
+        RACE_TRACE(a, 2, gc);
         mbar_arrive_expect_tx(fullO, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
       }
@@ -1367,6 +1371,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       }
       mbar_wait(fullQ, par);
       mbar_wait(&fullK[s], (gc >> 1) & 1);
+      RACE_TRACE(a, 4, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -1381,6 +1386,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       if (gc > 0) mbar_wait(dxfree, (gc - 1) & 1);  // E aliases the previous chunk's dX
       mbar_wait(fullV, par);
       mbar_wait(fullO, par);
+      RACE_TRACE(a, 5, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -1393,6 +1399,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       }
       __syncwarp();
       mbar_wait(phi_ready, par);
+      RACE_TRACE(a, 6, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -1402,6 +1409,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       }
       __syncwarp();
       mbar_wait(pt_ready, par);
+      RACE_TRACE(a, 7, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -1418,6 +1426,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       }
       __syncwarp();
       mbar_wait(dp_ready, par);
+      RACE_TRACE(a, 8, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -1446,7 +1455,19 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     uint32_t gc = 0;
     int64_t prev_bh = -1;
     RCursor cur;
-    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+    cur.start(a, i0, i1);
+    // per-token inputs of the current chunk, prefetched one chunk ahead
+    float rdr = 0.f, gdr = 0.f;
+    float2 sq2 = make_float2(0.f, 0.f);
+    auto fetch = [&](const RCursor& c) {
+      const bool v = c.t + r < c.m.t1;
+      const int64_t row = c.m.bh * a.N + c.t + r;
+      rdr = v ? rden[row] : 0.f;
+      gdr = v ? gden[row] : 0.f;
+      sq2 = v ? *reinterpret_cast<const float2*>(a.nrm_in + row * 2) : make_float2(0.f, 0.f);
+    };
+    if (cur.ok()) fetch(cur);
+    for (; cur.ok(); ++gc) {
       const Item m = cur.m;
       const int64_t t = cur.t;
       const uint32_t par = gc & 1;
@@ -1462,8 +1483,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           dcol[f] = f < F ? dcar[f * LDS_T + r] : 0.f;
           dA[f] = f < F ? dcar[f * LDS_T + DH] : 0.f;
         }
-        build_wop<256>(a, m.bh, sb + OFF_W);
-        build_w2<256>(a, m.bh, sb + OFF_W2);
+        build_wop<256, CT0>(a, m.bh, sb + OFF_W);
+        build_w2<256, CT0>(a, m.bh, sb + OFF_W2);
         if (h == 1) {
           float z[16];
 #pragma unroll
@@ -1480,15 +1501,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(wready);
       }
-      // per-query-token normaliser terms of this chunk
-      const float rdr = valid ? rden[m.bh * a.N + t + r] : 0.f;
-      const float gdr = valid ? gden[m.bh * a.N + t + r] : 0.f;
-      float2 sq2 = make_float2(0.f, 0.f);
-      if (valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
       const Scale scq = row_scale(sq2.x, a.normalize);
       const Scale sck = row_scale(sq2.y, a.normalize);
       xpar[h * 128 + r] = h ? gdr : rdr;
+      const float rdr_c = rdr, gdr_c = gdr;
       mbar_wait(projf, par);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
       tc_fence_after();
       float phq[FP], uq[5], hq[5], phk[FP], uk[5], hk[5];
       {
@@ -1510,8 +1528,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           float pht[FP], dac[FP];
 #pragma unroll
           for (int f = 0; f < FP; ++f) {
-            pht[f] = phq[f] * rdr;
-            dac[f] = phq[f] * gdr;
+            pht[f] = phq[f] * rdr_c;
+            dac[f] = phq[f] * gdr_c;
           }
           write_phi_k(sb + OFF_PHIT, r, pht);
 #pragma unroll
@@ -1530,6 +1548,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       // ---- EG~ (from E^T) and P~^T (from Pm^T), t >= i, my 64 columns -> TMEM A operands
       mbar_wait(c1, par);
       mbar_wait(c2, par);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -1541,18 +1560,22 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           tmem_ld_wait();
           uint32_t ue[16], up[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float ee[2], pp[2];
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 rd4 = *reinterpret_cast<const float4*>(xpar + c0 + 4 * j4);
+            const float4 gd4 = *reinterpret_cast<const float4*>(xpar + 128 + c0 + 4 * j4);
+            const float rdv[4] = {rd4.x, rd4.y, rd4.z, rd4.w}, gdv[4] = {gd4.x, gd4.y, gd4.z, gd4.w};
+            float ee[4], pp[4];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int tq = c0 + 2 * j + q;
-              const bool keep = tq >= r;
-              const float rdt = xpar[tq];
-              ee[q] = keep ? fmaf(e[2 * j + q], rdt, xpar[128 + tq]) : 0.f;
-              pp[q] = keep ? pm[2 * j + q] * rdt : 0.f;
+            for (int q = 0; q < 4; ++q) {
+              const int j = 4 * j4 + q;
+              const bool keep = c0 + j >= r;
+              ee[q] = keep ? fmaf(e[j], rdv[q], gdv[q]) : 0.f;
+              pp[q] = keep ? pm[j] * rdv[q] : 0.f;
             }
-            ue[j] = pack_bf16(ee[0], ee[1]);
-            up[j] = pack_bf16(pp[0], pp[1]);
+            ue[2 * j4] = pack_bf16(ee[0], ee[1]);
+            ue[2 * j4 + 1] = pack_bf16(ee[2], ee[3]);
+            up[2 * j4] = pack_bf16(pp[0], pp[1]);
+            up[2 * j4 + 1] = pack_bf16(pp[2], pp[3]);
           }
           tmem_st16u(tmem + lb + TM_EG + (c0 >> 1), ue);
           tmem_st16u(tmem + lb + TM_PT + (c0 >> 1), up);
@@ -1564,17 +1587,20 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_arrive(pt_ready);
       // ---- dphi_k, dV, next dS operands
       mbar_wait(c3, par);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
       tc_fence_after();
       float zz[32], zv[16];
       tmem_ld32(tmem + lb + TM_Z, zz);
       tmem_ld16(tmem + lb + TM_ZV, zv);
       tmem_ld_wait();
+      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 14, gc);
       float dphi[FP];
 #pragma unroll
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
       float dproj[8];
       row_feature_vjp<P>(a, uk, phk, dphi, dproj);
       const float dotk = dot_from_proj(dproj, hk);
+      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 15, gc);
       if (h == 1) {
         write_dproj(sb + OFF_DPROJ, r, dproj);
         float dsa[32];
@@ -1586,21 +1612,32 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         write_sopT(sb + OFF_DSOPT, r, dsn);
         write_sop(sb + OFF_DSOP, r, dsn);
       }
+      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 16, gc);
+#ifdef RACE_EXP_NODV
+      tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, false);
+#else
       tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, valid);
+#endif
+      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 17, gc);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dp_ready);
+      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 18, gc);
 #pragma unroll
       for (int f = 0; f < FP; ++f)
         dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
+      cur.next(a);
+      if (cur.ok()) fetch(cur);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
       tc_fence_after();
       tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&dkstaged[s]);
       mbar_arrive(dxfree);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 13, gc);
     }
   }
   tc_fence_before();
@@ -1625,6 +1662,7 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.tin = car;
   a.tout = dpart;
   a.nrm_in = nrm;
+  a.dbg = trace_for("bq");
   const char* v1 = getenv("RACE_BWDQ_V1");
   if (nrm && !(v1 && v1[0] == '1')) {
     switch (g.P) {
@@ -1652,6 +1690,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.w = w;
   a.tin = dcar;
   a.nrm_in = nrm;
+  a.dbg = trace_for("bk");
   const char* v1 = getenv("RACE_BWDK_V1");
   if (nrm && !(v1 && v1[0] == '1')) {
     __nv_bfloat16* dvp = static_cast<__nv_bfloat16*>(dv);

@@ -5,6 +5,8 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "race_common.cuh"
@@ -23,7 +25,8 @@ constexpr int TILE = 2 * SUB;        // [128 x 128] bf16 tile (32 KB)
 constexpr int WOP = 2 * 16 * 128;    // W' operand: [16 x 128] bf16, 2 SW128 sub-tiles of 2 KB
 constexpr int PHI = CH * 64;         // [128 x 32] bf16 K-major SW64 (8 KB)
 constexpr int NTHREADS = 192;
-constexpr int NTHREADS8 = 320;      // 8-compute-warp kernels: warps 2..9 compute
+constexpr int NTHREADS8 = 320;      // 8-compute-warp kernels: warp 0 TMA, warp 1 MMA, 2..9 compute
+constexpr int CT0 = 64;              // first compute thread of the 8-compute-warp kernels
 constexpr int FP = 8;                // padded feature count
 constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
 
@@ -185,10 +188,10 @@ __device__ __forceinline__ float inv_scale(float sumsq, int normalize) {
 }
 
 // W' rows 3j, 3j+1, 3j+2 = W_hi[j], W_mid[j], W_lo[j] (W to 24 bits), K-major SW128
-template <int NTC = 128>
+template <int NTC = 128, int T0 = 64>
 __device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wop) {
   const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
-  for (int idx = threadIdx.x - 64; idx < 16 * 16; idx += NTC) {
+  for (int idx = threadIdx.x - T0; idx < 16 * 16; idx += NTC) {
     const int n = idx >> 4, j = idx & 15;  // row n, 8-element chunk j
     const int hp = n / 3, piece = n % 3;
     uint32_t pk[4];
@@ -324,10 +327,10 @@ constexpr int W2OP = 2 * 32 * 128;  // 8 KB
 __device__ __forceinline__ uint64_t desc_w2(uint32_t base, int kk) {
   return smem_desc(base + kk * 2048, 4096, 1024, kSw128);
 }
-template <int NTC = 128>
+template <int NTC = 128, int T0 = 64>
 __device__ __forceinline__ void build_w2(const Args& a, int64_t bh, uint32_t w2) {
   const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
-  for (int idx = threadIdx.x - 64; idx < 32 * 16; idx += NTC) {
+  for (int idx = threadIdx.x - T0; idx < 32 * 16; idx += NTC) {
     const int k = idx >> 4, j = idx & 15;  // K-row k, 8-element column chunk j
     const int blk = k >> 3, hp = k & 7;
     uint32_t pk[4];
@@ -494,6 +497,12 @@ __device__ __forceinline__ void tangent_row_inplace(uint32_t tmem_col, uint32_t 
 // 8-compute-warp helpers (warps 2..9): warp w and w+4 share TMEM lane quarter
 // w % 4 (rows), and split the 128 columns into halves h = 0 / 1.
 // ---------------------------------------------------------------------------
+template <int N> __device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N> __device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
 __device__ __forceinline__ int chalf() { return warp_id() >= 6 ? 1 : 0; }
 __device__ __forceinline__ void cbar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void hbar128(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
@@ -806,6 +815,12 @@ inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g) {
 }
 
 unsigned* debug_progress_device();  // race_tc.cu
+// the debug buffer for kernel `name` ("fwd", "bq", "bk"), or null when RACE_TRACE_KERNEL names another
+inline unsigned* trace_for(const char* name) {
+  const char* k = getenv("RACE_TRACE_KERNEL");
+  if (k && k[0] && strcmp(k, name) != 0) return nullptr;
+  return debug_progress_device();
+}
 inline Args make_args(const Geo& g) {
   Args a{};
   a.dbg = debug_progress_device();

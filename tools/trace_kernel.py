@@ -11,6 +11,8 @@ import os
 import sys
 
 os.environ["RACE_DEBUG_PROGRESS"] = "1"
+_k = [sys.argv[i + 1] for i, x in enumerate(sys.argv[:-1]) if x == "--kernel"]
+os.environ["RACE_TRACE_KERNEL"] = _k[0] if _k else "fwd"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -40,8 +42,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     if args.kernel == "fwd":
         o, den, st = rb.race_forward(q, k, v, w, p)
-    else:  # the backward launches bwd_q then bwd_k: trace only the one asked for
-        os.environ["RACE_TRACE_KERNEL"] = args.kernel
+    else:  # RACE_TRACE_KERNEL (set above) picks which backward kernel writes the trace
         rb.race_backward(q, k, v, w, do, p, state=st)
     torch.cuda.synchronize()
 vals = [[buf[e * 32 + c] for c in range(32)] for e in range(args.events)]
