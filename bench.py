@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-max-context", action="store_true")
     return ap.parse_args()
 
 
@@ -165,6 +166,61 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# max context (BASELINE configs[2]): largest N whose fwd+bwd runs on this GPU
+# ---------------------------------------------------------------------------
+def max_context(dev, causal, dtype):
+    """Largest N (multiple of 2^20) whose RACE layer fwd+bwd (B=1, H=4, d=128)
+    completes on one GPU with every tensor resident in HBM, and its speed.
+
+    Starts from the free-memory estimate (~8.4 KB per token in bf16: Q, K, V,
+    dO, O, dQ, dK, dV plus den / row norms / normaliser terms) and steps down
+    1 Mi tokens on each out-of-memory."""
+    import torch
+
+    import paper_2510_04008_b200 as rb
+
+    cfg = rb.SketchConfig(hyperplanes=P_, tables=L_, beta=BETA, seed=0, causal=causal)
+    w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
+    p = cfg.params()
+    e = 2 if dtype == torch.bfloat16 else 4
+    per_token = HEADS * (8 * DIM * e + 96)
+    free, _ = torch.cuda.mem_get_info(dev)
+    n = int(free * 0.97 / per_token) >> 20 << 20
+    gen = torch.Generator(device=dev).manual_seed(7)
+    while n >= 1 << 20:
+        tensors = []
+        try:
+            shape = (1, HEADS, n, DIM)
+            q, k, v, g = (torch.randn(shape, generator=gen, device=dev, dtype=dtype) for _ in range(4))
+            tensors = [q, k, v, g]
+            o, den, st = rb.race_forward(q, k, v, w, p)
+            dq, dk, dv = rb.race_backward(q, k, v, w, g, p, state=st)
+            del o, den, st, dq, dk, dv
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            reps = 2
+            for _ in range(reps):
+                o, den, st = rb.race_forward(q, k, v, w, p)
+                dq, dk, dv = rb.race_backward(q, k, v, w, g, p, state=st)
+                del o, den, st, dq, dk, dv
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms = ev[0].elapsed_time(ev[1]) / reps
+            ok = bool(torch.isfinite(q[0, 0, -1].float()).all())
+            del q, k, v, g, tensors
+            torch.cuda.empty_cache()
+            return {"tokens": n, "causal": causal, "dtype": "bf16" if e == 2 else "f32", "ms_fwd_bwd": ms,
+                    "tokens_per_s": n / (ms / 1e3), "finite": ok,
+                    "hbm_gb_used_est": round(n * per_token / 1e9, 1)}
+        except torch.cuda.OutOfMemoryError:
+            del tensors
+            torch.cuda.empty_cache()
+            n -= 1 << 20
+    return {"tokens": 0, "causal": causal, "error": "nothing fits"}
 
 
 # ---------------------------------------------------------------------------
@@ -331,10 +387,23 @@ def run_ours(args, world, rank, local_rank):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     dom_bytes = kb[dom] * HEADS * n
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    # (tools/ncu_summary.py traffic; same workload: N=131072 per GPU, H=4, bf16)
+    ncu_names = {"kside_partials": "k_aggregate", "fwd_causal": "k_causal_fwd8", "bwd_causal_q": "k_bwd_causal_q8",
+                 "bwd_causal_k": "k_bwd_causal_k8", "fwd_readout": "k_readout", "bwd_qside": "k_bwd_q",
+                 "bwd_kside": "k_bwd_k", "combine": "k_combine", "combine_d": "k_combine"}
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if n == 131072 and dtype == torch.bfloat16 and ncu_names[dom] in tr:
+            traffic = tr[ncu_names[dom]]["dram_bytes"]
+    except Exception:
+        pass
     achieved = dom_bytes / (per[dom] / 1e3) / 1e9
     step_bytes = ((7 * DIM + 5 * DIM) * e + 8) * HEADS * n   # (7d+5dv)e+8 per token-head
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write per launch)", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "kernel_ms": {k2: round(v2, 4) for k2, v2 in per.items()},
                 "step_algorithmic_GBps": step_bytes / (ms_step / 1e3) / 1e9,
@@ -385,10 +454,11 @@ def run_ours(args, world, rank, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic N(0,1) Q,K,V,dO resident in HBM",
             "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "cuda_graph": graph is not None, "clocks": clocks,
+            "gpu_launches": launches, "cuda_graph": not args.no_graph and world == 1, "clocks": clocks,
             "fast_path": bool(_lib.fast_path(pr.desc)),
         }
-        print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
 def main():
@@ -406,7 +476,16 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, world, rank, local_rank)
+        line = run_ours(args, world, rank, local_rank)
+        if line is not None:
+            if world == 1 and not args.no_max_context:
+                import torch
+
+                torch.cuda.empty_cache()
+                dev = torch.device("cuda", local_rank)
+                dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+                line["max_context"] = [max_context(dev, c, dt) for c in (True, False)]
+            print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             import torch.distributed as dist

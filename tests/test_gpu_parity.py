@@ -340,3 +340,42 @@ def test_fast_path_backward(causal, n, pl):
         ref = ro.vjp(qh, kh, vh, w[1].double().cpu().numpy(), cfg.beta, gh, causal)
         errs = grad_errs([t[0, 1].float().cpu().numpy() for t in fast], ref, GRAD_FLOOR)
         assert max(errs) <= TOL_BF16, errs
+
+
+def test_long_context_prefix_and_oracle():
+    """BASELINE configs[2] scale: a 16 Mi-token causal layer (bf16, ~140 GB resident).
+
+    Causal outputs of the first 4096 tokens depend on those tokens only, so O,
+    den and dQ of that prefix must match (a) the same layer run on the prefix
+    alone and (b) the float64 oracle; the tail must be finite.  This covers the
+    long-sequence carry chain (many segments per head, carries over 16M tokens)."""
+    n, n0 = 1 << 24, 4096
+    dev = _cuda()
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < n * 8700:
+        pytest.skip("needs ~145 GB of free HBM")
+    gen = torch.Generator(device=dev).manual_seed(11)
+    shape = (1, 4, n, 128)
+    q, k, v, g = (torch.randn(shape, generator=gen, device=dev, dtype=torch.bfloat16) for _ in range(4))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=0, causal=True)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(dev)
+    p = cfg.params()
+    o, den, st = rb.race_forward(q, k, v, w, p)
+    dq, dk, dv = rb.race_backward(q, k, v, w, g, p, state=st)
+    o0, den0, dq0 = o[:, :, :n0].clone(), den[:, :, :n0].clone(), dq[:, :, :n0].clone()
+    tail_ok = all(bool(torch.isfinite(t[:, :, -4096:].float()).all()) for t in (o, dq, dk, dv))
+    qp, kp, vp, gp = (t[:, :, :n0].clone() for t in (q, k, v, g))
+    del q, k, v, g, o, den, st, dq, dk, dv
+    torch.cuda.empty_cache()
+    assert tail_ok
+    op, denp, stp = rb.race_forward(qp, kp, vp, w, p)
+    dqp, _, _ = rb.race_backward(qp, kp, vp, w, gp, p, state=stp)
+    assert rel_err(o0.float().cpu(), op.float().cpu().numpy()) <= TOL_BF16
+    assert rel_err(den0.cpu(), denp.cpu().numpy()) <= 1e-4
+    assert rel_err(dq0.float().cpu(), dqp.float().cpu().numpy()) <= TOL_BF16
+    qh, kh, vh, gh = (t[0, 0].double().cpu().numpy() for t in (qp, kp, vp, gp))
+    o_r, den_r, _ = ro.forward(qh, kh, vh, w[0].double().cpu().numpy(), cfg.beta, True)
+    dq_r, _, _ = ro.vjp(qh, kh, vh, w[0].double().cpu().numpy(), cfg.beta, gh, True)
+    assert rel_err(o0[0, 0].float().cpu(), o_r) <= TOL_BF16
+    assert rel_err(den0[0, 0].cpu(), den_r) <= TOL_F32
+    assert rel_err(dq0[0, 0].float().cpu(), dq_r) <= TOL_BF16

@@ -79,5 +79,30 @@ def launches(path: str) -> None:
         print(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f}% |")
 
 
+def traffic(path: str, out: str) -> None:
+    """profiles/ncu_traffic.json: dram read+write bytes per launch of each kernel
+    (first capture of each name), the `traffic` term of bench.py's roofline."""
+    import json
+
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], check=True, capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for r in data:
+        name = re.sub(r"<.*", "", short(r[col["Kernel Name"]])).split("::")[-1]
+        if name in res:
+            continue
+        b = sum(float(r[col[m]]) * scale[units[col[m]]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        res[name] = {"dram_bytes": b, "us": float(r[col["gpu__time_duration.sum"]]), "capture": path.split("/")[-1]}
+    json.dump(res, open(out, "w"), indent=1, sort_keys=True)
+    print(json.dumps(res, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3])
+    else:
+        {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
