@@ -1223,7 +1223,9 @@ constexpr int OFF_PHIT = OFF_PHIK + PHI;   // phi_q / D     B of dS (MN)
 constexpr int OFF_DPROJ = OFF_PHIT + PHI;
 constexpr int OFF_X = OFF_DPROJ + PHI;     // [2 parity] x { rd[128], gd[128], dac[4][8] }
 constexpr int XPAR = 256 + 32;
-constexpr int OFF_BAR = OFF_X + 2 * XPAR * 4;
+constexpr int OFF_TOK = OFF_X + 2 * XPAR * 4;  // [2 parity] x { rden[128], gden[128], rownorms[256] } (TMA)
+constexpr int TOK_BYTES = 512 * 4;
+constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 512 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_k8 shared memory");
 constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_EG = 128, TM_PT = 192, TM_E = 256,
@@ -1259,8 +1261,9 @@ template <int P>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                    const __grid_constant__ CUtensorMap tmDK, Args a, const float* __restrict__ rden,
-                    const float* __restrict__ gden, __nv_bfloat16* __restrict__ dvout) {
+                    const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmRD,
+                    const __grid_constant__ CUtensorMap tmGD, const __grid_constant__ CUtensorMap tmNRM, Args a,
+                    __nv_bfloat16* __restrict__ dvout) {
   using namespace ck8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1284,7 +1287,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* dp_ready = bars + 17;
   uint64_t* dxfree = bars + 18;
   uint64_t* wready = bars + 19;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* eg_ready = bars + 20;  // EG~ staged in TMEM (256 arrivals)
+  uint64_t* cdv = bars + 21;       // dV MMAs done
+  uint64_t* fullT = bars + 22;     // [2] per-token inputs landed (parity buffers)
+  uint64_t* emptyT = bars + 24;    // [2] ... consumed (256 arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
@@ -1298,6 +1305,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     mbar_init(dp_ready, 256);
     mbar_init(dxfree, 256);
     mbar_init(wready, 256);
+    mbar_init(eg_ready, 256);
+    mbar_init(cdv, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&fullT[i], 1);
+      mbar_init(&emptyT[i], 256);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -1316,6 +1329,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmDO);
       tma_prefetch_desc(&tmDK);
+      tma_prefetch_desc(&tmRD);
+      tma_prefetch_desc(&tmGD);
+      tma_prefetch_desc(&tmNRM);
       const uint64_t pol = policy_evict_first();
       int64_t kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
       auto store_dk = [&](uint32_t j) {
@@ -1344,6 +1360,15 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         RACE_TRACE(a, 0, gc);
         mbar_arrive_expect_tx(fullQ, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, t, bh, pol);
+        {  // per-token rden, gden, row norms of this chunk (parity buffer s)
+          uint8_t* tok = smem + OFF_TOK + s * TOK_BYTES;
+          const int row = bh * int(a.N) + t;
+          mbar_wait(&emptyT[s], ((gc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
+          tma_load_1d(tok, &tmRD, &fullT[s], row, pol);
+          tma_load_1d(tok + 512, &tmGD, &fullT[s], row, pol);
+          tma_load_1d(tok + 1024, &tmNRM, &fullT[s], 2 * row, pol);
+        }
         mbar_wait(emptyV, par);
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
@@ -1408,20 +1433,28 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         umma_commit(c2);
       }
       __syncwarp();
+      mbar_wait(eg_ready, par);
+      tc_fence_after();
+      if (elect_one()) {  // dphi_k's intra-chunk term and the dS update: the dq-critical path
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16_ts(tmem + TM_Z, tmem + TM_EG + kk * 8, desc_phi_mn(sb + OFF_PHIQ, kk), IDC_Z, kk > 0);
+          umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
+        }
+        umma_commit(c3);
+      }
+      __syncwarp();
       mbar_wait(pt_ready, par);
       RACE_TRACE(a, 7, gc);
       tc_fence_after();
-      if (elect_one()) {
+      if (elect_one()) {  // dV = Phi_k dS_>c,v + P~^T dO (into the consumed Pm columns)
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)
           umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), IDC_DVA, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16_ts(tmem + TM_Z, tmem + TM_EG + kk * 8, desc_phi_mn(sb + OFF_PHIQ, kk), IDC_Z, kk > 0);
+        for (int kk = 0; kk < 8; ++kk)
           umma_bf16_ts(tmem + TM_DV, tmem + TM_PT + kk * 8, desc_tile_mn(sb + OFF_DO, kk), IDC_DVB, 1u);
-          umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
-        }
-        umma_commit(c3);
+        umma_commit(cdv);
         umma_commit(emptyO);
       }
       __syncwarp();
@@ -1456,17 +1489,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     int64_t prev_bh = -1;
     RCursor cur;
     cur.start(a, i0, i1);
-    // per-token inputs of the current chunk, prefetched one chunk ahead
-    float rdr = 0.f, gdr = 0.f;
-    float2 sq2 = make_float2(0.f, 0.f);
-    auto fetch = [&](const RCursor& c) {
-      const bool v = c.t + r < c.m.t1;
-      const int64_t row = c.m.bh * a.N + c.t + r;
-      rdr = v ? rden[row] : 0.f;
-      gdr = v ? gden[row] : 0.f;
-      sq2 = v ? *reinterpret_cast<const float2*>(a.nrm_in + row * 2) : make_float2(0.f, 0.f);
-    };
-    if (cur.ok()) fetch(cur);
     for (; cur.ok(); ++gc) {
       const Item m = cur.m;
       const int64_t t = cur.t;
@@ -1501,10 +1523,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(wready);
       }
+      // per-token inputs (TMA-loaded with Q; rows past the segment end are masked by `valid`)
+      const float* tok = reinterpret_cast<const float*>(smem + OFF_TOK + (gc & 1) * TOK_BYTES);
+      mbar_wait(&fullT[gc & 1], (gc >> 1) & 1);
+      const float rdr_c = valid ? tok[r] : 0.f, gdr_c = valid ? tok[128 + r] : 0.f;
+      const float2 sq2 = valid ? *reinterpret_cast<const float2*>(tok + 256 + 2 * r) : make_float2(0.f, 0.f);
       const Scale scq = row_scale(sq2.x, a.normalize);
       const Scale sck = row_scale(sq2.y, a.normalize);
-      xpar[h * 128 + r] = h ? gdr : rdr;
-      const float rdr_c = rdr, gdr_c = gdr;
       mbar_wait(projf, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
       tc_fence_after();
@@ -1545,47 +1570,63 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
       }
       compute_bar256();  // rd / gd of every query token, dA partials
-      // ---- EG~ (from E^T) and P~^T (from Pm^T), t >= i, my 64 columns -> TMEM A operands
+      // ---- EG~ = (E^T rd + gd) masked t >= i, my 64 columns -> TMEM A operand of Z
       mbar_wait(c1, par);
-      mbar_wait(c2, par);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const int c0 = 64 * h + 32 * b;
         if ((c0 >> 5) >= qw) {  // warp-uniform; blocks below the diagonal stay zero
-          float e[32], pm[32];
+          float e[32];
           tmem_ld32(tmem + lb + TM_E + c0, e);
-          tmem_ld32(tmem + lb + TM_PMC + c0, pm);
           tmem_ld_wait();
-          uint32_t ue[16], up[16];
+          uint32_t ue[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 rd4 = *reinterpret_cast<const float4*>(xpar + c0 + 4 * j4);
-            const float4 gd4 = *reinterpret_cast<const float4*>(xpar + 128 + c0 + 4 * j4);
+            const float4 rd4 = *reinterpret_cast<const float4*>(tok + c0 + 4 * j4);
+            const float4 gd4 = *reinterpret_cast<const float4*>(tok + 128 + c0 + 4 * j4);
             const float rdv[4] = {rd4.x, rd4.y, rd4.z, rd4.w}, gdv[4] = {gd4.x, gd4.y, gd4.z, gd4.w};
-            float ee[4], pp[4];
+            float ee[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int j = 4 * j4 + q;
-              const bool keep = c0 + j >= r;
-              ee[q] = keep ? fmaf(e[j], rdv[q], gdv[q]) : 0.f;
-              pp[q] = keep ? pm[j] * rdv[q] : 0.f;
-            }
+            for (int q = 0; q < 4; ++q) ee[q] = (c0 + 4 * j4 + q >= r) ? fmaf(e[4 * j4 + q], rdv[q], gdv[q]) : 0.f;
             ue[2 * j4] = pack_bf16(ee[0], ee[1]);
             ue[2 * j4 + 1] = pack_bf16(ee[2], ee[3]);
-            up[2 * j4] = pack_bf16(pp[0], pp[1]);
-            up[2 * j4 + 1] = pack_bf16(pp[2], pp[3]);
           }
           tmem_st16u(tmem + lb + TM_EG + (c0 >> 1), ue);
-          tmem_st16u(tmem + lb + TM_PT + (c0 >> 1), up);
         }
       }
       tmem_st_wait();
-      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(eg_ready);
+      // ---- P~^T = Pm^T rd masked t >= i -> TMEM A operand of dV
+      mbar_wait(c2, par);
+      tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 64 * h + 32 * b;
+        if ((c0 >> 5) >= qw) {
+          float pm[32];
+          tmem_ld32(tmem + lb + TM_PMC + c0, pm);
+          tmem_ld_wait();
+          uint32_t up[16];
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 rd4 = *reinterpret_cast<const float4*>(tok + c0 + 4 * j4);
+            const float rdv[4] = {rd4.x, rd4.y, rd4.z, rd4.w};
+            float pp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pp[q] = (c0 + 4 * j4 + q >= r) ? pm[4 * j4 + q] * rdv[q] : 0.f;
+            up[2 * j4] = pack_bf16(pp[0], pp[1]);
+            up[2 * j4 + 1] = pack_bf16(pp[2], pp[3]);
+          }
+          tmem_st16u(tmem + lb + TM_PT + (c0 >> 1), up);
+        }
+      }
+      mbar_arrive(&emptyT[gc & 1]);  // last read of this chunk's per-token inputs
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(pt_ready);
-      // ---- dphi_k, dV, next dS operands
+      // ---- dphi_k -> dproj (Z and the dS update are done at c3)
       mbar_wait(c3, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
       tc_fence_after();
@@ -1593,16 +1634,23 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_ld32(tmem + lb + TM_Z, zz);
       tmem_ld16(tmem + lb + TM_ZV, zv);
       tmem_ld_wait();
-      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 14, gc);
       float dphi[FP];
 #pragma unroll
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
       float dproj[8];
       row_feature_vjp<P>(a, uk, phk, dphi, dproj);
       const float dotk = dot_from_proj(dproj, hk);
-      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 15, gc);
+      if (h == 1) write_dproj(sb + OFF_DPROJ, r, dproj);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(dp_ready);
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
+      // ---- dV out; dS_>c-1 operands for the next (earlier) chunk once the dV MMA has read DSOP
+      mbar_wait(cdv, par);
+      tc_fence_after();
       if (h == 1) {
-        write_dproj(sb + OFF_DPROJ, r, dproj);
         float dsa[32];
         tmem_ld32(tmem + lb + TM_DS, dsa);
         tmem_ld_wait();
@@ -1612,22 +1660,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         write_sopT(sb + OFF_DSOPT, r, dsn);
         write_sop(sb + OFF_DSOP, r, dsn);
       }
-      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 16, gc);
-#ifdef RACE_EXP_NODV
-      tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, false);
-#else
       tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, valid);
-#endif
-      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 17, gc);
       fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(dp_ready);
-      if (threadIdx.x == CT0 + 128) RACE_TRACE(a, 18, gc);
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
       cur.next(a);
-      if (cur.ok()) fetch(cur);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
@@ -1694,10 +1729,14 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   const char* v1 = getenv("RACE_BWDK_V1");
   if (nrm && !(v1 && v1[0] == '1')) {
     __nv_bfloat16* dvp = static_cast<__nv_bfloat16*>(dv);
+    CUtensorMap mrd, mgd, mnrm;
+    if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
+        !make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256))
+      return cudaErrorInvalidValue;
     switch (g.P) {
-      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
-      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
-      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, a, rden, gden, dvp);
+      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
+      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
+      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
     }
   }
   switch (g.P) {

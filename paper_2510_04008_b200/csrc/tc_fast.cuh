@@ -814,6 +814,20 @@ inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g) {
   return r == CUDA_SUCCESS;
 }
 
+// flat fp32 array of `elems` viewed 1-D, box of `box` elements (OOB reads are zero)
+inline bool make_map_f32_1d(CUtensorMap* m, const void* ptr, int64_t elems, int box) {
+  auto fn = encode_fn();
+  if (!fn || elems <= 0 || elems >= (int64_t(1) << 32)) return false;
+  cuuint64_t dims[1] = {cuuint64_t(elems)};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t bx[1] = {cuuint32_t(box)};
+  cuuint32_t es[1] = {1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(ptr), dims, strides, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 unsigned* debug_progress_device();  // race_tc.cu
 // the debug buffer for kernel `name` ("fwd", "bq", "bk"), or null when RACE_TRACE_KERNEL names another
 inline unsigned* trace_for(const char* name) {
