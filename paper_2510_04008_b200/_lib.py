@@ -13,7 +13,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librace_b200.so")
+# RACE_LIB_PATH lets a benchmark A/B two in-tree builds of the same library
+LIB_PATH = os.environ.get("RACE_LIB_PATH") or os.path.join(_HERE, "librace_b200.so")
 
 ABI_VERSION = 1
 RACE_OK, RACE_EBADSHAPE, RACE_EUNSUPPORTED, RACE_ECUDA = 0, 1, 2, 3

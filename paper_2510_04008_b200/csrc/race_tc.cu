@@ -17,6 +17,7 @@
 // as hi/lo bf16 pairs (16-bit mantissa); only the causal intra-chunk matrix
 // tril(Phi_q Phi_k^T) is rounded to bf16 before multiplying V.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmO);
       const uint64_t pol = policy_evict_first();
-      int64_t ot0 = 0, ob0 = 0, ot1 = 0, ob1 = 0;  // coordinates of the O tile held by each stage
+      int ot0 = 0, ob0 = 0, ot1 = 0, ob1 = 0;  // coordinates of the O tile held by each stage
       auto store_o = [&](uint32_t j) {             // O of chunk j (V tile of stage j & 1)
         const int s = j & 1;
         mbar_wait(&ostaged[s], (j >> 1) & 1);
@@ -723,6 +724,15 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
         const int s = gc & 1;
         uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+        if (a.pf > 0) {  // warm L2 with the tiles a.pf chunks ahead (same sequence; a hint only)
+          const int tp = int(cur.t) + a.pf * CH;
+          if (tp < a.N)
+            for (int h = 0; h < 2; ++h) {
+              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
+            }
+        }
         mbar_wait(&emptyqk[s], ((gc >> 1) & 1) ^ 1);
         RACE_TRACE(a, 0, gc);
         mbar_arrive_expect_tx(&fullqk[s], 2 * TILE);
@@ -1017,15 +1027,23 @@ __global__ void __launch_bounds__(256) k_rownorms(const uint4* __restrict__ q, c
 
 static unsigned* g_dbg_host = nullptr;
 static unsigned* g_dbg_dev = nullptr;
+static int g_dbg_mode = 0;  // RACE_DEBUG_PROGRESS: 1 = host-mapped (watch a hang live), 2 = device (timing traces)
+constexpr size_t kDbgBytes = 148 * 256 * sizeof(unsigned);
 unsigned* debug_progress_device() {
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = getenv("RACE_DEBUG_PROGRESS");
     if (e && e[0] == '1') {
-      const size_t bytes = 148 * 256 * sizeof(unsigned);
-      if (cudaHostAlloc(reinterpret_cast<void**>(&g_dbg_host), bytes, cudaHostAllocMapped) == cudaSuccess) {
-        memset(g_dbg_host, 0, bytes);
+      if (cudaHostAlloc(reinterpret_cast<void**>(&g_dbg_host), kDbgBytes, cudaHostAllocMapped) == cudaSuccess) {
+        memset(g_dbg_host, 0, kDbgBytes);
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_dbg_dev), g_dbg_host, 0);
+        g_dbg_mode = 1;
+      }
+    } else if (e && e[0] == '2') {  // device memory: trace stores do not go over PCIe
+      if (cudaMalloc(reinterpret_cast<void**>(&g_dbg_dev), kDbgBytes) == cudaSuccess) {
+        cudaMemset(g_dbg_dev, 0, kDbgBytes);
+        g_dbg_host = static_cast<unsigned*>(calloc(1, kDbgBytes));
+        g_dbg_mode = 2;
       }
     }
   });
@@ -1118,5 +1136,12 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
 // diagnostic (not part of the documented ABI): host view of the progress words
 extern "C" void* race_debug_progress_buffer(void) {
   race::tcfast::debug_progress_device();
+  if (race::tcfast::g_dbg_mode == 2)
+    cudaMemcpy(race::tcfast::g_dbg_host, race::tcfast::g_dbg_dev, race::tcfast::kDbgBytes, cudaMemcpyDeviceToHost);
   return race::tcfast::g_dbg_host;
+}
+extern "C" void race_debug_progress_clear(void) {
+  race::tcfast::debug_progress_device();
+  if (race::tcfast::g_dbg_mode == 2) cudaMemset(race::tcfast::g_dbg_dev, 0, race::tcfast::kDbgBytes);
+  if (race::tcfast::g_dbg_host) memset(race::tcfast::g_dbg_host, 0, race::tcfast::kDbgBytes);
 }

@@ -409,77 +409,114 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // ===========================================================================
 // causal backward, query side -- pipelined 8-compute-warp version (launched)
 //
-// Same math as k_bwd_causal_q above; the structure follows k_causal_fwd8:
-// contiguous CTA ranges (S, A continue across segments, dS / dA totals are
-// emitted per segment), compute warps 2..9 split every 128-column pass into
-// halves, E~ = tril(E - rho) lives in TMEM as the A operand of Z = E~ Phi_k,
-// the Q tile is double-buffered and dQ is staged in place and TMA-stored by
-// the producer right before that buffer is refilled.  Row norms come from
-// the forward (rownorms is required).
+// Same math as k_bwd_causal_q above, restructured for latency:
+//  * contiguous CTA ranges: S, A continue across segments; dS / dA totals are
+//    emitted per segment;
+//  * compute warps 2..9 split every 128-column pass into halves;
+//  * E~ = tril(E - rho) lives in TMEM as the A operand of Z = E~ Phi_k;
+//  * Q and dO are double-buffered, so the MMA warp issues the NEXT chunk's
+//    projection and E / Y right after this chunk's Z / dS -- they complete
+//    while the compute warps finish this chunk;
+//  * dx^ = dproj . W is one MMA pair against the projection operand W'
+//    itself (read MN-major: W_hi + W_mid + W_lo, i.e. W to 24 bits) with
+//    dproj split hi / lo; the sphere-tangent VJP writes dq over q in its
+//    tile and the producer TMA-stores it just before refilling that buffer;
+//  * the row norms saved by the forward arrive by TMA with their own
+//    full / empty barriers (no global loads in the compute warps).
 // ===========================================================================
 namespace cq8 {
-constexpr int OFF_Q = 0;  // two buffers
-constexpr int OFF_K = 2 * TILE, OFF_V = 3 * TILE, OFF_DO = 4 * TILE;
-constexpr int OFF_W = 5 * TILE;
-constexpr int OFF_W2 = OFF_W + WOP;
-constexpr int OFF_SOPT = OFF_W2 + W2OP;
-constexpr int OFF_PHIQ = OFF_SOPT + WOP;
-constexpr int OFF_PHIK = OFF_PHIQ + PHI;
-constexpr int OFF_PHIT = OFF_PHIK + PHI;
-constexpr int OFF_DPROJ = OFF_PHIT + PHI;
-constexpr int OFF_X = OFF_DPROJ + PHI;  // [2 parity] x { rs[2][128], nd[2][128], kp[4][8] }, then da[4][8]
+constexpr int OFF_Q = 0;                       // two buffers
+constexpr int OFF_K = 2 * TILE, OFF_V = 3 * TILE;
+constexpr int OFF_DO = 4 * TILE;               // two buffers
+constexpr int OFF_W = 6 * TILE;                // W' (B of the projection; B of dx^ read MN-major)
+constexpr int OFF_SOPT = OFF_W + WOP;
+constexpr int OFF_PHIQ = OFF_SOPT + WOP;       // Phi_q (A of Pm), then phi_q / D (B of dS)
+constexpr int OFF_PHIK = OFF_PHIQ + PHI;       // Phi_k (A of Pm, B of S and Z), then dproj (A of dx^)
+constexpr int OFF_X = OFF_PHIK + PHI;          // [2 parity] x { rs[2][128], nd[2][128], kp[4][8] }, then da[4][8]
 constexpr int XPAR = 256 + 256 + 32;
-constexpr int OFF_BAR = OFF_X + (2 * XPAR + 32) * 4;
-constexpr int SMEM = OFF_BAR + 512 + 1024;
+constexpr int OFF_TOK = OFF_X + (2 * XPAR + 32) * 4;  // [2] x row norms [256] (TMA)
+constexpr int TOK_BYTES = 256 * 4;
+constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_q8 shared memory");
+static_assert(OFF_TOK % 128 == 0, "TMA destination alignment");
 constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_ET = 144, TM_PMC = 256,
                    TM_E = 384, TM_DX = 256;
+// W' [16 x 128] (rows = hyperplane pieces, d contiguous, two SW128 64-column sub-tiles) as an MN-major B
+__device__ __forceinline__ uint64_t desc_wT(uint32_t base) { return smem_desc(base, 2048, 1024, kSw128); }
+// dproj expanded to W's rows: K cols 3j..3j+2 = dproj_j (hi) and 16 + 3j.. (lo)
+__device__ __forceinline__ void write_dproj_w(uint32_t buf, int r, const float* dproj, int tp) {
+  float hi[16], lo[16];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    const int j = n / 3;
+    const float x = (n < 15 && j < tp) ? dproj[j < 5 ? j : 0] : 0.f;
+    hi[n] = bf16_round(x);
+    lo[n] = x - hi[n];
+  }
+  uint32_t blk[4][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    blk[0][e] = pack_bf16(hi[2 * e], hi[2 * e + 1]);
+    blk[1][e] = pack_bf16(hi[8 + 2 * e], hi[8 + 2 * e + 1]);
+    blk[2][e] = pack_bf16(lo[2 * e], lo[2 * e + 1]);
+    blk[3][e] = pack_bf16(lo[8 + 2 * e], lo[8 + 2 * e + 1]);
+  }
+  write_row32(buf, r, blk);
+}
 }  // namespace cq8
 
 template <int P>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                    const __grid_constant__ CUtensorMap tmDQ, Args a, float* __restrict__ rden,
-                    float* __restrict__ gden) {
+                    const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmNRM, Args a,
+                    float* __restrict__ rden, float* __restrict__ gden) {
   using namespace cq8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* fullQ = bars + 0;     // [2]
-  uint64_t* dqstaged = bars + 2;  // [2] dQ staged in Q buffer (256 arrivals)
-  uint64_t* fullK = bars + 4;
-  uint64_t* fullV = bars + 5;
-  uint64_t* fullO = bars + 6;
-  uint64_t* emptyK = bars + 7;
-  uint64_t* emptyV = bars + 8;
-  uint64_t* emptyO = bars + 9;
-  uint64_t* c1 = bars + 10;
-  uint64_t* c2 = bars + 11;
-  uint64_t* c3 = bars + 12;
-  uint64_t* c4 = bars + 13;
-  uint64_t* phi_ready = bars + 14;
-  uint64_t* et_ready = bars + 15;
-  uint64_t* dp_ready = bars + 16;
-  uint64_t* wready = bars + 17;
-  uint64_t* acc_full = bars + 18;
-  uint64_t* acc_empty = bars + 19;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* fullQ = bars + 0;      // [2]
+  uint64_t* dqstaged = bars + 2;   // [2] dQ staged in the Q buffer (256 arrivals)
+  uint64_t* fullO = bars + 4;      // [2]
+  uint64_t* emptyO = bars + 6;     // [2] (dS MMA commit)
+  uint64_t* fullT = bars + 8;      // [2] row norms landed
+  uint64_t* emptyT = bars + 10;    // [2] row norms read (256 arrivals)
+  uint64_t* fullK = bars + 12;
+  uint64_t* emptyK = bars + 13;
+  uint64_t* fullV = bars + 14;
+  uint64_t* emptyV = bars + 15;
+  uint64_t* c1 = bars + 16;        // projection + E + Y
+  uint64_t* c2 = bars + 17;        // Pm + S state
+  uint64_t* c3 = bars + 18;        // Z + dS
+  uint64_t* phi_ready = bars + 19;
+  uint64_t* et_ready = bars + 20;
+  uint64_t* wready = bars + 21;
+  uint64_t* acc_full = bars + 22;
+  uint64_t* acc_empty = bars + 23;
+  uint64_t* dp_ready = bars + 24;  // dproj staged (256 arrivals)
+  uint64_t* c4 = bars + 25;        // dx^ MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&fullQ[i], 1);
       mbar_init(&dqstaged[i], 256);
+      mbar_init(&fullO[i], 1);
+      mbar_init(&emptyO[i], 1);
+      mbar_init(&fullT[i], 1);
+      mbar_init(&emptyT[i], 256);
     }
-    for (int i = 4; i < 14; ++i) mbar_init(&bars[i], 1);
+    for (int i = 12; i < 19; ++i) mbar_init(&bars[i], 1);
     mbar_init(phi_ready, 256);
     mbar_init(et_ready, 256);
-    mbar_init(dp_ready, 256);
     mbar_init(wready, 256);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 256);
+    mbar_init(dp_ready, 256);
+    mbar_init(c4, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -498,8 +535,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmDO);
       tma_prefetch_desc(&tmDQ);
+      tma_prefetch_desc(&tmNRM);
       const uint64_t pol = policy_evict_first();
-      int64_t qt0 = 0, qb0 = 0, qt1 = 0, qb1 = 0;
+      int qt0 = 0, qb0 = 0, qt1 = 0, qb1 = 0;
       auto store_dq = [&](uint32_t j) {
         const int s = j & 1;
         mbar_wait(&dqstaged[s], (j >> 1) & 1);
@@ -511,7 +549,18 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       uint32_t gc = 0;
       Cursor cur;
       for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
-        const uint32_t par = (gc & 1) ^ 1;
+        if (a.pf > 0) {  // warm L2 with the tiles a.pf chunks ahead (same sequence; a hint only)
+          const int tp = int(cur.t) + a.pf * CH;
+          if (tp < a.N)
+            for (int h = 0; h < 2; ++h) {
+              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
+            }
+        }
+        const uint32_t par1 = (gc & 1) ^ 1;          // single buffers: one phase per chunk
+        const uint32_t par2 = ((gc >> 1) & 1) ^ 1;   // double buffers: one phase per two chunks
         const int s = gc & 1;
         const int t = int(cur.t), bh = int(cur.m.bh);
         if (gc >= 2) {
@@ -522,63 +571,72 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&fullQ[s], TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + s * TILE + h * SUB, &tmQ, &fullQ[s], h * 64, t, bh, pol);
         if (s) { qt1 = t; qb1 = bh; } else { qt0 = t; qb0 = bh; }
-        mbar_wait(emptyK, par);
+        mbar_wait(&emptyT[s], par2);
+        mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
+        tma_load_1d(smem + OFF_TOK + s * TOK_BYTES, &tmNRM, &fullT[s], 2 * (bh * int(a.N) + t), pol);
+        mbar_wait(emptyK, par1);
         RACE_TRACE(a, 0, gc);
         mbar_arrive_expect_tx(fullK, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
-        mbar_wait(emptyV, par);
+        mbar_wait(emptyV, par1);
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
-        mbar_wait(emptyO, par);
+        mbar_wait(&emptyO[s], par2);
         RACE_TRACE(a, 2, gc);
-        mbar_arrive_expect_tx(fullO, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
+        mbar_arrive_expect_tx(&fullO[s], TILE);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dq(j);
       tma_store_wait_all<0>();
     }
   } else if (warp == 1) {
+    // projection + E / Y of chunk `gc` (issued one step ahead of its use)
+    auto issue_front = [&](uint32_t gc) {
+      const int s = gc & 1;
+      mbar_wait(&fullQ[s], (gc >> 1) & 1);
+      mbar_wait(fullK, gc & 1);
+      RACE_TRACE(a, 4, gc);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        }
+        umma_commit(emptyK);
+      }
+      __syncwarp();
+      mbar_wait(fullV, gc & 1);
+      mbar_wait(&fullO[s], (gc >> 1) & 1);
+      RACE_TRACE(a, 5, gc);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_DO + s * TILE, kk), desc_tile_k(sb + OFF_V, kk), IDC_E, kk > 0);
+          umma_bf16(tmem + TM_Y, desc_tile_k(sb + OFF_DO + s * TILE, kk), desc_w(sb + OFF_SOPT, kk), IDC_Y, kk > 0);
+        }
+        umma_commit(c1);
+      }
+      __syncwarp();
+    };
     uint32_t gc = 0, nr = 0, ni = 0;
     int64_t prev_bh = -1;
     for (int64_t it = i0; it < i1; ++it, ++ni) {
       const Item m = item_of(a, it);
-      if (m.bh != prev_bh) {
-        prev_bh = m.bh;
-        mbar_wait(wready, nr & 1);
-        ++nr;
-      }
-      tc_fence_after();
-      bool first = true;
       for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
         const uint32_t par = gc & 1;
         const int s = gc & 1;
-        mbar_wait(&fullQ[s], (gc >> 1) & 1);
-        mbar_wait(fullK, par);
-        RACE_TRACE(a, 4, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          }
-          umma_commit(emptyK);
+        const bool first = t == m.t0;
+        if (m.bh != prev_bh) {  // new sequence: W', S, SOPT rebuilt by the compute warps
+          prev_bh = m.bh;
+          mbar_wait(wready, nr & 1);
+          ++nr;
+          tc_fence_after();
+          issue_front(gc);
         }
-        __syncwarp();
-        mbar_wait(fullV, par);
-        mbar_wait(fullO, par);
-        RACE_TRACE(a, 5, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_DO, kk), desc_tile_k(sb + OFF_V, kk), IDC_E, kk > 0);
-            umma_bf16(tmem + TM_Y, desc_tile_k(sb + OFF_DO, kk), desc_w(sb + OFF_SOPT, kk), IDC_Y, kk > 0);
-          }
-          umma_commit(c1);
-        }
-        __syncwarp();
         mbar_wait(phi_ready, par);
         RACE_TRACE(a, 6, gc);
         tc_fence_after();
@@ -601,25 +659,33 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             umma_bf16_ts(tmem + TM_Z, tmem + TM_ET + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
-            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST,
+            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO + s * TILE, kk), desc_phi_mn(sb + OFF_PHIQ, kk), IDC_ST,
                       (!first || kk > 0) ? 1u : 0u);
           }
           umma_commit(c3);
-          umma_commit(emptyO);
+          umma_commit(&emptyO[s]);
           if (t + CH >= m.t1) umma_commit(acc_full);
         }
         __syncwarp();
         mbar_wait(dp_ready, par);
         RACE_TRACE(a, 8, gc);
         tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
+        if (elect_one()) {  // dx^ = dproj . W (hi and lo halves of dproj against W' read MN-major)
+          umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIK, 0), desc_wT(sb + OFF_W), IDC_DX, 0u);
+          umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIK, 1), desc_wT(sb + OFF_W), IDC_DX, 1u);
           umma_commit(c4);
         }
         __syncwarp();
-        first = false;
+        // the next chunk's front MMAs, unless it starts a new sequence (then W' changes first)
+        int64_t tn = t + CH, itn = it;
+        if (tn >= m.t1) {
+          ++itn;
+          tn = -1;
+        }
+        if (itn < i1) {
+          const int64_t bhn = tn >= 0 ? m.bh : item_of(a, itn).bh;
+          if (bhn == m.bh) issue_front(gc + 1);
+        }
       }
     }
   } else {
@@ -653,8 +719,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
           scol[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
         }
-        build_wop<256, CT0>(a, m.bh, sb + OFF_W);
-        build_w2<256, CT0>(a, m.bh, sb + OFF_W2);
+        build_wop<256>(a, m.bh, sb + OFF_W);
         if (h == 1) {
           float z[16];
 #pragma unroll
@@ -678,12 +743,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         uint8_t* qtile = smem + OFF_Q + s * TILE;
         float* xpar = xbase + par * XPAR;
         const bool valid = t + r < m.t1;
-        float2 sq2 = make_float2(0.f, 0.f);
-        if (valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
+        mbar_wait(&fullT[s], (gc >> 1) & 1);
+        const float2 sq2 = valid ? *reinterpret_cast<const float2*>(smem + OFF_TOK + s * TOK_BYTES + 8 * r)
+                                 : make_float2(0.f, 0.f);
+        mbar_arrive(&emptyT[s]);
         const Scale scq = row_scale(sq2.x, a.normalize);
         const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_wait(c1, par);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
+        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
         tc_fence_after();
         float pq[16], yv[16];
         float phq[FP], uq[5], hq[5];
@@ -727,22 +794,25 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- row statistics from Pm and E over my 64 columns
         mbar_wait(c2, par);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
+        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
         tc_fence_after();
         float rs = 0.f, nd = 0.f;
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int c0 = 64 * h + 32 * b;
           if ((c0 >> 5) <= qw) {  // warp-uniform
-            float pm[32], e[32];
-            tmem_ld32(tmem + lb + TM_PMC + c0, pm);
-            tmem_ld32(tmem + lb + TM_E + c0, e);
-            tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float pmj = (c0 + j <= r) ? pm[j] : 0.f;
-              rs += pmj;
-              nd = fmaf(pmj, e[j], nd);
+            for (int hh = 0; hh < 32; hh += 16) {  // 16 columns at a time: keeps register pressure down
+              float pm[16], e[16];
+              tmem_ld16(tmem + lb + TM_PMC + c0 + hh, pm);
+              tmem_ld16(tmem + lb + TM_E + c0 + hh, e);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float pmj = (c0 + hh + j <= r) ? pm[j] : 0.f;
+                rs += pmj;
+                nd = fmaf(pmj, e[j], nd);
+              }
             }
           }
         }
@@ -774,7 +844,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           float pht[FP];
 #pragma unroll
           for (int f = 0; f < FP; ++f) pht[f] = phq[f] * rD;
-          write_phi_k(sb + OFF_PHIT, r, pht);
+          write_phi_k(sb + OFF_PHIQ, r, pht);  // Phi_q is dead after Pm (c2): reuse its buffer
           // S_<=c for the next chunk's y (the Y MMA of this chunk completed at c1)
           float sacc[32];
           tmem_ld32(tmem + lb + TM_S, sacc);
@@ -797,7 +867,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- dphi_q -> dproj
         mbar_wait(c3, par);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
+        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
         tc_fence_after();
         float zz[32];
         tmem_ld32(tmem + lb + TM_Z, zz);
@@ -808,22 +878,22 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         float dproj[8];
         row_feature_vjp<P>(a, uq, phq, dphi, dproj);
         const float dotq = dot_from_proj(dproj, hq);
-        if (h == 0) write_dproj(sb + OFF_DPROJ, r, dproj);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(dp_ready);
+        if (h == 0) write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z (c3)
 #pragma unroll
         for (int f = 0; f < FP; ++f)
           A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(dp_ready);
         // ---- dq (my 64 columns) in place of q; the producer stores it
         mbar_wait(c4, par);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
+        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
         tc_fence_after();
         tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 13, gc);
+        if (threadIdx.x == 64) RACE_TRACE(a, 13, gc);
       }
       // ---- segment done: dS total (TMEM) and dA total (block reduction)
       mbar_wait(acc_full, ni & 1);
@@ -1234,11 +1304,11 @@ constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_
 
 // reverse chunk cursor over a CTA's item range (last item, last chunk first)
 struct RCursor {
-  int64_t it, i0, t;
+  int it, i0, t;
   Item m;
   __device__ __forceinline__ void start(const Args& a, int64_t i0_, int64_t i1) {
-    i0 = i0_;
-    it = i1 - 1;
+    i0 = int(i0_);
+    it = int(i1 - 1);
     if (it >= i0) {
       m = item_of(a, it);
       t = m.t0 + ((m.t1 - m.t0 - 1) / CH) * CH;
@@ -1333,7 +1403,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmGD);
       tma_prefetch_desc(&tmNRM);
       const uint64_t pol = policy_evict_first();
-      int64_t kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
+      int kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
       auto store_dk = [&](uint32_t j) {
         const int s = j & 1;
         mbar_wait(&dkstaged[s], (j >> 1) & 1);
@@ -1345,6 +1415,16 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       uint32_t gc = 0;
       RCursor cur;
       for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        if (a.pf > 0) {  // reverse scan: warm L2 with the tiles a.pf chunks earlier in the sequence
+          const int tp = int(cur.t) - a.pf * CH;
+          if (tp >= 0)
+            for (int h = 0; h < 2; ++h) {
+              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
+              tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
+            }
+        }
         const uint32_t par = (gc & 1) ^ 1;
         const int s = gc & 1;
         const int t = int(cur.t), bh = int(cur.m.bh);
@@ -1458,6 +1538,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         umma_commit(emptyO);
       }
       __syncwarp();
+      RACE_TRACE(a, 22, gc);
+      if (a.dbg && blockIdx.x == 0) {
+        mbar_wait(cdv, par);
+        RACE_TRACE(a, 23, gc);
+      }
       mbar_wait(dp_ready, par);
       RACE_TRACE(a, 8, gc);
       tc_fence_after();
@@ -1468,6 +1553,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         umma_commit(c4);
       }
       __syncwarp();
+      RACE_TRACE(a, 20, gc);
+      if (a.dbg && blockIdx.x == 0) {  // trace only: time the dX MMA's completion
+        mbar_wait(c4, par);
+        RACE_TRACE(a, 21, gc);
+      }
     }
   } else {
     const int r = crow();
@@ -1660,15 +1750,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         write_sopT(sb + OFF_DSOPT, r, dsn);
         write_sop(sb + OFF_DSOP, r, dsn);
       }
+      if (threadIdx.x == CT0) RACE_TRACE(a, 17, gc);
       tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, valid);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 18, gc);
       fence_proxy_async();
+      if (threadIdx.x == CT0) RACE_TRACE(a, 19, gc);
       cur.next(a);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
       tc_fence_after();
+      if (threadIdx.x == CT0) RACE_TRACE(a, 14, gc);
       tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 15, gc);
       fence_proxy_async();
+      if (threadIdx.x == CT0) RACE_TRACE(a, 16, gc);
       tc_fence_before();
       mbar_arrive(&dkstaged[s]);
       mbar_arrive(dxfree);
@@ -1700,10 +1796,12 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.dbg = trace_for("bq");
   const char* v1 = getenv("RACE_BWDQ_V1");
   if (nrm && !(v1 && v1[0] == '1')) {
+    CUtensorMap mnrm;
+    if (!make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256)) return cudaErrorInvalidValue;
     switch (g.P) {
-      case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
-      case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
-      default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
+      case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
+      case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
+      default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
     }
   }
   switch (g.P) {

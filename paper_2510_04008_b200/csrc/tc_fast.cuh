@@ -28,6 +28,7 @@ constexpr int NTHREADS = 192;
 constexpr int NTHREADS8 = 320;      // 8-compute-warp kernels: warp 0 TMA, warp 1 MMA, 2..9 compute
 constexpr int CT0 = 64;              // first compute thread of the 8-compute-warp kernels
 constexpr int FP = 8;                // padded feature count
+
 constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
 
 // TMEM column map
@@ -45,6 +46,7 @@ struct Args {
   float* den;
   const float* nrm_in;  // [BH, N, 2] row sums of squares (q, k) saved by the causal forward, or null
   float* nrm_out;
+  int pf;               // chunks of L2 prefetch (cp.async.bulk.prefetch) ahead of the TMA loads
 };
 
 #define RACE_DBG(a_, slot_, val_)                                                        \
@@ -88,14 +90,14 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 struct Item {
-  int64_t bh, seg, t0, t1;  // tokens [t0, t1) of sequence bh
+  int bh, seg, t0, t1;  // tokens [t0, t1) of sequence bh (32-bit: N < 2^31, B*H <= 65535)
 };
 __device__ __forceinline__ Item item_of(const Args& a, int64_t it) {
   Item r;
-  r.bh = it / a.nseg;
-  r.seg = it % a.nseg;
-  r.t0 = r.seg * a.seg_tokens;
-  r.t1 = r.t0 + a.seg_tokens < a.N ? r.t0 + a.seg_tokens : a.N;
+  r.bh = int(it / a.nseg);
+  r.seg = int(it % a.nseg);
+  r.t0 = int(r.seg * a.seg_tokens);
+  r.t1 = int(r.t0 + a.seg_tokens < a.N ? r.t0 + a.seg_tokens : a.N);
   return r;
 }
 
@@ -106,11 +108,11 @@ __device__ __forceinline__ void cta_range(int64_t nitems, int64_t& i0, int64_t& 
 }
 // chunk cursor over a CTA's item range
 struct Cursor {
-  int64_t it, i1, t;
+  int it, i1, t;
   Item m;
   __device__ __forceinline__ void start(const Args& a, int64_t i0, int64_t i1_) {
-    it = i0;
-    i1 = i1_;
+    it = int(i0);
+    i1 = int(i1_);
     if (it < i1) {
       m = item_of(a, it);
       t = m.t0;
@@ -761,6 +763,44 @@ __device__ __forceinline__ void tangent_half_inplace(uint32_t tmem_col, uint8_t*
   for (int j = 0; j < 4; ++j)
     *tile_chunk(tile, r, 8 * h + 4 + j) = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
 }
+// fp32 hyperplane rows (TP x 128, zero-padded to 5 rows) for the CUDA-core dx^ = dproj . W
+template <int NTC, int T0>
+__device__ __forceinline__ void build_wf32(const Args& a, int64_t bh, float* wf) {
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  for (int idx = threadIdx.x - T0; idx < 5 * DH; idx += NTC) wf[idx] = idx < a.TP * DH ? w[idx] : 0.f;
+}
+// columns [64h, 64h + 64) of row r: dx^ = dproj . W (fp32 FMA, W from smem), then the
+// sphere-tangent VJP dx = (dx^ - (dx^.x^) x^) / ||x||, written as bf16 over x in the SW128 tile
+__device__ __forceinline__ void dx_tangent_half(const float* dproj, const float* wf, uint8_t* tile, int r, int h,
+                                                Scale sc, float dot_hat) {
+  const float cx = sc.tangent ? dot_hat * sc.inv : 0.f;
+#pragma unroll 2
+  for (int ch = 0; ch < 8; ++ch) {  // one 16-byte chunk = 8 columns
+    const int chunk = 8 * h + ch, c0 = 8 * chunk;
+    float d[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d[e] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const float4 w0 = *reinterpret_cast<const float4*>(wf + j * DH + c0);
+      const float4 w1 = *reinterpret_cast<const float4*>(wf + j * DH + c0 + 4);
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d[e] = fmaf(dproj[j], wv[e], d[e]);
+    }
+    uint4* px = tile_chunk(tile, r, chunk);
+    const uint4 x = *px;
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float lo = sc.tangent ? (d[2 * q] - cx * bf16_lo(xw[q])) * sc.inv : d[2 * q];
+      const float hi = sc.tangent ? (d[2 * q + 1] - cx * bf16_hi(xw[q])) * sc.inv : d[2 * q + 1];
+      o[q] = pack_bf16(lo, hi);
+    }
+    *px = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
 // TMEM columns [64h, 64h + 64) -> bf16 global row (double-buffered TMEM loads)
 __device__ __forceinline__ void tmem_half_to_global_p(uint32_t tmem_col, int h, __nv_bfloat16* grow, bool store) {
   float v0[32], v1[32];
@@ -849,6 +889,8 @@ inline Args make_args(const Geo& g) {
   a.beta = g.beta;
   a.normalize = g.normalize;
   a.w_per_head = g.w_per_head;
+  const char* pf = getenv("RACE_PF");  // tuning knob, off by default
+  a.pf = pf && pf[0] ? atoi(pf) : 0;  // measured: L2 prefetch slows every kernel here (r01)
   return a;
 }
 
