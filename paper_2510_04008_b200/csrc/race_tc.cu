@@ -195,6 +195,181 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<64>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// K1, contiguous-range version (the one launched).  Each CTA walks a
+// contiguous run of (b*h, segment) items, so W' is rebuilt only when the run
+// enters a new sequence, and the per-segment accumulator is double-buffered
+// in TMEM: segment i accumulates into SACC[i & 1] while the compute warps
+// read out segment i - 1, so the MMA never waits for the read-out.
+// ---------------------------------------------------------------------------
+namespace agg2 {
+using agg::STAGES;
+using agg::STAGE_BYTES;
+using agg::OFF_STAGE;
+using agg::OFF_W;
+using agg::OFF_PHI;
+constexpr int OFF_BAR = agg::OFF_BAR;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr uint32_t TM_PK = 0, TM_ACC = 32;  // accumulators at 32 and 64
+}  // namespace agg2
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_aggregate2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+  using namespace agg2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;               // [STAGES]
+  uint64_t* empty = bars + STAGES;     // [STAGES]
+  uint64_t* proj_full = bars + 2 * STAGES;
+  uint64_t* phi_full = proj_full + 1;
+  uint64_t* phi_empty = phi_full + 1;  // [2]
+  uint64_t* wready = phi_empty + 2;
+  uint64_t* acc_full = wready + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* scratch = reinterpret_cast<float*>(tslot + 4);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&phi_empty[i], 1);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    mbar_init(wready, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<128>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      const uint64_t pol = policy_evict_first();
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc % STAGES;
+        mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+        for (int h = 0; h < 2; ++h) {
+          tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0, ns = 0;
+    int prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ns) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      if (ns >= 2) mbar_wait(&acc_empty[ns & 1], ((ns >> 1) - 1) & 1);  // segment ns - 2 read out
+      tc_fence_after();
+      const uint32_t acc = tmem + TM_ACC + 32 * (ns & 1);
+      for (int t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_PK, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_commit(proj_full);
+        }
+        __syncwarp();
+        mbar_wait(phi_full, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(acc, desc_tile_mn(stage + TILE, kk), desc_phi_mn(phib, kk), ID_STATE,
+                      (t != m.t0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+          umma_commit(&phi_empty[gc & 1]);
+          if (t + CH >= m.t1) umma_commit(&acc_full[ns & 1]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int r = crow();
+    const int F = a.T << a.P;
+    uint32_t gc = 0, ns = 0;
+    int prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ns) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        build_wop(a, m.bh, sb + OFF_W);
+        fence_proxy_async();
+        mbar_arrive(wready);
+      }
+      float asum[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) asum[f] = 0.f;
+      for (int t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc % STAGES;
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc / STAGES) & 1);
+        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
+        mbar_wait(proj_full, gc & 1);
+        tc_fence_after();
+        float proj[16];
+        tmem_ld16(tmem + lane_base() + TM_PK, proj);
+        tmem_ld_wait();
+        float phi[FP];
+        row_features<P>(a, proj, inv, t + r < m.t1, phi);
+#pragma unroll
+        for (int f = 0; f < FP; ++f) asum[f] += phi[f];
+        if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
+        write_phi_k(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(phi_full);
+      }
+      // segment done: S^T (lane r = value column r) from its TMEM buffer, A by a block sum
+      mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
+      tc_fence_after();
+      float acc[32];
+      tmem_ld32(tmem + lane_base() + TM_ACC + 32 * (ns & 1), acc);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ns & 1]);
+      csum8(asum, scratch);
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+#pragma unroll
+      for (int f = 0; f < FP; ++f)
+        if (f < F && r == f) out[f * LDS_T + DH] = asum[f];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
 // ===========================================================================
 // K2: non-causal query-side readout  O = Phi_q S_v / (Phi_q A), den = D / T
 // ===========================================================================
@@ -1072,6 +1247,14 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
   Args a = make_args(g);
   a.w = w;
   a.tout = part;
+  const char* v1 = getenv("RACE_AGG_V1");
+  if (!(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch(k_aggregate2<1>, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      case 2: return launch(k_aggregate2<2>, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      default: return launch(k_aggregate2<3>, agg2::SMEM, grid_for(g), st, mk, mv, a);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_aggregate<1>, agg::SMEM, grid_for(g), st, mk, mv, a);
     case 2: return launch(k_aggregate<2>, agg::SMEM, grid_for(g), st, mk, mv, a);
