@@ -540,6 +540,207 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// K2, 8-compute-warp contiguous-range version (the one launched): W' and the
+// S operand are rebuilt only when the CTA's run enters a new sequence; each
+// half of the compute warps handles 64 columns of every row pass (row norm
+// halves exchanged through shared memory); the producer issues the O store
+// right before refilling that Q buffer, so no compute warp waits on it.
+// ---------------------------------------------------------------------------
+namespace rdo8 {
+using rdo::STAGES;
+using rdo::STAGE_BYTES;
+using rdo::OFF_STAGE;
+using rdo::OFF_W;
+using rdo::OFF_PHI;
+using rdo::OFF_SOP;
+constexpr int OFF_X = rdo::OFF_BAR;  // [2 parity][2 halves][128] row-norm partials
+constexpr int OFF_BAR = OFF_X + 2 * 256 * 4;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr uint32_t TM_NUM_R = 128;
+}  // namespace rdo8
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_readout8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
+  using namespace rdo8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;                    // [STAGES]
+  uint64_t* empty = bars + STAGES;          // [STAGES] (MMA done with the Q tile)
+  uint64_t* ostaged = bars + 2 * STAGES;    // [STAGES] (O staged, 256 arrivals)
+  uint64_t* proj_full = bars + 3 * STAGES;
+  uint64_t* phi_full = proj_full + 1;
+  uint64_t* phi_empty = phi_full + 1;       // [2]
+  uint64_t* wready = phi_empty + 2;
+  uint64_t* num_full = wready + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(num_full + 1);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&ostaged[i], 256);
+    }
+    mbar_init(proj_full, 1);
+    mbar_init(phi_full, 256);
+    mbar_init(&phi_empty[0], 1);
+    mbar_init(&phi_empty[1], 1);
+    mbar_init(wready, 256);
+    mbar_init(num_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmO);
+      const uint64_t pol = policy_evict_first();
+      int ot[STAGES], ob[STAGES];
+      auto store_o = [&](uint32_t j) {  // O of chunk j, staged in its Q tile
+        const int s = j % STAGES;
+        mbar_wait(&ostaged[s], (j / STAGES) & 1);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + h * SUB), h * 64, ot[s], ob[s]);
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc % STAGES;
+        if (gc >= STAGES) {
+          store_o(gc - STAGES);
+          tma_store_wait_read<0>();
+        }
+        mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
+        for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        ot[s] = cur.t;
+        ob[s] = cur.m.bh;
+      }
+      for (uint32_t j = gc >= STAGES ? gc - STAGES : 0; j < gc; ++j) store_o(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      if (cur.m.bh != prev_bh) {
+        prev_bh = cur.m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      const int s = gc % STAGES;
+      const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+      mbar_wait(&full[s], (gc / STAGES) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        umma_commit(proj_full);
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      mbar_wait(phi_full, gc & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+          umma_bf16(tmem + TM_NUM_R, desc_phi_k(phib, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
+        umma_commit(num_full);
+        umma_commit(&phi_empty[gc & 1]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const uint32_t lb = lane_base();
+    const float invT = 1.f / float(a.T);
+    const int F = a.T << a.P;
+    float* xsq = reinterpret_cast<float*>(smem + OFF_X);
+    float A[FP];
+    uint32_t gc = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      const Item m = cur.m;
+      const int t = cur.t;
+      if (m.bh != prev_bh) {  // W' and S operand of this sequence (the previous num MMA is complete)
+        prev_bh = m.bh;
+        const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        float srow[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          srow[f] = f < F ? tab[f * LDS_T + r] : 0.f;
+          A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
+        }
+        if (h == 1) write_sop(sb + OFF_SOP, r, srow);
+        fence_proxy_async();
+        mbar_arrive(wready);
+      }
+      const int s = gc % STAGES;
+      uint8_t* stage = smem + OFF_STAGE + s * STAGE_BYTES;
+      float* xp = xsq + (gc & 1) * 256;
+      mbar_wait(&full[s], (gc / STAGES) & 1);
+      xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
+      compute_bar256();
+      const float inv = inv_scale(xp[r] + xp[128 + r], a.normalize);
+      mbar_wait(proj_full, gc & 1);
+      tc_fence_after();
+      float proj[16];
+      tmem_ld16(tmem + lb + TM_PROJQ, proj);
+      tmem_ld_wait();
+      const bool valid = t + r < m.t1;
+      float phi[FP];
+      row_features<P>(a, proj, inv, valid, phi);
+      float D = 0.f;
+#pragma unroll
+      for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
+      if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
+      if (h == 0) write_phi_q(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(phi_full);
+      if (h == 0 && valid) a.den[m.bh * a.N + t + r] = D * invT;
+      const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+      mbar_wait(num_full, gc & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 64 * h + 32 * b;
+        float v[32];
+        tmem_ld32(tmem + lb + TM_NUM_R + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= rD;
+        stage32_p(stage, r, v, c0);  // the Q tile is dead (proj done, norms read): O staging
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&ostaged[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
 // ===========================================================================
 // K3: causal forward, chunked scan with carry-in per segment
 //   num_c = Phi_q,c S_<c + tril(Phi_q,c Phi_k,c^T) V_c,   S_<c+1 = S_<c + Phi_k,c^T [V_c | 1]
@@ -1271,6 +1472,14 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
   a.w = w;
   a.tin = tab;
   a.den = den;
+  const char* v1 = getenv("RACE_RDO_V1");
+  if (!(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+      case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+      default: return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_readout<1>, rdo::SMEM, grid_for(g), st, mq, mo, a);
     case 2: return launch(k_readout<2>, rdo::SMEM, grid_for(g), st, mq, mo, a);

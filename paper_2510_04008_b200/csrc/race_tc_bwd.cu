@@ -7,6 +7,8 @@
 //   dx^ = dproj . W (MMA), dq = sphere-tangent(dx^) / ||q||
 // Key side (ra/backward.py:122-128):
 //   z = dS_v v (MMA), dphi_k = z + dA, dV = phi_k dS_v (MMA), dk as above.
+#include <cstdlib>
+
 #include "tc_fast.cuh"
 
 namespace race {
@@ -407,6 +409,477 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ===========================================================================
+// Non-causal backward, 8-compute-warp contiguous-range versions (launched).
+// Same math as k_bwd_q / k_bwd_k above.  W' / W'' / the table operands are
+// rebuilt only when a CTA's run enters a new sequence; per-segment dS totals
+// use two TMEM accumulators (segment i accumulates while segment i - 1 is
+// read out); the compute warps split each 128-column pass into halves; the
+// producer issues the gradient stores right before refilling a stage.
+// ===========================================================================
+namespace bq8n {
+using bq::STAGES;
+using bq::STAGE_BYTES;
+using bq::OFF_W;
+using bq::OFF_W2;
+using bq::OFF_SOPT;
+using bq::OFF_PHIT;
+using bq::OFF_DPROJ;
+constexpr int OFF_X = bq::OFF_BAR;  // [2 parity][2 halves][128] norm partials, then da[4][8]
+constexpr int OFF_BAR = OFF_X + (2 * 256 + 32) * 4;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;  // DS: two accumulators at 32 and 64
+}  // namespace bq8n
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_bwd_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+             const __grid_constant__ CUtensorMap tmDQ, Args a) {
+  using namespace bq8n;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;            // [2]
+  uint64_t* empty = bars + 2;       // [2] MMA done with the stage
+  uint64_t* dqstaged = bars + 4;    // [2] dQ staged over Q (256 arrivals)
+  uint64_t* c1 = bars + 6;          // proj + y
+  uint64_t* ready = bars + 7;       // Phi~, dproj staged (256)
+  uint64_t* c2 = bars + 8;          // dS += ..., dx^
+  uint64_t* wready = bars + 9;      // (256)
+  uint64_t* acc_full = bars + 10;   // [2]
+  uint64_t* acc_empty = bars + 12;  // [2] (256)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&dqstaged[i], 256);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 256);
+    }
+    mbar_init(c1, 1);
+    mbar_init(ready, 256);
+    mbar_init(c2, 1);
+    mbar_init(wready, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmDO);
+      tma_prefetch_desc(&tmDQ);
+      const uint64_t pol = policy_evict_first();
+      int qt[2] = {0, 0}, qb[2] = {0, 0};
+      auto store_dq = [&](uint32_t j) {
+        const int s = j & 1;
+        mbar_wait(&dqstaged[s], (j >> 1) & 1);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, qt[s], qb[s]);
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc & 1;
+        if (gc >= 2) {
+          store_dq(gc - 2);
+          tma_store_wait_read<0>();
+        }
+        mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        for (int h = 0; h < 2; ++h) {
+          tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tma_load_3d(st + TILE + h * SUB, &tmDO, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        }
+        qt[s] = cur.t;
+        qb[s] = cur.m.bh;
+      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dq(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0, ns = 0;
+    int prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ns) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      if (ns >= 2) mbar_wait(&acc_empty[ns & 1], ((ns >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t dsacc = tmem + TM_DS + 32 * (ns & 1);
+      for (int t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc & 1;
+        const uint32_t stage = sb + s * STAGE_BYTES;
+        mbar_wait(&full[s], (gc >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + TM_P, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+            umma_bf16(tmem + TM_Y, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_SOPT, kk), ID_Y, kk > 0);
+          }
+          umma_commit(c1);
+        }
+        __syncwarp();
+        mbar_wait(ready, gc & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(dsacc, desc_tile_mn(stage + TILE, kk), desc_phi_mn(sb + OFF_PHIT, kk), ID_DS,
+                      (t != m.t0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), ID_DX, kk > 0);
+          umma_commit(c2);
+          umma_commit(&empty[s]);
+          if (t + CH >= m.t1) umma_commit(&acc_full[ns & 1]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const int qw = warp & 3;
+    const uint32_t lb = lane_base();
+    const float invT = 1.f / float(a.T);
+    const int F = a.T << a.P;
+    float* xsq = reinterpret_cast<float*>(smem + OFF_X);
+    float* xda = xsq + 512;
+    float A[FP];
+    uint32_t gc = 0, ns = 0;
+    int prev_bh = -1;
+    for (int64_t it = i0; it < i1; ++it, ++ns) {
+      const Item m = item_of(a, it);
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        build_w2<256>(a, m.bh, sb + OFF_W2);
+        float scol[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          scol[f] = f < F ? tab[f * LDS_T + r] : 0.f;
+          A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
+        }
+        if (h == 1) write_sopT(sb + OFF_SOPT, r, scol);
+        fence_proxy_async();
+        mbar_arrive(wready);
+      }
+      float dA[FP];
+#pragma unroll
+      for (int f = 0; f < FP; ++f) dA[f] = 0.f;
+      for (int t = m.t0; t < m.t1; t += CH, ++gc) {
+        const int s = gc & 1;
+        uint8_t* stage = smem + s * STAGE_BYTES;
+        float* xp = xsq + (gc & 1) * 256;
+        const bool valid = t + r < m.t1;
+        mbar_wait(&full[s], (gc >> 1) & 1);
+        xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
+        compute_bar256();
+        const Scale sc = row_scale(xp[r] + xp[128 + r], a.normalize);
+        mbar_wait(c1, gc & 1);
+        tc_fence_after();
+        float proj[16], yv[16];
+        tmem_ld16(tmem + lb + TM_P, proj);
+        tmem_ld16(tmem + lb + TM_Y, yv);
+        tmem_ld_wait();
+        float phi[FP], u[5], ph[5];
+        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
+        float y[FP], D = 0.f, num = 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          y[f] = yv[f] + yv[8 + f];
+          D = fmaf(phi[f], A[f], D);
+          num = fmaf(phi[f], y[f], num);
+        }
+        const bool live = valid && D * invT > kDegenerateDenEps;
+        const float rD = live ? 1.f / D : 0.f;
+        const float rho = num * rD;
+        float dphi[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
+        float dproj[8];
+        row_feature_vjp<P>(a, u, phi, dphi, dproj);
+        if (h == 0) {
+          float phit[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) {
+            phit[f] = phi[f] * rD;
+            dA[f] = fmaf(phi[f], -rho * rD, dA[f]);
+          }
+          write_phi_k(sb + OFF_PHIT, r, phit);  // [hi | hi | lo | 0]: MN-major B of dS += dO^T Phi~
+        } else {
+          write_dproj(sb + OFF_DPROJ, r, dproj);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(ready);
+        mbar_wait(c2, gc & 1);
+        tc_fence_after();
+        tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, dot_from_proj(dproj, ph));
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(&dqstaged[s]);
+      }
+      // segment done: partial dS (lane r = value column r) from its TMEM buffer, dA by a block sum
+      mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
+      tc_fence_after();
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      if (h == 1) {
+        float acc[32];
+        tmem_ld32(tmem + lb + TM_DS + 32 * (ns & 1), acc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int f = 0; f < FP; ++f)
+          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+      } else {
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dA[f] += __shfl_xor_sync(0xffffffffu, dA[f], o);
+        }
+        if (lane_id() == 0) {
+#pragma unroll
+          for (int f = 0; f < FP; ++f) xda[qw * FP + f] = dA[f];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ns & 1]);
+      compute_bar256();
+      if (h == 0 && r < F) out[r * LDS_T + DH] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
+      compute_bar256();  // xda is reused by the next segment
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+namespace bk8n {
+using bk::STAGES;
+using bk::STAGE_BYTES;
+using bk::OFF_W;
+using bk::OFF_W2;
+using bk::OFF_DSOPT;
+using bk::OFF_DSOP;
+using bk::OFF_PHIK;
+using bk::OFF_DPROJ;
+constexpr int OFF_X = bk::OFF_BAR;  // [2 parity][2 halves][128] norm partials
+constexpr int OFF_BAR = OFF_X + 2 * 256 * 4;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+using bk::TM_P;
+using bk::TM_Z;
+using bk::TM_DV;
+using bk::TM_DX;
+}  // namespace bk8n
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS8, 1)
+    k_bwd_k8(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+             const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a) {
+  using namespace bk8n;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;          // [2]
+  uint64_t* empty = bars + 2;     // [2] MMA done with the stage
+  uint64_t* staged = bars + 4;    // [2] dK, dV staged over K, V (256)
+  uint64_t* c1 = bars + 6;
+  uint64_t* ready = bars + 7;     // (256)
+  uint64_t* c2 = bars + 8;
+  uint64_t* wready = bars + 9;    // (256)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&staged[i], 256);
+    }
+    mbar_init(c1, 1);
+    mbar_init(ready, 256);
+    mbar_init(c2, 1);
+    mbar_init(wready, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmDK);
+      tma_prefetch_desc(&tmDV);
+      const uint64_t pol = policy_evict_first();
+      int kt[2] = {0, 0}, kb[2] = {0, 0};
+      auto store_kv = [&](uint32_t j) {
+        const int s = j & 1;
+        mbar_wait(&staged[s], (j >> 1) & 1);
+        for (int h = 0; h < 2; ++h) {
+          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, kt[s], kb[s]);
+          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + s * STAGE_BYTES + TILE + h * SUB), h * 64, kt[s], kb[s]);
+        }
+        tma_store_commit();
+      };
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc & 1;
+        if (gc >= 2) {
+          store_kv(gc - 2);
+          tma_store_wait_read<0>();
+        }
+        mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        for (int h = 0; h < 2; ++h) {
+          tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        }
+        kt[s] = cur.t;
+        kb[s] = cur.m.bh;
+      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_kv(j);
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      if (cur.m.bh != prev_bh) {
+        prev_bh = cur.m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      const int s = gc & 1;
+      const uint32_t stage = sb + s * STAGE_BYTES;
+      mbar_wait(&full[s], (gc >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + TM_P, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_bf16(tmem + TM_Z, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_DSOPT, kk), ID_Y, kk > 0);
+        }
+        umma_commit(c1);
+      }
+      __syncwarp();
+      mbar_wait(ready, gc & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), ID_DV, kk > 0);
+          umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), ID_DX, kk > 0);
+        }
+        umma_commit(c2);
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int r = crow();
+    const int h = chalf();
+    const uint32_t lb = lane_base();
+    const int F = a.T << a.P;
+    float* xsq = reinterpret_cast<float*>(smem + OFF_X);
+    float dA[FP];
+    uint32_t gc = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      const Item m = cur.m;
+      const int t = cur.t;
+      if (m.bh != prev_bh) {
+        prev_bh = m.bh;
+        const float* dtab = a.tin + m.bh * int64_t(F) * LDS_T;
+        build_wop<256>(a, m.bh, sb + OFF_W);
+        build_w2<256>(a, m.bh, sb + OFF_W2);
+        float dcol[FP];
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          dcol[f] = f < F ? dtab[f * LDS_T + r] : 0.f;
+          dA[f] = f < F ? dtab[f * LDS_T + DH] : 0.f;
+        }
+        if (h == 1) {
+          write_sopT(sb + OFF_DSOPT, r, dcol);
+          write_sop(sb + OFF_DSOP, r, dcol);
+        }
+        fence_proxy_async();
+        mbar_arrive(wready);
+      }
+      const int s = gc & 1;
+      uint8_t* stage = smem + s * STAGE_BYTES;
+      float* xp = xsq + (gc & 1) * 256;
+      const bool valid = t + r < m.t1;
+      mbar_wait(&full[s], (gc >> 1) & 1);
+      xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
+      compute_bar256();
+      const Scale sc = row_scale(xp[r] + xp[128 + r], a.normalize);
+      mbar_wait(c1, gc & 1);
+      tc_fence_after();
+      float proj[16], zv[16];
+      tmem_ld16(tmem + lb + TM_P, proj);
+      tmem_ld16(tmem + lb + TM_Z, zv);
+      tmem_ld_wait();
+      float phi[FP], u[5], ph[5], dphi[FP];
+      row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
+#pragma unroll
+      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
+      float dproj[8];
+      row_feature_vjp<P>(a, u, phi, dphi, dproj);
+      if (h == 0) write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
+      else write_dproj(sb + OFF_DPROJ, r, dproj);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ready);
+      mbar_wait(c2, gc & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {  // dV over the dead V row (my 64 columns)
+        const int c0 = 64 * h + 32 * b;
+        float v[32];
+        tmem_ld32(tmem + lb + TM_DV + c0, v);
+        tmem_ld_wait();
+        stage32_p(stage + TILE, r, v, c0);
+      }
+      tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, dot_from_proj(dproj, ph));
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&staged[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace tcfast
 
 // ---- entry points ------------------------------------------------------------
@@ -419,6 +892,14 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   a.w = w;
   a.tin = tab;
   a.tout = dpart;
+  const char* v1 = getenv("RACE_BWDNC_V1");
+  if (!(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+      case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+      default: return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_bwd_q<1>, bq::SMEM, grid_for(g), st, mq, mdo, mdq, a);
     case 2: return launch(k_bwd_q<2>, bq::SMEM, grid_for(g), st, mq, mdo, mdq, a);
@@ -435,6 +916,14 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
   Args a = make_args(g);
   a.w = w;
   a.tin = dtab;
+  const char* v1 = getenv("RACE_BWDNC_V1");
+  if (!(v1 && v1[0] == '1')) {
+    switch (g.P) {
+      case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+      case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+      default: return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    }
+  }
   switch (g.P) {
     case 1: return launch(k_bwd_k<1>, bk::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
     case 2: return launch(k_bwd_k<2>, bk::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
