@@ -389,9 +389,9 @@ def run_ours(args, world, rank, local_rank):
     dom_bytes = kb[dom] * HEADS * n
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     # (tools/ncu_summary.py traffic; same workload: N=131072 per GPU, H=4, bf16)
-    ncu_names = {"kside_partials": "k_aggregate", "fwd_causal": "k_causal_fwd8", "bwd_causal_q": "k_bwd_causal_q8",
-                 "bwd_causal_k": "k_bwd_causal_k8", "fwd_readout": "k_readout", "bwd_qside": "k_bwd_q",
-                 "bwd_kside": "k_bwd_k", "combine": "k_combine", "combine_d": "k_combine"}
+    ncu_names = {"kside_partials": "k_aggregate2", "fwd_causal": "k_causal_fwd8", "bwd_causal_q": "k_bwd_causal_q8",
+                 "bwd_causal_k": "k_bwd_causal_k8", "fwd_readout": "k_readout8", "bwd_qside": "k_bwd_q8",
+                 "bwd_kside": "k_bwd_k8", "combine": "k_combine", "combine_d": "k_combine"}
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))

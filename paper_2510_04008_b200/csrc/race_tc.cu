@@ -548,15 +548,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // right before refilling that Q buffer, so no compute warp waits on it.
 // ---------------------------------------------------------------------------
 namespace rdo8 {
-using rdo::STAGES;
-using rdo::STAGE_BYTES;
-using rdo::OFF_STAGE;
-using rdo::OFF_W;
-using rdo::OFF_PHI;
-using rdo::OFF_SOP;
-constexpr int OFF_X = rdo::OFF_BAR;  // [2 parity][2 halves][128] row-norm partials
+constexpr int STAGES = 6;             // Q tiles in flight (each reused as its O staging)
+constexpr int STAGE_BYTES = TILE;
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_W = STAGES * STAGE_BYTES;
+constexpr int OFF_PHI = OFF_W + WOP;  // 2 buffers
+constexpr int OFF_SOP = OFF_PHI + 2 * PHI;
+constexpr int OFF_X = OFF_SOP + PHI;  // [2 parity][2 halves][128] row-norm partials
 constexpr int OFF_BAR = OFF_X + 2 * 256 * 4;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
+static_assert(SMEM <= 232448, "k_readout8 shared memory");
 constexpr uint32_t TM_NUM_R = 128;
 }  // namespace rdo8
 
