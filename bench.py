@@ -223,6 +223,44 @@ def max_context(dev, causal, dtype):
     return {"tokens": 0, "causal": causal, "error": "nothing fits"}
 
 
+def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 1 << 24)):
+    """BASELINE configs[2]: fwd+bwd tokens/s of the H=4, d=128 layer for N from 1 Mi to
+    16 Mi tokens on one GPU, causal and non-causal (inputs resident in HBM, 2 timed reps)."""
+    import torch
+
+    import paper_2510_04008_b200 as rb
+
+    out = []
+    gen = torch.Generator(device=dev).manual_seed(5)
+    for causal in (True, False):
+        cfg = rb.SketchConfig(hyperplanes=P_, tables=L_, beta=BETA, seed=0, causal=causal)
+        w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
+        p = cfg.params()
+        for n in sizes:
+            try:
+                q, k, v, g = (torch.randn((1, HEADS, n, DIM), generator=gen, device=dev, dtype=dtype) for _ in range(4))
+                o, den, st = rb.race_forward(q, k, v, w, p)
+                rb.race_backward(q, k, v, w, g, p, state=st)
+                del o, den, st
+                torch.cuda.synchronize()
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                ev[0].record()
+                for _ in range(2):
+                    o, den, st = rb.race_forward(q, k, v, w, p)
+                    rb.race_backward(q, k, v, w, g, p, state=st)
+                    del o, den, st
+                ev[1].record()
+                torch.cuda.synchronize()
+                ms = ev[0].elapsed_time(ev[1]) / 2
+                out.append({"tokens": n, "causal": causal, "ms_fwd_bwd": round(ms, 3),
+                            "tokens_per_s": n / (ms / 1e3)})
+                del q, k, v, g
+            except torch.cuda.OutOfMemoryError:
+                out.append({"tokens": n, "causal": causal, "error": "out of memory"})
+            torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # our GPU path
 # ---------------------------------------------------------------------------
@@ -485,6 +523,7 @@ def main():
                 dev = torch.device("cuda", local_rank)
                 dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
                 line["max_context"] = [max_context(dev, c, dt) for c in (True, False)]
+                line["scale_sweep"] = scale_sweep(dev, dt)
             print(json.dumps(line), flush=True)
     finally:
         if world > 1:

@@ -576,8 +576,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* phi_full = proj_full + 1;
   uint64_t* phi_empty = phi_full + 1;       // [2]
   uint64_t* wready = phi_empty + 2;
-  uint64_t* num_full = wready + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(num_full + 1);
+  uint64_t* num_full = wready + 1;          // [2] (per NUM buffer: the compute warps run one chunk ahead)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(num_full + 2);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
@@ -591,10 +591,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     mbar_init(&phi_empty[0], 1);
     mbar_init(&phi_empty[1], 1);
     mbar_init(wready, 256);
-    mbar_init(num_full, 1);
+    mbar_init(&num_full[0], 1);
+    mbar_init(&num_full[1], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tslot);
+  if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -661,13 +662,17 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)
-          umma_bf16(tmem + TM_NUM_R, desc_phi_k(phib, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
-        umma_commit(num_full);
+          umma_bf16(tmem + TM_NUM_R + 128 * (gc & 1), desc_phi_k(phib, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA,
+                    kk > 0);
+        umma_commit(&num_full[gc & 1]);
         umma_commit(&phi_empty[gc & 1]);
       }
       __syncwarp();
     }
   } else {
+    // Software-pipelined: the front half of chunk c + 1 (row norms, features, Phi_q,
+    // den) runs before the back half of chunk c (numerator read-out), so the numerator
+    // MMA of c + 1 overlaps the read-out of c (two NUM buffers in TMEM).
     const int r = crow();
     const int h = chalf();
     const uint32_t lb = lane_base();
@@ -675,13 +680,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     const int F = a.T << a.P;
     float* xsq = reinterpret_cast<float*>(smem + OFF_X);
     float A[FP];
-    uint32_t gc = 0;
     int prev_bh = -1;
-    Cursor cur;
-    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
-      const Item m = cur.m;
-      const int t = cur.t;
-      if (m.bh != prev_bh) {  // W' and S operand of this sequence (the previous num MMA is complete)
+    auto front = [&](const Cursor& c, uint32_t g) -> float {  // returns 1/D of row r
+      const Item m = c.m;
+      if (m.bh != prev_bh) {  // W' and S operand of this sequence (no MMA of the old one in flight)
         prev_bh = m.bh;
         const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
         build_wop<256>(a, m.bh, sb + OFF_W);
@@ -695,38 +697,42 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         fence_proxy_async();
         mbar_arrive(wready);
       }
-      const int s = gc % STAGES;
+      const int s = g % STAGES;
       uint8_t* stage = smem + OFF_STAGE + s * STAGE_BYTES;
-      float* xp = xsq + (gc & 1) * 256;
-      mbar_wait(&full[s], (gc / STAGES) & 1);
+      float* xp = xsq + (g & 1) * 256;
+      mbar_wait(&full[s], (g / STAGES) & 1);
       xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
       compute_bar256();
       const float inv = inv_scale(xp[r] + xp[128 + r], a.normalize);
-      mbar_wait(proj_full, gc & 1);
+      mbar_wait(proj_full, g & 1);
       tc_fence_after();
       float proj[16];
       tmem_ld16(tmem + lb + TM_PROJQ, proj);
       tmem_ld_wait();
-      const bool valid = t + r < m.t1;
+      const bool valid = c.t + r < m.t1;
       float phi[FP];
       row_features<P>(a, proj, inv, valid, phi);
       float D = 0.f;
 #pragma unroll
       for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
-      if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
-      if (h == 0) write_phi_q(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
+      if (g >= 2) mbar_wait(&phi_empty[g & 1], ((g >> 1) - 1) & 1);
+      if (h == 0) write_phi_q(sb + OFF_PHI + (g & 1) * PHI, r, phi);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(phi_full);
-      if (h == 0 && valid) a.den[m.bh * a.N + t + r] = D * invT;
-      const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
-      mbar_wait(num_full, gc & 1);
+      if (h == 0 && valid) a.den[m.bh * a.N + c.t + r] = D * invT;
+      return (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+    };
+    auto back = [&](uint32_t g, float rD) {
+      const int s = g % STAGES;
+      uint8_t* stage = smem + OFF_STAGE + s * STAGE_BYTES;
+      mbar_wait(&num_full[g & 1], (g >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const int c0 = 64 * h + 32 * b;
         float v[32];
-        tmem_ld32(tmem + lb + TM_NUM_R + c0, v);
+        tmem_ld32(tmem + lb + TM_NUM_R + 128 * (g & 1) + c0, v);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= rD;
@@ -735,11 +741,29 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&ostaged[s]);
+    };
+    uint32_t gc = 0;
+    Cursor cur;
+    cur.start(a, i0, i1);
+    float rD = cur.ok() ? front(cur, 0) : 0.f;
+    while (cur.ok()) {
+      Cursor nx = cur;
+      nx.next(a);
+      if (nx.ok() && nx.m.bh == cur.m.bh) {
+        const float rDn = front(nx, gc + 1);
+        back(gc, rD);
+        rD = rDn;
+      } else {  // the next chunk rebuilds the S operand: finish this one first
+        back(gc, rD);
+        if (nx.ok()) rD = front(nx, gc + 1);
+      }
+      cur = nx;
+      ++gc;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // ===========================================================================
