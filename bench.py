@@ -261,6 +261,37 @@ def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 1 << 24))
     return out
 
 
+def gpt_train_step(dev, steps=5, warmup=3):
+    """BASELINE configs[4]: one training step (fwd + bwd + fused AdamW, bf16 autocast) of a
+    6-layer, d_model=768, 12-head GPT with causal RACE attention in every layer, on a
+    16K-token synthetic sequence (random init, random tokens).  Device-timed."""
+    import torch
+
+    from paper_2510_04008_b200.gpt import GPTConfig, RaceGPT, train_step
+
+    torch.manual_seed(0)
+    cfg = GPTConfig()
+    model = RaceGPT(cfg).to(dev)
+    opt = torch.optim.AdamW(model.parameters(), lr=3e-4, fused=True)
+    g = torch.Generator(device=dev).manual_seed(3)
+    idx = torch.randint(0, cfg.vocab, (1, cfg.seq_len), device=dev, generator=g)
+    tgt = torch.roll(idx, -1, dims=1)
+    for _ in range(warmup):
+        train_step(model, opt, idx, tgt)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(steps):
+        loss = train_step(model, opt, idx, tgt)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / steps
+    return {"model": "RaceGPT 6 layers, d_model 768, 12 heads (d=64 padded onto the d=128 kernels)",
+            "params_M": round(sum(p.numel() for p in model.parameters()) / 1e6, 1), "seq_len": cfg.seq_len,
+            "batch": 1, "ms_per_step": round(ms, 3), "tokens_per_s": cfg.seq_len / (ms / 1e3),
+            "loss": float(loss), "data": "synthetic random tokens", "dtype": "bf16 autocast, fp32 master"}
+
+
 # ---------------------------------------------------------------------------
 # our GPU path
 # ---------------------------------------------------------------------------
@@ -524,6 +555,7 @@ def main():
                 dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
                 line["max_context"] = [max_context(dev, c, dt) for c in (True, False)]
                 line["scale_sweep"] = scale_sweep(dev, dt)
+                line["gpt_train_step"] = gpt_train_step(dev)
             print(json.dumps(line), flush=True)
     finally:
         if world > 1:
