@@ -88,7 +88,7 @@ def train_step(model: RaceGPT, opt: torch.optim.Optimizer, idx: torch.Tensor, ta
     """One optimiser step (bf16 autocast, fp32 master weights); returns the loss (device tensor)."""
     with torch.autocast("cuda", dtype=torch.bfloat16):
         logits = model(idx)
-        loss = F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))
+        loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.view(-1))  # fp32 inside autocast
     loss.backward()
     opt.step()
     opt.zero_grad(set_to_none=True)
