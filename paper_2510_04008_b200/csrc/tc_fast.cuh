@@ -218,6 +218,24 @@ __device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wo
   }
 }
 
+// Fast-path transcendental helpers (bf16 inputs, 1e-2 tolerance): ex2.approx has
+// ~2^-22 relative error; tanh via e = 2^(-2|x| log2 e): tanh|x| = (1 - e) / (1 + e),
+// accurate to ~1e-6 relative (the hardware tanh.approx, ~2^-11, would put ~1e-2 of
+// error into phi at beta = 8, so it is not used).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_tanh(float x) {
+  const float e = ex2_approx(-2.8853900817779268f * fabsf(x));  // exp(-2|x|)
+  const float t = __fdividef(1.f - e, 1.f + e);
+  return copysignf(t, x);
+}
+__device__ __forceinline__ float fast_exp_neg(float y) {  // exp(-y)
+  return ex2_approx(-1.4426950408889634f * y);
+}
+
 // features of one row from its 16 projection columns (P compile-time, T <= 8 >> P)
 template <int P>
 __device__ __forceinline__ void row_features(const Args& a, const float* proj, float inv, bool valid, float* phi) {
@@ -233,8 +251,8 @@ __device__ __forceinline__ void row_features(const Args& a, const float* proj, f
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const int j = tau * P + p;
-        const float u = tanhf((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
-        e[p] = expf(-2.f * a.beta * fabsf(u));
+        const float u = fast_tanh((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
+        e[p] = fast_exp_neg(2.f * a.beta * fabsf(u));
         neg[p] = u < 0.f;
         z *= 1.f + e[p];
       }
@@ -391,10 +409,10 @@ __device__ __forceinline__ void row_features_u(const Args& a, const float* proj,
       for (int p = 0; p < P; ++p) {
         const int j = tau * P + p;
         const float ph = (proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv;
-        const float uu = tanhf(ph);
+        const float uu = fast_tanh(ph);
         phat[j] = ph;
         u[j] = uu;
-        e[p] = expf(-2.f * a.beta * fabsf(uu));
+        e[p] = fast_exp_neg(2.f * a.beta * fabsf(uu));
         neg[p] = uu < 0.f;
         z *= 1.f + e[p];
       }
