@@ -1332,8 +1332,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmRD,
-                    const __grid_constant__ CUtensorMap tmGD, const __grid_constant__ CUtensorMap tmNRM, Args a,
-                    __nv_bfloat16* __restrict__ dvout) {
+                    const __grid_constant__ CUtensorMap tmGD, const __grid_constant__ CUtensorMap tmNRM,
+                    const __grid_constant__ CUtensorMap tmDV, Args a) {
   using namespace ck8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1361,7 +1361,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* cdv = bars + 21;       // dV MMAs done
   uint64_t* fullT = bars + 22;     // [2] per-token inputs landed (parity buffers)
   uint64_t* emptyT = bars + 24;    // [2] ... consumed (256 arrivals)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* dvstaged = bars + 26;  // dV staged in the (consumed) V tile (256 arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 27);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
@@ -1381,6 +1382,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_init(&fullT[i], 1);
       mbar_init(&emptyT[i], 256);
     }
+    mbar_init(dvstaged, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -1402,8 +1404,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmRD);
       tma_prefetch_desc(&tmGD);
       tma_prefetch_desc(&tmNRM);
+      tma_prefetch_desc(&tmDV);
       const uint64_t pol = policy_evict_first();
       int kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
+      int vt = 0, vb = 0;  // coordinates of the dV tile held by the V buffer
       auto store_dk = [&](uint32_t j) {
         const int s = j & 1;
         mbar_wait(&dkstaged[s], (j >> 1) & 1);
@@ -1449,7 +1453,15 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           tma_load_1d(tok + 512, &tmGD, &fullT[s], row, pol);
           tma_load_1d(tok + 1024, &tmNRM, &fullT[s], 2 * row, pol);
         }
-        mbar_wait(emptyV, par);
+        if (gc >= 1) {  // dV of the previous chunk is staged in the V tile: store it, then refill
+          mbar_wait(dvstaged, (gc - 1) & 1);
+          for (int h = 0; h < 2; ++h)
+            tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + h * SUB), h * 64, vt, vb);
+          tma_store_commit();
+          tma_store_wait_read<0>();
+        }
+        vt = t;
+        vb = bh;
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
@@ -1457,6 +1469,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         RACE_TRACE(a, 2, gc);
         mbar_arrive_expect_tx(fullO, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
+      }
+      if (gc >= 1) {
+        mbar_wait(dvstaged, (gc - 1) & 1);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + h * SUB), h * 64, vt, vb);
+        tma_store_commit();
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dk(j);
       tma_store_wait_all<0>();
@@ -1500,7 +1518,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
         }
         umma_commit(c1);
-        umma_commit(emptyV);
       }
       __syncwarp();
       mbar_wait(phi_ready, par);
@@ -1659,7 +1676,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);  // for dk (off the MMA path)
         }
       }
+      if (threadIdx.x == CT0) RACE_TRACE(a, 24, gc);
       compute_bar256();  // rd / gd of every query token, dA partials
+      if (threadIdx.x == CT0) RACE_TRACE(a, 25, gc);
       // ---- EG~ = (E^T rd + gd) masked t >= i, my 64 columns -> TMEM A operand of Z
       mbar_wait(c1, par);
       tc_fence_after();
@@ -1688,6 +1707,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(eg_ready);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 26, gc);
       // ---- P~^T = Pm^T rd masked t >= i -> TMEM A operand of dV
       mbar_wait(c2, par);
       tc_fence_after();
@@ -1716,6 +1736,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(pt_ready);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 27, gc);
       // ---- dphi_k -> dproj (Z and the dS update are done at c3)
       mbar_wait(c3, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
@@ -1734,6 +1755,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dp_ready);
+      if (threadIdx.x == CT0) RACE_TRACE(a, 28, gc);
 #pragma unroll
       for (int f = 0; f < FP; ++f)
         dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
@@ -1750,21 +1772,24 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         write_sopT(sb + OFF_DSOPT, r, dsn);
         write_sop(sb + OFF_DSOP, r, dsn);
       }
-      if (threadIdx.x == CT0) RACE_TRACE(a, 17, gc);
-      tmem_half_to_global_p(tmem + lb + TM_DV, h, dvout + (m.bh * a.N + t + r) * DH, valid);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 18, gc);
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {  // dV (my 64 columns) into the V tile (consumed at c1); the producer stores it
+        const int c0 = 64 * h + 32 * b;
+        float v[32];
+        tmem_ld32(tmem + lb + TM_DV + c0, v);
+        tmem_ld_wait();
+        stage32_p(smem + OFF_V, r, v, c0);
+      }
       fence_proxy_async();
-      if (threadIdx.x == CT0) RACE_TRACE(a, 19, gc);
+      tc_fence_before();
+      mbar_arrive(dvstaged);
       cur.next(a);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
       tc_fence_after();
-      if (threadIdx.x == CT0) RACE_TRACE(a, 14, gc);
       tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 15, gc);
       fence_proxy_async();
-      if (threadIdx.x == CT0) RACE_TRACE(a, 16, gc);
       tc_fence_before();
       mbar_arrive(&dkstaged[s]);
       mbar_arrive(dxfree);
@@ -1826,15 +1851,15 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.dbg = trace_for("bk");
   const char* v1 = getenv("RACE_BWDK_V1");
   if (nrm && !(v1 && v1[0] == '1')) {
-    __nv_bfloat16* dvp = static_cast<__nv_bfloat16*>(dv);
-    CUtensorMap mrd, mgd, mnrm;
+    CUtensorMap mrd, mgd, mnrm, mdv2;
+    if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
     if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
         !make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256))
       return cudaErrorInvalidValue;
     switch (g.P) {
-      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
-      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
-      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, a, dvp);
+      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
+      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
+      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
     }
   }
   switch (g.P) {
