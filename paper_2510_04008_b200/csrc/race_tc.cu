@@ -782,242 +782,6 @@ constexpr int OFF_BAR = OFF_SOP + PHI;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace cfw
 
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_causal_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Args a) {
-  using namespace cfw;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;                 // [2]
-  uint64_t* empty = bars + 2;            // [2]  (MMA commit + store-read arrive)
-  uint64_t* proj_full = bars + 4;
-  uint64_t* phi_full = bars + 5;
-  uint64_t* pm_full = bars + 6;
-  uint64_t* pt_full = bars + 7;
-  uint64_t* num_full = bars + 8;
-  uint64_t* wready = bars + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 2); }
-    mbar_init(proj_full, 1);
-    mbar_init(phi_full, 128);
-    mbar_init(pm_full, 1);
-    mbar_init(pt_full, 128);
-    mbar_init(num_full, 1);
-    mbar_init(wready, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      tma_prefetch_desc(&tmO);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const int s = gc & 1;
-          mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
-          for (int h = 0; h < 2; ++h) {
-            tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, int(t), int(m.bh), pol);
-            tma_load_3d(st + TILE + h * SUB, &tmK, &full[s], h * 64, int(t), int(m.bh), pol);
-            tma_load_3d(st + 2 * TILE + h * SUB, &tmV, &full[s], h * 64, int(t), int(m.bh), pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      tc_fence_after();
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          }
-          umma_commit(proj_full);
-        }
-        __syncwarp();
-        mbar_wait(phi_full, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_PM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), ID_PM, kk > 0);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + 2 * TILE, kk), desc_phi_mn(sb + OFF_PHIK, kk), ID_STATE, 1u);
-          umma_commit(pm_full);
-        }
-        __syncwarp();
-        mbar_wait(pt_full, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_NUM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_NUM, desc_tile_k(stage, kk), desc_tile_mn(stage + 2 * TILE, kk), ID_NUMB, 1u);
-          umma_commit(num_full);
-          umma_commit(&empty[s]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int r = crow();
-    const float invT = 1.f / float(a.T);
-    const int F = a.T << a.P;
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-      build_wop(a, m.bh, sb + OFF_W);
-      float srow[FP], A[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        srow[f] = f < F ? car[f * LDS_T + r] : 0.f;
-        A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
-      }
-      // S accumulator (lane r = value column r): cols 0..7 = S_in, the rest 0
-      {
-        float z[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = j < FP ? srow[j] : 0.f;
-        tmem_st16(tmem + lane_base() + TM_SACC, z);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = 0.f;
-        tmem_st16(tmem + lane_base() + TM_SACC + 16, z);
-        tmem_st_wait();
-      }
-      write_sop(sb + OFF_SOP, r, srow);
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(wready);
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        const float sqq = tile_row_sumsq(stage, r), sqk = tile_row_sumsq(stage + TILE, r);
-        const float invq = inv_scale(sqq, a.normalize);
-        const float invk = inv_scale(sqk, a.normalize);
-        const bool valid = t + r < m.t1;
-        if (a.nrm_out && valid)
-          *reinterpret_cast<float2*>(a.nrm_out + (m.bh * a.N + t + r) * 2) = make_float2(sqq, sqk);
-        mbar_wait(proj_full, gc & 1);
-        tc_fence_after();
-        float pq[16], pk[16];
-        tmem_ld16(tmem + lane_base() + TM_PROJQ, pq);
-        tmem_ld16(tmem + lane_base() + TM_PROJK, pk);
-        tmem_ld_wait();
-        float phq[FP], phk[FP];
-        row_features<P>(a, pq, invq, valid, phq);
-        row_features<P>(a, pk, invk, valid, phk);
-        write_phi_q(sb + OFF_PHIQ, r, phq);
-        write_phi_k(sb + OFF_PHIK, r, phk);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(phi_full);
-        float D = 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
-        csum8(phk, scratch);  // chunk total of phi_k (identical in every thread)
-        // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 into the dead Q tile
-        mbar_wait(pm_full, gc & 1);
-        tc_fence_after();
-        float rs = 0.f;
-        const int qw = warp & 3;  // rows 32qw..: column blocks > qw are above the diagonal
-#pragma unroll
-        for (int c0 = 0; c0 < CH; c0 += 32) {
-          float v[32];
-          if ((c0 >> 5) > qw) {  // warp-uniform
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            stage_row_bf16(stage, r, v, c0);
-            continue;
-          }
-          tmem_ld32(tmem + lane_base() + TM_PM + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] = (c0 + j <= r) ? v[j] : 0.f;
-            rs += v[j];
-          }
-          stage_row_bf16(stage, r, v, c0);
-        }
-        D += rs;
-        float sacc[32];
-        tmem_ld32(tmem + lane_base() + TM_SACC, sacc);  // S_<=c (value column r)
-        tmem_ld_wait();
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(pt_full);
-        if (valid) a.den[m.bh * a.N + t + r] = D * invT;
-        const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) A[f] += phk[f];
-        // ---- numerator -> O (staged in the dead K tile), then next chunk's S operand
-        mbar_wait(num_full, gc & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base() + TM_NUM + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= rD;
-          stage_row_bf16(stage + TILE, r, v, c0);
-        }
-        float snext[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
-        write_sop(sb + OFF_SOP, r, snext);
-        fence_proxy_async();
-        tc_fence_before();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + TILE + h * SUB), h * 64,
-                         int(t), int(m.bh));
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          mbar_arrive(&empty[s]);
-        }
-      }
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
 // ---------------------------------------------------------------------------
 // K3, pipelined 8-compute-warp version (the one launched).
 //
@@ -1533,18 +1297,10 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.den = den;
   a.nrm_out = nrm;
   a.dbg = trace_for("fwd");
-  const char* v1 = getenv("RACE_FWD_V1");
-  if (!(v1 && v1[0] == '1')) {
-    switch (g.P) {
-      case 1: return launch_nt(k_causal_fwd8<1>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-      case 2: return launch_nt(k_causal_fwd8<2>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-      default: return launch_nt(k_causal_fwd8<3>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-    }
-  }
   switch (g.P) {
-    case 1: return launch(k_causal_fwd<1>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-    case 2: return launch(k_causal_fwd<2>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-    default: return launch(k_causal_fwd<3>, cfw::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    case 1: return launch_nt(k_causal_fwd8<1>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    case 2: return launch_nt(k_causal_fwd8<2>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+    default: return launch_nt(k_causal_fwd8<3>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
   }
 }
 

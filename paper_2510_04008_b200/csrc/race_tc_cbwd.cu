@@ -32,381 +32,6 @@ constexpr uint32_t IDC_DVA = idesc_bf16(128, 128, 0, 0);  // Phi_k x dS-op      
 constexpr uint32_t IDC_DVB = idesc_bf16(128, 128, 0, 1);  // P~^T x dO            (K, MN)
 
 // ===========================================================================
-// causal backward, query side
-// ===========================================================================
-namespace cq {
-constexpr int OFF_Q = 0, OFF_K = TILE, OFF_V = 2 * TILE, OFF_DO = 3 * TILE, OFF_ET = 4 * TILE;
-constexpr int OFF_W = 5 * TILE;
-constexpr int OFF_W2 = OFF_W + WOP;
-constexpr int OFF_SOPT = OFF_W2 + W2OP;
-constexpr int OFF_PHIQ = OFF_SOPT + WOP;  // [hi|lo|hi|0]  A of Pm
-constexpr int OFF_PHIK = OFF_PHIQ + PHI;  // [hi|hi|lo|0]  B of Pm (K), of state / Z (MN)
-constexpr int OFF_PHIT = OFF_PHIK + PHI;  // phi_q / D     B of dS (MN)
-constexpr int OFF_DPROJ = OFF_PHIT + PHI;
-constexpr int OFF_BAR = OFF_DPROJ + PHI;
-constexpr int SMEM = OFF_BAR + 512 + 1024;
-constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_PMC = 256, TM_E = 384,
-                   TM_DX = 256;
-}  // namespace cq
-
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_bwd_causal_q(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                   const __grid_constant__ CUtensorMap tmDQ, Args a, float* __restrict__ rden,
-                   float* __restrict__ gden) {
-  using namespace cq;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* fullQ = bars + 0;
-  uint64_t* fullK = bars + 1;
-  uint64_t* fullV = bars + 2;
-  uint64_t* fullO = bars + 3;
-  uint64_t* emptyQ = bars + 4;   // store drained (thread 64)
-  uint64_t* emptyK = bars + 5;   // projK MMA + 128 norm readers
-  uint64_t* emptyV = bars + 6;   // MMA (E, state)
-  uint64_t* emptyO = bars + 7;   // MMA (Y, E, dS)
-  uint64_t* c1 = bars + 8;
-  uint64_t* c2 = bars + 9;
-  uint64_t* c3 = bars + 10;
-  uint64_t* c4 = bars + 11;
-  uint64_t* phi_ready = bars + 12;
-  uint64_t* et_ready = bars + 13;
-  uint64_t* dp_ready = bars + 14;
-  uint64_t* wready = bars + 15;
-  uint64_t* acc_full = bars + 16;
-  uint64_t* acc_empty = bars + 17;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-    mbar_init(emptyQ, 1);
-    mbar_init(emptyK, 129);
-    mbar_init(emptyV, 1);
-    mbar_init(emptyO, 1);
-    for (int i = 8; i < 12; ++i) mbar_init(&bars[i], 1);
-    mbar_init(phi_ready, 128);
-    mbar_init(et_ready, 128);
-    mbar_init(dp_ready, 128);
-    mbar_init(wready, 128);
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-  if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
-  if (warp >= 2) {  // masked blocks of E~ are never written: zero them once
-    for (int i = threadIdx.x - 64; i < TILE / 16; i += 128)
-      reinterpret_cast<uint4*>(smem + OFF_ET)[i] = make_uint4(0, 0, 0, 0);
-    fence_proxy_async();
-  }
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      tma_prefetch_desc(&tmDO);
-      tma_prefetch_desc(&tmDQ);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const uint32_t par = (gc & 1) ^ 1;
-          // tiles free up in this order within a chunk: K, V, dO, Q
-          mbar_wait(emptyK, par);
-          RACE_TRACE(a, 0, gc);
-          mbar_arrive_expect_tx(fullK, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, int(t), int(m.bh), pol);
-          mbar_wait(emptyV, par);
-          RACE_TRACE(a, 1, gc);
-          mbar_arrive_expect_tx(fullV, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, int(t), int(m.bh), pol);
-          mbar_wait(emptyO, par);
-          RACE_TRACE(a, 2, gc);
-          mbar_arrive_expect_tx(fullO, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, int(t), int(m.bh), pol);
-          mbar_wait(emptyQ, par);
-          RACE_TRACE(a, 3, gc);
-          mbar_arrive_expect_tx(fullQ, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, int(t), int(m.bh), pol);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
-      tc_fence_after();
-      bool first = true;
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const uint32_t par = gc & 1;
-        mbar_wait(fullQ, par);
-        mbar_wait(fullK, par);
-        RACE_TRACE(a, 4, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          }
-          umma_commit(emptyK);
-        }
-        __syncwarp();
-        mbar_wait(fullV, par);
-        mbar_wait(fullO, par);
-        RACE_TRACE(a, 5, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_DO, kk), desc_tile_k(sb + OFF_V, kk), IDC_E, kk > 0);
-            umma_bf16(tmem + TM_Y, desc_tile_k(sb + OFF_DO, kk), desc_w(sb + OFF_SOPT, kk), IDC_Y, kk > 0);
-          }
-          umma_commit(c1);
-        }
-        __syncwarp();
-        mbar_wait(phi_ready, par);
-        RACE_TRACE(a, 6, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_PMC, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), IDC_PM, kk > 0);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_S, desc_tile_mn(sb + OFF_V, kk), desc_phi_mn(sb + OFF_PHIK, kk), IDC_ST, 1u);
-          umma_commit(c2);
-          umma_commit(emptyV);
-        }
-        __syncwarp();
-        mbar_wait(et_ready, par);
-        RACE_TRACE(a, 7, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_Z, desc_tile_k(sb + OFF_ET, kk), desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
-            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST,
-                      (!first || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(c3);
-          umma_commit(emptyO);
-          if (t + CH >= m.t1) umma_commit(acc_full);
-        }
-        __syncwarp();
-        mbar_wait(dp_ready, par);
-        RACE_TRACE(a, 8, gc);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
-          umma_commit(c4);
-        }
-        __syncwarp();
-        first = false;
-      }
-    }
-  } else {
-    const int r = crow();
-    const float invT = 1.f / float(a.T);
-    const int F = a.T << a.P;
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-      build_wop(a, m.bh, sb + OFF_W);
-      build_w2(a, m.bh, sb + OFF_W2);
-      float scol[FP], A[FP], dA[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        scol[f] = f < F ? car[f * LDS_T + r] : 0.f;
-        A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
-        dA[f] = 0.f;
-      }
-      {
-        float z[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = j < FP ? scol[j] : 0.f;
-        tmem_st16(tmem + lane_base() + TM_S, z);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = 0.f;
-        tmem_st16(tmem + lane_base() + TM_S + 16, z);
-        tmem_st_wait();
-      }
-      write_sopT(sb + OFF_SOPT, r, scol);
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(wready);
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const uint32_t par = gc & 1;
-        const bool valid = t + r < m.t1;
-        float2 sq2 = make_float2(0.f, 0.f);
-        if (a.nrm_in && valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
-        mbar_wait(fullQ, par);
-        mbar_wait(fullK, par);
-        if (!a.nrm_in) sq2 = make_float2(tile_row_sumsq(sb + OFF_Q, r), tile_row_sumsq(sb + OFF_K, r));
-        const Scale scq = row_scale(sq2.x, a.normalize);
-        const Scale sck = row_scale(sq2.y, a.normalize);
-        mbar_arrive(emptyK);
-        mbar_wait(c1, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
-        tc_fence_after();
-        float pq[16], pk[16], yv[16];
-        tmem_ld16(tmem + lane_base() + TM_PQ, pq);
-        tmem_ld16(tmem + lane_base() + TM_PK, pk);
-        tmem_ld16(tmem + lane_base() + TM_Y, yv);
-        tmem_ld_wait();
-        float phq[FP], uq[5], hq[5], phk[FP], uk[5], hk[5];
-        row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
-        row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
-        write_phi_q(sb + OFF_PHIQ, r, phq);
-        write_phi_k(sb + OFF_PHIK, r, phk);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(phi_ready);
-        float y[FP], Dint = 0.f, ydot = 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          y[f] = yv[f] + yv[8 + f];
-          Dint = fmaf(phq[f], A[f], Dint);
-          ydot = fmaf(phq[f], y[f], ydot);
-        }
-        csum8(phk, scratch);  // chunk total of phi_k
-        // ---- row statistics from Pm and E
-        mbar_wait(c2, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
-        tc_fence_after();
-        float rs = 0.f, nd = 0.f;
-        const int qw = warp & 3;  // this warp's rows are 32qw..32qw+31: column blocks > qw are masked out
-#pragma unroll
-        for (int c0 = 0; c0 < CH; c0 += 32) {
-          if ((c0 >> 5) > qw) continue;  // warp-uniform: the whole block is above the diagonal
-          float pm[32], e[32];
-          tmem_ld32(tmem + lane_base() + TM_PMC + c0, pm);
-          tmem_ld32(tmem + lane_base() + TM_E + c0, e);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float pmj = (c0 + j <= r) ? pm[j] : 0.f;
-            rs += pmj;
-            nd = fmaf(pmj, e[j], nd);
-          }
-        }
-        const float D = Dint + rs;
-        const bool live = valid && D * invT > kDegenerateDenEps;
-        const float rD = live ? 1.f / D : 0.f;
-        const float rho = (ydot + nd) * rD;
-        // E~ = tril(E - rho) -> bf16 A operand
-#pragma unroll
-        for (int c0 = 0; c0 < CH; c0 += 32) {
-          if ((c0 >> 5) > qw) continue;  // stays zero from the kernel prologue
-          float e[32];
-          tmem_ld32(tmem + lane_base() + TM_E + c0, e);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) e[j] = (c0 + j <= r) ? e[j] - rho : 0.f;
-          stage_row_bf16(sb + OFF_ET, r, e, c0);
-        }
-        float pht[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          pht[f] = phq[f] * rD;
-          dA[f] = fmaf(phq[f], -rho * rD, dA[f]);
-        }
-        write_phi_k(sb + OFF_PHIT, r, pht);
-        // S_<=c for the next chunk's y (M_Y of this chunk has completed at c1)
-        float sacc[32];
-        tmem_ld32(tmem + lane_base() + TM_S, sacc);
-        tmem_ld_wait();
-        float snext[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
-        write_sopT(sb + OFF_SOPT, r, snext);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(et_ready);
-        if (valid) {
-          rden[m.bh * a.N + t + r] = rD;
-          gden[m.bh * a.N + t + r] = -rho * rD;
-        }
-        // ---- dphi_q -> dproj
-        mbar_wait(c3, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
-        tc_fence_after();
-        float zz[32];
-        tmem_ld32(tmem + lane_base() + TM_Z, zz);
-        tmem_ld_wait();
-        float dphi[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
-        float dproj[8];
-        row_feature_vjp<P>(a, uq, phq, dphi, dproj);
-        const float dotq = dot_from_proj(dproj, hq);
-        write_dproj(sb + OFF_DPROJ, r, dproj);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(dp_ready);
-#pragma unroll
-        for (int f = 0; f < FP; ++f) A[f] += phk[f];
-        // ---- dq in place of q, then store
-        mbar_wait(c4, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
-        tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_Q, r, scq, dotq);
-        tc_fence_before();
-        fence_proxy_async();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          RACE_TRACE(a, 13, gc);
-          for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + h * SUB), h * 64, int(t), int(m.bh));
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          RACE_TRACE(a, 14, gc);
-          mbar_arrive(emptyQ);
-        }
-      }
-      // item done: segment dS total
-      mbar_wait(acc_full, ni & 1);
-      tc_fence_after();
-      float acc[32];
-      tmem_ld32(tmem + lane_base() + TM_DS, acc);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(acc_empty);
-      csum8(dA, scratch);
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F && r == f) out[f * LDS_T + DH] = dA[f];
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
-// ===========================================================================
 // causal backward, query side -- pipelined 8-compute-warp version (launched)
 //
 // Same math as k_bwd_causal_q above, restructured for latency:
@@ -926,347 +551,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) RACE_CTA_TIME(a, 1);
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
-// ===========================================================================
-// causal backward, key side (reverse scan)
-// ===========================================================================
-namespace ck {
-constexpr int OFF_Q = 0, OFF_K = TILE, OFF_V = 2 * TILE, OFF_DO = 3 * TILE, OFF_EG = 4 * TILE;
-constexpr int OFF_W = 5 * TILE;
-constexpr int OFF_W2 = OFF_W + WOP;
-constexpr int OFF_DSOPT = OFF_W2 + W2OP;   // [16 x 128] B of z = V dS_v^T
-constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // [128 x 32] B of dV_a = Phi_k dS_v
-constexpr int OFF_PHIQ = OFF_DSOP + PHI;   // [hi|hi|lo|0]  B of Pm^T (K) and of Z' (MN)
-constexpr int OFF_PHIK = OFF_PHIQ + PHI;   // [hi|lo|hi|0]  A of Pm^T and dV_a
-constexpr int OFF_PHIT = OFF_PHIK + PHI;   // phi_q / D     B of dS (MN)
-constexpr int OFF_DPROJ = OFF_PHIT + PHI;
-constexpr int OFF_RG = OFF_DPROJ + PHI;    // rden[128], gden[128]
-constexpr int OFF_BAR = OFF_RG + 1024;
-constexpr int SMEM = OFF_BAR + 512 + 1024;
-constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_E = 128, TM_DX = 128, TM_PMC = 256,
-                   TM_DV = 384;
-}  // namespace ck
-
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_bwd_causal_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                   const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a,
-                   const float* __restrict__ rden, const float* __restrict__ gden) {
-  using namespace ck;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* fullQ = bars + 0;
-  uint64_t* fullK = bars + 1;
-  uint64_t* fullV = bars + 2;
-  uint64_t* fullO = bars + 3;
-  uint64_t* emptyQ = bars + 4;   // projQ MMA + 128 norm readers
-  uint64_t* emptyK = bars + 5;   // dK store drained
-  uint64_t* emptyV = bars + 6;   // dV store drained (V slot also holds P~^T and dV)
-  uint64_t* emptyO = bars + 7;   // MMA (E^T, dV_b, dS)
-  uint64_t* c1 = bars + 8;
-  uint64_t* c2 = bars + 9;
-  uint64_t* c3 = bars + 10;
-  uint64_t* c4 = bars + 11;
-  uint64_t* phi_ready = bars + 12;
-  uint64_t* pt_ready = bars + 13;
-  uint64_t* dp_ready = bars + 14;
-  uint64_t* wready = bars + 15;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
-  float* rg = reinterpret_cast<float*>(smem + OFF_RG);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-    mbar_init(emptyQ, 129);
-    mbar_init(emptyK, 1);
-    mbar_init(emptyV, 1);
-    mbar_init(emptyO, 1);
-    for (int i = 8; i < 12; ++i) mbar_init(&bars[i], 1);
-    mbar_init(phi_ready, 128);
-    mbar_init(pt_ready, 128);
-    mbar_init(dp_ready, 128);
-    mbar_init(wready, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-  if (warp >= 2) {  // masked blocks of EG~ are never written: zero them once
-    for (int i = threadIdx.x - 64; i < TILE / 16; i += 128)
-      reinterpret_cast<uint4*>(smem + OFF_EG)[i] = make_uint4(0, 0, 0, 0);
-    fence_proxy_async();
-  }
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      tma_prefetch_desc(&tmDO);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        const int64_t nch = (m.t1 - m.t0 + CH - 1) / CH;
-        for (int64_t ci = nch - 1; ci >= 0; --ci, ++gc) {
-          const int t = int(m.t0 + ci * CH);
-          const uint32_t par = (gc & 1) ^ 1;
-          // free order within a chunk: Q, dO, K/V (stores)
-          mbar_wait(emptyQ, par);
-          mbar_arrive_expect_tx(fullQ, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, t, int(m.bh), pol);
-          mbar_wait(emptyO, par);
-          mbar_arrive_expect_tx(fullO, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, int(m.bh), pol);
-          mbar_wait(emptyK, par);
-          mbar_arrive_expect_tx(fullK, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, int(m.bh), pol);
-          mbar_wait(emptyV, par);
-          mbar_arrive_expect_tx(fullV, TILE);
-          for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, int(m.bh), pol);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const int64_t nch = (m.t1 - m.t0 + CH - 1) / CH;
-      for (int64_t ci = nch - 1; ci >= 0; --ci, ++gc) {
-        const uint32_t par = gc & 1;
-        // dS operands for this chunk are written by the compute warps before
-        // wready (first chunk) / dp_ready of the previous chunk
-        if (ci == nch - 1) mbar_wait(wready, ni & 1);
-        mbar_wait(fullQ, par);
-        mbar_wait(fullK, par);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          }
-          umma_commit(emptyQ);
-        }
-        __syncwarp();
-        mbar_wait(fullV, par);
-        mbar_wait(fullO, par);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_ZV, desc_tile_k(sb + OFF_V, kk), desc_w(sb + OFF_DSOPT, kk), IDC_Y, kk > 0);
-            umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
-          }
-          umma_commit(c1);
-        }
-        __syncwarp();
-        mbar_wait(phi_ready, par);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            umma_bf16(tmem + TM_PMC, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_PHIQ, kk), IDC_PM, kk > 0);
-            umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), IDC_DVA, kk > 0);
-          }
-          umma_commit(c2);
-        }
-        __syncwarp();
-        mbar_wait(pt_ready, par);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_Z, desc_tile_k(sb + OFF_EG, kk), desc_phi_mn(sb + OFF_PHIQ, kk), IDC_Z, kk > 0);
-            umma_bf16(tmem + TM_DV, desc_tile_k(sb + OFF_V, kk), desc_tile_mn(sb + OFF_DO, kk), IDC_DVB, 1u);
-            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
-          }
-          umma_commit(c3);
-          umma_commit(emptyO);
-        }
-        __syncwarp();
-        mbar_wait(dp_ready, par);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
-          umma_commit(c4);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int r = crow();
-    const int F = a.T << a.P;
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const float* dcar = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-      build_wop(a, m.bh, sb + OFF_W);
-      build_w2(a, m.bh, sb + OFF_W2);
-      float dcol[FP], dA[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        dcol[f] = f < F ? dcar[f * LDS_T + r] : 0.f;
-        dA[f] = f < F ? dcar[f * LDS_T + DH] : 0.f;
-      }
-      {
-        float z[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = j < FP ? dcol[j] : 0.f;
-        tmem_st16(tmem + lane_base() + TM_DS, z);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = 0.f;
-        tmem_st16(tmem + lane_base() + TM_DS + 16, z);
-        tmem_st_wait();
-      }
-      write_sopT(sb + OFF_DSOPT, r, dcol);
-      write_sop(sb + OFF_DSOP, r, dcol);
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(wready);
-      const int64_t nch = (m.t1 - m.t0 + CH - 1) / CH;
-      for (int64_t ci = nch - 1; ci >= 0; --ci, ++gc) {
-        const int64_t t = m.t0 + ci * CH;
-        const uint32_t par = gc & 1;
-        const bool valid = t + r < m.t1;
-        // per-query-token normaliser terms of this chunk (rg is free: the previous
-        // chunk finished reading it before its final compute_bar)
-        const float rd_ld = valid ? rden[m.bh * a.N + t + r] : 0.f;
-        const float gd_ld = valid ? gden[m.bh * a.N + t + r] : 0.f;
-        float2 sq2 = make_float2(0.f, 0.f);
-        if (a.nrm_in && valid) sq2 = *reinterpret_cast<const float2*>(a.nrm_in + (m.bh * a.N + t + r) * 2);
-        mbar_wait(fullQ, par);
-        mbar_wait(fullK, par);
-        if (!a.nrm_in) sq2 = make_float2(tile_row_sumsq(sb + OFF_Q, r), tile_row_sumsq(sb + OFF_K, r));
-        const Scale scq = row_scale(sq2.x, a.normalize);
-        const Scale sck = row_scale(sq2.y, a.normalize);
-        mbar_arrive(emptyQ);
-        rg[r] = rd_ld;
-        rg[128 + r] = gd_ld;
-        mbar_wait(c1, par);
-        tc_fence_after();
-        float pq[16], pk[16], zv[16];
-        tmem_ld16(tmem + lane_base() + TM_PQ, pq);
-        tmem_ld16(tmem + lane_base() + TM_PK, pk);
-        tmem_ld16(tmem + lane_base() + TM_ZV, zv);
-        tmem_ld_wait();
-        float phq[FP], phk[FP], uk[5], uq[5], hq[5], hk[5];
-        row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
-        row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
-        write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
-        write_phi_q(sb + OFF_PHIK, r, phk);  // [hi|lo|hi|0]
-        fence_proxy_async();
-        tc_fence_before();
-        compute_bar();  // rg visible to all compute threads
-        mbar_arrive(phi_ready);
-        const float rDr = rg[r], gdr = rg[128 + r];
-        // ---- EG~ (from E^T) and P~^T (from Pm^T), masked t >= i
-        mbar_wait(c2, par);
-        tc_fence_after();
-        const int qw = warp & 3;  // rows 32qw..32qw+31: column blocks < qw are masked out (t < i)
-#pragma unroll
-        for (int c0 = 0; c0 < CH; c0 += 32) {
-          if ((c0 >> 5) < qw) {  // warp-uniform: EG~ block stays zero from the prologue
-            float z[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = 0.f;
-            stage_row_bf16(sb + OFF_V, r, z, c0);
-            continue;
-          }
-          float e[32], pm[32];
-          tmem_ld32(tmem + lane_base() + TM_E + c0, e);
-          tmem_ld32(tmem + lane_base() + TM_PMC + c0, pm);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int tq = c0 + j;
-            const bool keep = tq >= r;
-            const float rdt = rg[tq];
-            e[j] = keep ? fmaf(e[j], rdt, rg[128 + tq]) : 0.f;
-            pm[j] = keep ? pm[j] * rdt : 0.f;
-          }
-          stage_row_bf16(sb + OFF_EG, r, e, c0);
-          stage_row_bf16(sb + OFF_V, r, pm, c0);  // V is dead after c1
-        }
-        float pht[FP], dAc[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          pht[f] = phq[f] * rDr;
-          dAc[f] = phq[f] * gdr;
-        }
-        write_phi_k(sb + OFF_PHIT, r, pht);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(pt_ready);
-        csum8(dAc, scratch);  // this chunk's contribution to dA (for the earlier chunks)
-        // ---- dphi_k, dV, next dS operands
-        mbar_wait(c3, par);
-        tc_fence_after();
-        float zz[32];
-        tmem_ld32(tmem + lane_base() + TM_Z, zz);
-        tmem_ld_wait();
-        float dphi[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
-        float dproj[8];
-        row_feature_vjp<P>(a, uk, phk, dphi, dproj);
-        const float dotk = dot_from_proj(dproj, hk);
-        write_dproj(sb + OFF_DPROJ, r, dproj);
-        float dsa[32];
-        tmem_ld32(tmem + lane_base() + TM_DS, dsa);
-        tmem_ld_wait();
-        float dsn[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          dsn[f] = dsa[f] + dsa[16 + f];
-          dA[f] += dAc[f];
-        }
-        write_sopT(sb + OFF_DSOPT, r, dsn);
-        write_sop(sb + OFF_DSOP, r, dsn);
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base() + TM_DV + c0, v);
-          tmem_ld_wait();
-          stage_row_bf16(sb + OFF_V, r, v, c0);  // dV over P~^T (consumed at c3)
-        }
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(dp_ready);
-        // ---- dk in place of k, then store dK, dV
-        mbar_wait(c4, par);
-        tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, sb + OFF_K, r, sck, dotk);
-        tc_fence_before();
-        fence_proxy_async();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          for (int h = 0; h < 2; ++h) {
-            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, int(t), int(m.bh));
-            tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + h * SUB), h * 64, int(t), int(m.bh));
-          }
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          mbar_arrive(emptyK);
-          mbar_arrive(emptyV);
-        }
-      }
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -1819,20 +1103,13 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.tout = dpart;
   a.nrm_in = nrm;
   a.dbg = trace_for("bq");
-  const char* v1 = getenv("RACE_BWDQ_V1");
-  if (nrm && !(v1 && v1[0] == '1')) {
-    CUtensorMap mnrm;
-    if (!make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256)) return cudaErrorInvalidValue;
-    switch (g.P) {
-      case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
-      case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
-      default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
-    }
-  }
+  if (!nrm) return cudaErrorInvalidValue;  // race_abi.cu always supplies the forward's rows
+  CUtensorMap mnrm;
+  if (!make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256)) return cudaErrorInvalidValue;
   switch (g.P) {
-    case 1: return launch(k_bwd_causal_q<1>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
-    case 2: return launch(k_bwd_causal_q<2>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
-    default: return launch(k_bwd_causal_q<3>, cq::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, a, rden, gden);
+    case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
+    case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
+    default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
   }
 }
 
@@ -1849,23 +1126,16 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.tin = dcar;
   a.nrm_in = nrm;
   a.dbg = trace_for("bk");
-  const char* v1 = getenv("RACE_BWDK_V1");
-  if (nrm && !(v1 && v1[0] == '1')) {
-    CUtensorMap mrd, mgd, mnrm, mdv2;
-    if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
-    if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
-        !make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256))
-      return cudaErrorInvalidValue;
-    switch (g.P) {
-      case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
-      case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
-      default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
-    }
-  }
+  if (!nrm) return cudaErrorInvalidValue;
+  CUtensorMap mrd, mgd, mnrm, mdv2;
+  if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
+  if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
+      !make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256))
+    return cudaErrorInvalidValue;
   switch (g.P) {
-    case 1: return launch(k_bwd_causal_k<1>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);
-    case 2: return launch(k_bwd_causal_k<2>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);
-    default: return launch(k_bwd_causal_k<3>, ck::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mdv, a, rden, gden);
+    case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
+    case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
+    default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
   }
 }
 
