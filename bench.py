@@ -407,7 +407,7 @@ def run_ours(args, world, rank, local_rank):
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     rden = torch.empty((pr.bh, n), device=dev)
     gden = torch.empty_like(rden)
-    norms = torch.empty((pr.bh, n, 2), device=dev)
+    norms = torch.empty((pr.bh, n, 16), device=dev)  # sketch rows
     S = _stream()
     ptr = _vp
     if causal:

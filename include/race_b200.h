@@ -94,8 +94,11 @@ int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
 
 /* Elements (float32) of the state race_fwd saves for race_bwd:
  * non-causal: tables [BH, F, dv+1];
- * causal: carries [BH, nseg, F, dv+1] followed by rownorms [BH, N, 2]
- *         (sum of squares of each q and k row, reused by the backward).    */
+ * causal: carries [BH, nseg, F, dv+1] followed by the sketch rows
+ *         [BH, N, 16]: per token, floats 0..7 describe q and 8..15 k; slot j
+ *         (j < T*P) holds x^.w_j = (x.w_j)/||x|| and slot 7 holds ||x||^2.
+ *         The backward rebuilds phi from them instead of re-reading the
+ *         other operand (the generic path fills only the norms).          */
 int race_state_elems(const race_desc_t* desc, int64_t* elems);
 
 /* ---- monolithic single-device entry points ---------------------------- */
@@ -138,8 +141,8 @@ int race_fwd_readout(const race_desc_t* desc, const void* q, const float* w,
                      void* workspace, void* stream);
 
 /* Causal chunked scan given per-segment carry-in tables
- * (ra/forward.py:100-121).  rownorms (may be NULL) receives [BH, N, 2]
- * float32: the sum of squares of each q and k row.                        */
+ * (ra/forward.py:100-121).  rownorms (may be NULL) receives the sketch
+ * rows [BH, N, 16] (see race_state_elems).                                */
 int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k,
                     const void* v, const float* w, const float* carries,
                     void* o, float* den, float* rownorms, void* workspace,
@@ -158,8 +161,8 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v,
 
 /* Causal backward, forward-direction scan: dq, per-token normaliser terms
  * rden = 1/(T*den), gden = -(dO.O)/(T*den), and per-segment dS totals
- * (ra/backward.py:142-168).  rownorms (may be NULL = recompute) is what
- * race_fwd_causal wrote.                                                  */
+ * (ra/backward.py:142-168).  rownorms (may be NULL = recompute into the
+ * workspace) is what race_fwd_causal wrote (sketch rows).                 */
 int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k,
                       const void* v, const void* d_o, const float* w,
                       const float* carries, const float* rownorms, void* dq,

@@ -30,7 +30,7 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
 cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
                             const float* w, const float* rden, const float* gden, const float* dcar,
                             const float* nrm, void* dk, void* dv, cudaStream_t st);
-cudaError_t tc_rownorms(const Geo& g, const void* q, const void* k, float* nrm, cudaStream_t st);
+cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* w, float* rows, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
                           const float* car, void* o, float* den, float* nrm, cudaStream_t st);
 }  // namespace race
@@ -117,7 +117,7 @@ struct WsLayout {
   float* dtables;  // [BH, nseg, E]
   float* rden;
   float* gden;
-  float* nrm;      // [BH, N, 2] row norms when the caller has no forward state
+  float* rows;     // [BH, N, 16] sketch rows when the caller has no forward state
   size_t bytes;
 };
 
@@ -136,7 +136,7 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
   w.dtables = take(segE);
   w.rden = take(tok);
   w.gden = take(tok);
-  w.nrm = take(2 * tok);
+  w.rows = take(16 * tok);
   w.bytes = off;
   return w;
 }
@@ -175,7 +175,7 @@ int race_workspace_bytes(const race_desc_t* desc, size_t* bytes) {
 int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
-  *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g) + (g.causal ? 2 * g.BH * g.N : 0);
+  *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g) + (g.causal ? 16 * g.BH * g.N : 0);
   return RACE_OK;
 }
 
@@ -255,11 +255,11 @@ int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k, con
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
   if (race::tc_supported(g)) {
-    if (!rownorms) {  // recompute the forward's row norms (same summation order)
+    if (!rownorms) {  // recompute the forward's sketch rows (bit-identical)
       if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
-      float* nrm = ws_layout(g, workspace).nrm;
-      if (int rc = cuda_status(race::tc_rownorms(g, q, k, nrm, S(stream)), "tc_rownorms")) return rc;
-      rownorms = nrm;
+      float* rows = ws_layout(g, workspace).rows;
+      if (int rc = cuda_status(race::tc_project(g, q, k, w, rows, S(stream)), "tc_project")) return rc;
+      rownorms = rows;
     }
     return cuda_status(race::tc_bwd_causal_q(g, q, k, v, d_o, w, carries, rownorms, dq, rden, gden, dpart, S(stream)),
                        "tc_bwd_causal_q");
@@ -277,9 +277,9 @@ int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, con
   if (race::tc_supported(g)) {
     if (!rownorms) {
       if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
-      float* nrm = ws_layout(g, workspace).nrm;
-      if (int rc = cuda_status(race::tc_rownorms(g, q, k, nrm, S(stream)), "tc_rownorms")) return rc;
-      rownorms = nrm;
+      float* rows = ws_layout(g, workspace).rows;
+      if (int rc = cuda_status(race::tc_project(g, q, k, w, rows, S(stream)), "tc_project")) return rc;
+      rownorms = rows;
     }
     return cuda_status(race::tc_bwd_causal_k(g, q, k, v, d_o, w, rden, gden, dcarries, rownorms, dk, dv, S(stream)),
                        "tc_bwd_causal_k");
@@ -328,8 +328,8 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   }
   const float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
   if (!nrm && race::tc_supported(g)) {  // once for both passes
-    if (int rc = cuda_status(race::tc_rownorms(g, q, k, ws.nrm, S(stream)), "tc_rownorms")) return rc;
-    nrm = ws.nrm;
+    if (int rc = cuda_status(race::tc_project(g, q, k, w, ws.rows, S(stream)), "tc_project")) return rc;
+    nrm = ws.rows;
   }
   if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, nrm, dq, ws.rden, ws.gden, ws.dpart, workspace,
                                  stream))

@@ -357,11 +357,13 @@ __global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict_
     __syncthreads();
     tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
     tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
-    if (nrm) {  // row sums of squares for the backward (same meaning as the fast path's)
+    if (nrm) {  // sketch rows (race_b200.h): the generic backward only uses the row norms
       for (int r = threadIdx.x; r < rows; r += NT) {
         const float sq = rowv[kScQ * TILE + r], sk = rowv[kScK * TILE + r];
-        nrm[(bh * g.N + t0 + r) * 2 + 0] = sq > 0.f ? sq * sq : 0.f;
-        nrm[(bh * g.N + t0 + r) * 2 + 1] = sk > 0.f ? sk * sk : 0.f;
+        float* row = nrm + (bh * g.N + t0 + r) * 16;
+        for (int j = 0; j < 16; ++j) row[j] = 0.f;
+        row[7] = sq > 0.f ? sq * sq : 0.f;
+        row[15] = sk > 0.f ? sk * sk : 0.f;
       }
     }
     __syncthreads();

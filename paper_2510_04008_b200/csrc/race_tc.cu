@@ -1004,7 +1004,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(&fullqk[0], 0);
       const float sq = tile_row_sumsq(sb + OFF_STAGE + h * TILE, r);
       xbase[h * 128 + r] = sq;
-      if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
       compute_bar256();
       if (threadIdx.x == CT0) mbar_arrive(&emptyqk[0]);
       sqq = xbase[r];
@@ -1056,6 +1055,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tmem_ld_wait();
         row_features<P>(a, pq, invq, valid, phq);
         write_phi_q(sb + OFF_PHIQ, r, phq);
+        if (a.rows_out && valid) {  // sketch row, q half
+          float hat[5];
+          row_hat(a, pq, invq, hat);
+          store_row_half(a.rows_out + (m.bh * a.N + t + r) * ROWW, hat, sqq);
+        }
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(phi_full);
@@ -1066,6 +1070,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tmem_ld_wait();
         row_features<P>(a, pk, invk, valid, phk);
         write_phi_k(sb + OFF_PHIK, r, phk);
+        if (a.rows_out && valid) {  // sketch row, k half
+          float hat[5];
+          row_hat(a, pk, invk, hat);
+          store_row_half(a.rows_out + (m.bh * a.N + t + r) * ROWW + 8, hat, sqk);
+        }
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(phi_full);
@@ -1125,7 +1134,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(&fullqk[sn], ((gc + 1) >> 1) & 1);
         const float sq = tile_row_sumsq(sb + OFF_STAGE + sn * STAGE_BYTES + h * TILE, r);
         xpar[h * 128 + r] = sq;
-        if (a.nrm_out && cur.t + r < cur.m.t1) a.nrm_out[(cur.m.bh * a.N + cur.t + r) * 2 + h] = sq;
       }
       compute_bar256();
       if (threadIdx.x == CT0 && cur.ok()) mbar_arrive(&emptyqk[(gc + 1) & 1]);
@@ -1165,29 +1173,133 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 }
 
 
-// row sums of squares of q and k ([BH, N, 2]) in exactly the order the
-// forward's tile_row_sumsq accumulates them, for backward calls without state
-__global__ void __launch_bounds__(256) k_rownorms(const uint4* __restrict__ q, const uint4* __restrict__ k,
-                                                  float* __restrict__ nrm, int64_t rows) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-#pragma unroll
-  for (int which = 0; which < 2; ++which) {
-    const uint4* x = (which ? k : q) + i * 16;
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const uint4 v = x[c];
-      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = bf16_lo(w4[e]), hi = bf16_hi(w4[e]);
-        s0 = fmaf(lo, lo, s0);
-        s1 = fmaf(hi, hi, s1);
+// ---------------------------------------------------------------------------
+// Sketch rows of q and k for backward calls without forward state (the
+// reference itself recomputes the forward, ra/backward.py:200).  Same TMA
+// tiles, same projection MMA chain and the same row-norm code as
+// k_causal_fwd8, so the rows are bit-identical to the ones the forward saves.
+// ---------------------------------------------------------------------------
+namespace prj {
+constexpr int STAGES = 2;
+constexpr int STAGE_BYTES = 2 * TILE;  // Q, K
+constexpr int OFF_W = STAGES * STAGE_BYTES;
+constexpr int OFF_BAR = OFF_W + WOP;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+}  // namespace prj
+
+template <int P>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_project(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, Args a) {
+  using namespace prj;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;          // [2]
+  uint64_t* empty = bars + 2;     // [2] (MMA commit + 128 row-norm readers)
+  uint64_t* proj_full = bars + 4; // [2] (TMEM projection buffer per parity)
+  uint64_t* proj_empty = bars + 6;// [2] (128 readers)
+  uint64_t* wready = bars + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 129);
+      mbar_init(&proj_full[i], 1);
+      mbar_init(&proj_empty[i], 128);
+    }
+    mbar_init(wready, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<64>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  int64_t i0, i1;
+  cta_range(a.BH * a.nseg, i0, i1);
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t gc = 0;
+      Cursor cur;
+      for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+        const int s = gc & 1;
+        mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        for (int h = 0; h < 2; ++h) {
+          tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tma_load_3d(st + TILE + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        }
       }
     }
-    nrm[i * 2 + which] = s0 + s1;
+  } else if (warp == 1) {
+    uint32_t gc = 0, nr = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      if (cur.m.bh != prev_bh) {
+        prev_bh = cur.m.bh;
+        mbar_wait(wready, nr & 1);
+        ++nr;
+      }
+      const int s = gc & 1;
+      const uint32_t stage = sb + s * STAGE_BYTES;
+      const uint32_t acc = tmem + 32 * s;
+      mbar_wait(&full[s], (gc >> 1) & 1);
+      if (gc >= 2) mbar_wait(&proj_empty[s], ((gc >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(acc, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+          umma_bf16(acc + 16, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        }
+        umma_commit(&proj_full[s]);
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int r = crow();
+    uint32_t gc = 0;
+    int prev_bh = -1;
+    Cursor cur;
+    for (cur.start(a, i0, i1); cur.ok(); cur.next(a), ++gc) {
+      if (cur.m.bh != prev_bh) {  // the previous projections are consumed (program order)
+        prev_bh = cur.m.bh;
+        build_wop(a, cur.m.bh, sb + OFF_W);
+        fence_proxy_async();
+        mbar_arrive(wready);
+      }
+      const int s = gc & 1;
+      const uint32_t stage = sb + s * STAGE_BYTES;
+      mbar_wait(&full[s], (gc >> 1) & 1);
+      const float sqq = tile_row_sumsq(stage, r), sqk = tile_row_sumsq(stage + TILE, r);
+      mbar_arrive(&empty[s]);
+      mbar_wait(&proj_full[s], (gc >> 1) & 1);
+      tc_fence_after();
+      float pq[16], pk[16];
+      tmem_ld16(tmem + lane_base() + 32 * s, pq);
+      tmem_ld16(tmem + lane_base() + 32 * s + 16, pk);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&proj_empty[s]);
+      if (cur.t + r < cur.m.t1) {
+        float hat[5];
+        float* dst = a.rows_out + (int64_t(cur.m.bh) * a.N + cur.t + r) * ROWW;
+        row_hat(a, pq, inv_scale(sqq, a.normalize), hat);
+        store_row_half(dst, hat, sqq);
+        row_hat(a, pk, inv_scale(sqk, a.normalize), hat);
+        store_row_half(dst + 8, hat, sqk);
+      }
+    }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<64>(tmem);
 }
 
 static unsigned* g_dbg_host = nullptr;
@@ -1276,13 +1388,19 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
   }
 }
 
-cudaError_t tc_rownorms(const Geo& g, const void* q, const void* k, float* nrm, cudaStream_t st) {
-  const int64_t rows = g.BH * g.N;
-  if (rows == 0) return cudaSuccess;
-  tcfast::k_rownorms<<<unsigned((rows + 255) / 256), 256, 0, st>>>(static_cast<const uint4*>(q),
-                                                                  static_cast<const uint4*>(k), nrm, rows);
-  note_launch();
-  return cudaGetLastError();
+cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* w, float* rows, cudaStream_t st) {
+  using namespace tcfast;
+  if (g.BH * g.N == 0) return cudaSuccess;
+  CUtensorMap mq, mk;
+  if (!make_map(&mq, q, g) || !make_map(&mk, k, g)) return cudaErrorInvalidValue;
+  Args a = make_args(g);
+  a.w = w;
+  a.rows_out = rows;
+  switch (g.P) {
+    case 1: return launch(k_project<1>, prj::SMEM, grid_for(g), st, mq, mk, a);
+    case 2: return launch(k_project<2>, prj::SMEM, grid_for(g), st, mq, mk, a);
+    default: return launch(k_project<3>, prj::SMEM, grid_for(g), st, mq, mk, a);
+  }
 }
 
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
@@ -1295,7 +1413,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.w = w;
   a.tin = car;
   a.den = den;
-  a.nrm_out = nrm;
+  a.rows_out = nrm;
   a.dbg = trace_for("fwd");
   switch (g.P) {
     case 1: return launch_nt(k_causal_fwd8<1>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);

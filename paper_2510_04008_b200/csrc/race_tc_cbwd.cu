@@ -51,16 +51,16 @@ constexpr uint32_t IDC_DVB = idesc_bf16(128, 128, 0, 1);  // P~^T x dO          
 // ===========================================================================
 namespace cq8 {
 constexpr int OFF_Q = 0;                       // two buffers
-constexpr int OFF_K = 2 * TILE, OFF_V = 3 * TILE;
-constexpr int OFF_DO = 4 * TILE;               // two buffers
-constexpr int OFF_W = 6 * TILE;                // W' (B of the projection; B of dx^ read MN-major)
+constexpr int OFF_V = 2 * TILE;
+constexpr int OFF_DO = 3 * TILE;               // two buffers
+constexpr int OFF_W = 5 * TILE;                // W' (B of the projection; B of dx^ read MN-major)
 constexpr int OFF_SOPT = OFF_W + WOP;
 constexpr int OFF_PHIQ = OFF_SOPT + WOP;       // Phi_q (A of Pm), then phi_q / D (B of dS)
 constexpr int OFF_PHIK = OFF_PHIQ + PHI;       // Phi_k (A of Pm, B of S and Z), then dproj (A of dx^)
 constexpr int OFF_X = OFF_PHIK + PHI;          // [2 parity] x { rs[2][128], nd[2][128], kp[4][8] }, then da[4][8]
 constexpr int XPAR = 256 + 256 + 32;
-constexpr int OFF_TOK = OFF_X + (2 * XPAR + 32) * 4;  // [2] x row norms [256] (TMA)
-constexpr int TOK_BYTES = 256 * 4;
+constexpr int OFF_TOK = OFF_X + (2 * XPAR + 32) * 4;  // [2] x sketch rows [128][ROWW] (TMA)
+constexpr int TOK_BYTES = CH * ROWW * 4;
 constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_q8 shared memory");
@@ -95,7 +95,7 @@ template <int P>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                    const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmNRM, Args a,
+                    const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmROWS, Args a,
                     float* __restrict__ rden, float* __restrict__ gden) {
   using namespace cq8;
   extern __shared__ uint8_t smem_raw[];
@@ -106,10 +106,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* dqstaged = bars + 2;   // [2] dQ staged in the Q buffer (256 arrivals)
   uint64_t* fullO = bars + 4;      // [2]
   uint64_t* emptyO = bars + 6;     // [2] (dS MMA commit)
-  uint64_t* fullT = bars + 8;      // [2] row norms landed
-  uint64_t* emptyT = bars + 10;    // [2] row norms read (256 arrivals)
-  uint64_t* fullK = bars + 12;
-  uint64_t* emptyK = bars + 13;
+  uint64_t* fullT = bars + 8;      // [2] sketch rows landed
+  uint64_t* emptyT = bars + 10;    // [2] sketch rows read (256 arrivals)
   uint64_t* fullV = bars + 14;
   uint64_t* emptyV = bars + 15;
   uint64_t* c1 = bars + 16;        // projection + E + Y
@@ -160,7 +158,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmDO);
       tma_prefetch_desc(&tmDQ);
-      tma_prefetch_desc(&tmNRM);
+      tma_prefetch_desc(&tmROWS);
       const uint64_t pol = policy_evict_first();
       int qt0 = 0, qb0 = 0, qt1 = 0, qb1 = 0;
       auto store_dq = [&](uint32_t j) {
@@ -198,11 +196,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         if (s) { qt1 = t; qb1 = bh; } else { qt0 = t; qb0 = bh; }
         mbar_wait(&emptyT[s], par2);
         mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
-        tma_load_1d(smem + OFF_TOK + s * TOK_BYTES, &tmNRM, &fullT[s], 2 * (bh * int(a.N) + t), pol);
-        mbar_wait(emptyK, par1);
-        RACE_TRACE(a, 0, gc);
-        mbar_arrive_expect_tx(fullK, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
+        tma_load_2d(smem + OFF_TOK + s * TOK_BYTES, &tmROWS, &fullT[s], 0, bh * int(a.N) + t, pol);
         mbar_wait(emptyV, par1);
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
@@ -221,16 +215,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     auto issue_front = [&](uint32_t gc) {
       const int s = gc & 1;
       mbar_wait(&fullQ[s], (gc >> 1) & 1);
-      mbar_wait(fullK, gc & 1);
       RACE_TRACE(a, 4, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = 0; kk < 8; ++kk)
           umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-        }
-        umma_commit(emptyK);
       }
       __syncwarp();
       mbar_wait(fullV, gc & 1);
@@ -369,11 +359,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         float* xpar = xbase + par * XPAR;
         const bool valid = t + r < m.t1;
         mbar_wait(&fullT[s], (gc >> 1) & 1);
-        const float2 sq2 = valid ? *reinterpret_cast<const float2*>(smem + OFF_TOK + s * TOK_BYTES + 8 * r)
-                                 : make_float2(0.f, 0.f);
+        const float* trow = reinterpret_cast<const float*>(smem + OFF_TOK + s * TOK_BYTES) + r * ROWW;
+        float hatk[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) hatk[j] = trow[8 + j];
+        const Scale scq = row_scale(valid ? trow[7] : 0.f, a.normalize);
         mbar_arrive(&emptyT[s]);
-        const Scale scq = row_scale(sq2.x, a.normalize);
-        const Scale sck = row_scale(sq2.y, a.normalize);
         mbar_wait(c1, par);
         if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
         tc_fence_after();
@@ -389,12 +380,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           tc_fence_before();
           mbar_arrive(phi_ready);
         } else {
-          float pk[16], phk[FP], uk[5], hk[5];
-          tmem_ld16(tmem + lb + TM_PK, pk);
+          float phk[FP], uk[5];
           tmem_ld16(tmem + lb + TM_PQ, pq);
           tmem_ld16(tmem + lb + TM_Y, yv);
           tmem_ld_wait();
-          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
+          row_features_hat<P>(a, hatk, valid, phk, uk);  // phi_k from the forward's sketch row
           write_phi_k(sb + OFF_PHIK, r, phk);
           fence_proxy_async();
           tc_fence_before();
@@ -565,20 +555,19 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 // dV goes straight from TMEM to global memory.  Row norms are required.
 // ===========================================================================
 namespace ck8 {
-constexpr int OFF_K = 0;  // two buffers
-constexpr int OFF_Q = 2 * TILE, OFF_V = 3 * TILE, OFF_DO = 4 * TILE;
-constexpr int OFF_W = 5 * TILE;
-constexpr int OFF_W2 = OFF_W + WOP;
-constexpr int OFF_DSOPT = OFF_W2 + W2OP;   // [16 x 128] B of z = V dS_v^T
+constexpr int OFF_K = 0;                   // two buffers (dK staged in place)
+constexpr int OFF_V = 2 * TILE;            // two buffers (dV staged in place once E / z are done)
+constexpr int OFF_DO = 4 * TILE;
+constexpr int OFF_W = 5 * TILE;            // W' (projection; read MN-major as the B of dx^)
+constexpr int OFF_DSOPT = OFF_W + WOP;     // [16 x 128] B of z = V dS_v^T
 constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // [128 x 32] B of dV_a = Phi_k dS_v
-constexpr int OFF_PHIQ = OFF_DSOP + PHI;   // [hi|hi|lo|0]  B of Pm^T (K) and of Z (MN)
+constexpr int OFF_PHIQ = OFF_DSOP + PHI;   // [hi|hi|lo|0]  B of Pm^T (K) and of Z (MN); then dproj (A of dx^)
 constexpr int OFF_PHIK = OFF_PHIQ + PHI;   // [hi|lo|hi|0]  A of Pm^T and dV_a
 constexpr int OFF_PHIT = OFF_PHIK + PHI;   // phi_q / D     B of dS (MN)
-constexpr int OFF_DPROJ = OFF_PHIT + PHI;
-constexpr int OFF_X = OFF_DPROJ + PHI;     // [2 parity] x { rd[128], gd[128], dac[4][8] }
+constexpr int OFF_X = OFF_PHIT + PHI;      // [2 parity] x { unused[256], dac[4][8] }
 constexpr int XPAR = 256 + 32;
-constexpr int OFF_TOK = OFF_X + 2 * XPAR * 4;  // [2 parity] x { rden[128], gden[128], rownorms[256] } (TMA)
-constexpr int TOK_BYTES = 512 * 4;
+constexpr int OFF_TOK = OFF_X + 2 * XPAR * 4;  // [2 parity] x { rden[128], gden[128], sketch rows[128][ROWW] } (TMA)
+constexpr int TOK_BYTES = (256 + CH * ROWW) * 4;
 constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 512 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_k8 shared memory");
@@ -613,10 +602,10 @@ struct RCursor {
 
 template <int P>
 __global__ void __launch_bounds__(NTHREADS8, 1)
-    k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmRD,
-                    const __grid_constant__ CUtensorMap tmGD, const __grid_constant__ CUtensorMap tmNRM,
+                    const __grid_constant__ CUtensorMap tmGD, const __grid_constant__ CUtensorMap tmROWS,
                     const __grid_constant__ CUtensorMap tmDV, Args a) {
   using namespace ck8;
   extern __shared__ uint8_t smem_raw[];
@@ -625,11 +614,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* fullK = bars + 0;     // [2]
   uint64_t* dkstaged = bars + 2;  // [2]
-  uint64_t* fullQ = bars + 4;
-  uint64_t* fullV = bars + 5;
+  uint64_t* fullV = bars + 4;     // [2]
   uint64_t* fullO = bars + 6;
-  uint64_t* emptyQ = bars + 7;
-  uint64_t* emptyV = bars + 8;
   uint64_t* emptyO = bars + 9;
   uint64_t* projf = bars + 10;
   uint64_t* c1 = bars + 11;
@@ -645,8 +631,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* cdv = bars + 21;       // dV MMAs done
   uint64_t* fullT = bars + 22;     // [2] per-token inputs landed (parity buffers)
   uint64_t* emptyT = bars + 24;    // [2] ... consumed (256 arrivals)
-  uint64_t* dvstaged = bars + 26;  // dV staged in the (consumed) V tile (256 arrivals)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 27);
+  uint64_t* dvstaged = bars + 26;  // [2] dV staged in the (consumed) V buffer (256 arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 28);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
@@ -666,7 +652,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_init(&fullT[i], 1);
       mbar_init(&emptyT[i], 256);
     }
-    mbar_init(dvstaged, 256);
+    mbar_init(&dvstaged[0], 256);
+    mbar_init(&dvstaged[1], 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -680,18 +667,24 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmDO);
       tma_prefetch_desc(&tmDK);
       tma_prefetch_desc(&tmRD);
       tma_prefetch_desc(&tmGD);
-      tma_prefetch_desc(&tmNRM);
+      tma_prefetch_desc(&tmROWS);
       tma_prefetch_desc(&tmDV);
       const uint64_t pol = policy_evict_first();
       int kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
-      int vt = 0, vb = 0;  // coordinates of the dV tile held by the V buffer
+      int vt[2] = {0, 0}, vb[2] = {0, 0};  // coordinates of the dV tile held by each V buffer
+      auto store_dv = [&](uint32_t j) {
+        const int s = j & 1;
+        mbar_wait(&dvstaged[s], (j >> 1) & 1);
+        for (int h = 0; h < 2; ++h)
+          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + s * TILE + h * SUB), h * 64, vt[s], vb[s]);
+        tma_store_commit();
+      };
       auto store_dk = [&](uint32_t j) {
         const int s = j & 1;
         mbar_wait(&dkstaged[s], (j >> 1) & 1);
@@ -707,7 +700,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           const int tp = int(cur.t) - a.pf * CH;
           if (tp >= 0)
             for (int h = 0; h < 2; ++h) {
-              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
               tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
               tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
               tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
@@ -724,10 +716,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&fullK[s], TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + s * TILE + h * SUB, &tmK, &fullK[s], h * 64, t, bh, pol);
         if (s) { kt1 = t; kb1 = bh; } else { kt0 = t; kb0 = bh; }
-        mbar_wait(emptyQ, par);
-        RACE_TRACE(a, 0, gc);
-        mbar_arrive_expect_tx(fullQ, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + h * SUB, &tmQ, fullQ, h * 64, t, bh, pol);
         {  // per-token rden, gden, row norms of this chunk (parity buffer s)
           uint8_t* tok = smem + OFF_TOK + s * TOK_BYTES;
           const int row = bh * int(a.N) + t;
@@ -735,31 +723,24 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
           tma_load_1d(tok, &tmRD, &fullT[s], row, pol);
           tma_load_1d(tok + 512, &tmGD, &fullT[s], row, pol);
-          tma_load_1d(tok + 1024, &tmNRM, &fullT[s], 2 * row, pol);
+          tma_load_2d(tok + 1024, &tmROWS, &fullT[s], 0, row, pol);
         }
-        if (gc >= 1) {  // dV of the previous chunk is staged in the V tile: store it, then refill
-          mbar_wait(dvstaged, (gc - 1) & 1);
-          for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + h * SUB), h * 64, vt, vb);
-          tma_store_commit();
+        if (gc >= 2) {  // dV of chunk gc - 2 is staged in this V buffer: store it, then refill
+          store_dv(gc - 2);
           tma_store_wait_read<0>();
         }
-        vt = t;
-        vb = bh;
+        vt[s] = t;
+        vb[s] = bh;
         RACE_TRACE(a, 1, gc);
-        mbar_arrive_expect_tx(fullV, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
+        mbar_arrive_expect_tx(&fullV[s], TILE);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(smem + OFF_V + s * TILE + h * SUB, &tmV, &fullV[s], h * 64, t, bh, pol);
         mbar_wait(emptyO, par);
         RACE_TRACE(a, 2, gc);
         mbar_arrive_expect_tx(fullO, TILE);
         for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
       }
-      if (gc >= 1) {
-        mbar_wait(dvstaged, (gc - 1) & 1);
-        for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + h * SUB), h * 64, vt, vb);
-        tma_store_commit();
-      }
+      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dv(j);
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dk(j);
       tma_store_wait_all<0>();
     }
@@ -776,30 +757,26 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         ++nr;
         tc_fence_after();
       }
-      mbar_wait(fullQ, par);
       mbar_wait(&fullK[s], (gc >> 1) & 1);
       RACE_TRACE(a, 4, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        for (int kk = 0; kk < 8; ++kk)
           umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-        }
         umma_commit(projf);
-        umma_commit(emptyQ);
       }
       __syncwarp();
       if (gc > 0) mbar_wait(dxfree, (gc - 1) & 1);  // E aliases the previous chunk's dX
-      mbar_wait(fullV, par);
+      mbar_wait(&fullV[s], (gc >> 1) & 1);
       mbar_wait(fullO, par);
       RACE_TRACE(a, 5, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16(tmem + TM_ZV, desc_tile_k(sb + OFF_V, kk), desc_w(sb + OFF_DSOPT, kk), IDC_Y, kk > 0);
-          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
+          umma_bf16(tmem + TM_ZV, desc_tile_k(sb + OFF_V + s * TILE, kk), desc_w(sb + OFF_DSOPT, kk), IDC_Y, kk > 0);
+          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V + s * TILE, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
         }
         umma_commit(c1);
       }
@@ -849,8 +826,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-          umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), IDC_DX, kk > 0);
+        // dx^ = dproj . W (hi and lo halves of dproj against W' read MN-major)
+        umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIQ, 0), cq8::desc_wT(sb + OFF_W), IDC_DX, 0u);
+        umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIQ, 1), cq8::desc_wT(sb + OFF_W), IDC_DX, 1u);
         umma_commit(c4);
       }
       __syncwarp();
@@ -897,7 +875,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           dA[f] = f < F ? dcar[f * LDS_T + DH] : 0.f;
         }
         build_wop<256, CT0>(a, m.bh, sb + OFF_W);
-        build_w2<256, CT0>(a, m.bh, sb + OFF_W2);
         if (h == 1) {
           float z[16];
 #pragma unroll
@@ -918,20 +895,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const float* tok = reinterpret_cast<const float*>(smem + OFF_TOK + (gc & 1) * TOK_BYTES);
       mbar_wait(&fullT[gc & 1], (gc >> 1) & 1);
       const float rdr_c = valid ? tok[r] : 0.f, gdr_c = valid ? tok[128 + r] : 0.f;
-      const float2 sq2 = valid ? *reinterpret_cast<const float2*>(tok + 256 + 2 * r) : make_float2(0.f, 0.f);
-      const Scale scq = row_scale(sq2.x, a.normalize);
-      const Scale sck = row_scale(sq2.y, a.normalize);
+      const float* trow = tok + 256 + r * ROWW;  // this token's sketch row
+      float hatq[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) hatq[j] = trow[j];
+      const Scale sck = row_scale(valid ? trow[15] : 0.f, a.normalize);
       mbar_wait(projf, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
       tc_fence_after();
-      float phq[FP], uq[5], hq[5], phk[FP], uk[5], hk[5];
+      float phq[FP], uq[5], phk[FP], uk[5], hk[5];
       {
-        float pq[16], pk[16];
-        tmem_ld16(tmem + lb + TM_PQ, pq);
+        float pk[16];
         tmem_ld16(tmem + lb + TM_PK, pk);
         tmem_ld_wait();
         if (h == 0) {
-          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+          row_features_hat<P>(a, hatq, valid, phq, uq);  // phi_q from the forward's sketch row
           write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
         } else {
           row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
@@ -1035,7 +1013,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       float dproj[8];
       row_feature_vjp<P>(a, uk, phk, dphi, dproj);
       const float dotk = dot_from_proj(dproj, hk);
-      if (h == 1) write_dproj(sb + OFF_DPROJ, r, dproj);
+      if (h == 1) cq8::write_dproj_w(sb + OFF_PHIQ, r, dproj, a.TP);  // Phi_q is dead after Pm, Z (c3)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dp_ready);
@@ -1062,11 +1040,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         float v[32];
         tmem_ld32(tmem + lb + TM_DV + c0, v);
         tmem_ld_wait();
-        stage32_p(smem + OFF_V, r, v, c0);
+        stage32_p(smem + OFF_V + s * TILE, r, v, c0);
       }
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(dvstaged);
+      mbar_arrive(&dvstaged[s]);
       cur.next(a);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
@@ -1101,15 +1079,15 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.w = w;
   a.tin = car;
   a.tout = dpart;
-  a.nrm_in = nrm;
+  a.rows_in = nrm;
   a.dbg = trace_for("bq");
   if (!nrm) return cudaErrorInvalidValue;  // race_abi.cu always supplies the forward's rows
-  CUtensorMap mnrm;
-  if (!make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256)) return cudaErrorInvalidValue;
+  CUtensorMap mrows;
+  if (!make_map_rows(&mrows, nrm, g.BH * g.N)) return cudaErrorInvalidValue;
   switch (g.P) {
-    case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
-    case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
-    default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mnrm, a, rden, gden);
+    case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
+    case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
+    default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
   }
 }
 
@@ -1124,18 +1102,18 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   Args a = make_args(g);
   a.w = w;
   a.tin = dcar;
-  a.nrm_in = nrm;
+  a.rows_in = nrm;
   a.dbg = trace_for("bk");
   if (!nrm) return cudaErrorInvalidValue;
-  CUtensorMap mrd, mgd, mnrm, mdv2;
+  CUtensorMap mrd, mgd, mrows, mdv2;
   if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
   if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
-      !make_map_f32_1d(&mnrm, nrm, 2 * g.BH * g.N, 256))
+      !make_map_rows(&mrows, nrm, g.BH * g.N))
     return cudaErrorInvalidValue;
   switch (g.P) {
-    case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
-    case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
-    default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdk, mrd, mgd, mnrm, mdv2, a);
+    case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
+    case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
+    default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
   }
 }
 

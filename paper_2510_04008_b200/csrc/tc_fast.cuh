@@ -28,6 +28,11 @@ constexpr int NTHREADS = 192;
 constexpr int NTHREADS8 = 320;      // 8-compute-warp kernels: warp 0 TMA, warp 1 MMA, 2..9 compute
 constexpr int CT0 = 64;              // first compute thread of the 8-compute-warp kernels
 constexpr int FP = 8;                // padded feature count
+// Sketch rows (causal forward state, one per token): floats [0, 8) describe q, [8, 16) k:
+// slot j < T*P holds x^.w_j = (x . w_j) / ||x|| exactly as the kernels compute it, slot 7
+// holds ||x||^2.  The backward rebuilds phi and the tanh values from them instead of
+// re-reading and re-projecting the other operand's tiles.
+constexpr int ROWW = 16;
 
 constexpr int LDS_T = DH + 1;        // table row stride (dv + 1)
 
@@ -44,8 +49,8 @@ struct Args {
   const float* tin;   // tables / carries
   float* tout;        // partial tables
   float* den;
-  const float* nrm_in;  // [BH, N, 2] row sums of squares (q, k) saved by the causal forward, or null
-  float* nrm_out;
+  const float* rows_in;  // [BH, N, ROWW] sketch rows saved by the causal forward (see ROWW)
+  float* rows_out;
   int pf;               // chunks of L2 prefetch (cp.async.bulk.prefetch) ahead of the TMA loads
 };
 
@@ -254,6 +259,51 @@ __device__ __forceinline__ void row_features(const Args& a, const float* proj, f
         const float u = fast_tanh((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv);
         e[p] = fast_exp_neg(2.f * a.beta * fabsf(u));
         neg[p] = u < 0.f;
+        z *= 1.f + e[p];
+      }
+      const float rz = 1.f / z;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float prod = rz;
+#pragma unroll
+        for (int p = 0; p < P; ++p) prod *= (((rr >> p) & 1) == int(neg[p])) ? 1.f : e[p];
+        phi[tau * R + rr] = prod;
+      }
+    }
+  }
+}
+
+// projections of one row as stored in the sketch rows: hat[j] = (x . w_j) / ||x||
+__device__ __forceinline__ void row_hat(const Args& a, const float* proj, float inv, float* hat) {
+#pragma unroll
+  for (int j = 0; j < 5; ++j) hat[j] = j < a.TP ? (proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv : 0.f;
+}
+// store the 8-float half of a sketch row (hat[0..5), 0, 0, ||x||^2)
+__device__ __forceinline__ void store_row_half(float* dst, const float* hat, float sumsq) {
+  reinterpret_cast<float4*>(dst)[0] = make_float4(hat[0], hat[1], hat[2], hat[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(hat[4], 0.f, 0.f, sumsq);
+}
+// features from stored projections hat (same arithmetic as row_features[_u])
+template <int P>
+__device__ __forceinline__ void row_features_hat(const Args& a, const float* hat, bool valid, float* phi, float* u) {
+  constexpr int R = 1 << P;
+  constexpr int TMAX = FP / R;
+#pragma unroll
+  for (int f = 0; f < FP; ++f) phi[f] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) u[j] = 0.f;
+#pragma unroll
+  for (int tau = 0; tau < TMAX; ++tau) {
+    if (tau < a.T && valid) {
+      float e[P], z = 1.f;
+      bool neg[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int j = tau * P + p;
+        const float uu = fast_tanh(hat[j < 5 ? j : 0]);
+        u[j < 5 ? j : 0] = uu;
+        e[p] = fast_exp_neg(2.f * a.beta * fabsf(uu));
+        neg[p] = uu < 0.f;
         z *= 1.f + e[p];
       }
       const float rz = 1.f / z;
@@ -881,6 +931,20 @@ inline bool make_map_f32_1d(CUtensorMap* m, const void* ptr, int64_t elems, int 
   cuuint32_t bx[1] = {cuuint32_t(box)};
   cuuint32_t es[1] = {1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(ptr), dims, strides, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// sketch rows [rows, ROWW] fp32 (race_b200.h), box of 128 rows (OOB rows read as zero)
+inline bool make_map_rows(CUtensorMap* m, const void* ptr, int64_t rows) {
+  auto fn = encode_fn();
+  if (!fn || rows <= 0 || rows >= (int64_t(1) << 32)) return false;
+  cuuint64_t dims[2] = {cuuint64_t(ROWW), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ROWW) * 4};
+  cuuint32_t bx[2] = {cuuint32_t(ROWW), cuuint32_t(CH)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, bx, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;

@@ -116,17 +116,18 @@ class Problem:
 
     def state_shape(self) -> tuple[int, ...]:
         """Non-causal: the global tables [BH, F, dv+1].  Causal: a flat buffer holding the
-        per-segment carries [BH, nseg, F, dv+1] then the q/k row norms [BH, N, 2]."""
+        per-segment carries [BH, nseg, F, dv+1] then the q/k sketch rows [BH, N, 16]
+        (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h)."""
         f = self.p.tables << self.p.hyperplanes
         if self.p.causal:
-            return (self.bh * self.nseg * f * (self.dv + 1) + 2 * self.bh * self.n,)
+            return (self.bh * self.nseg * f * (self.dv + 1) + 16 * self.bh * self.n,)
         return (self.bh, f, self.dv + 1)
 
     def split_causal_state(self, state: torch.Tensor):
-        """(carries [BH, nseg, F, dv+1], rownorms [BH, N, 2]) views of a causal state buffer."""
+        """(carries [BH, nseg, F, dv+1], sketch rows [BH, N, 16]) views of a causal state buffer."""
         nc = self.bh * self.nseg * self.table_elems
         return (state[:nc].view(self.bh, self.nseg, self.table_elems),
-                state[nc:].view(self.bh, max(self.n, 0), 2))
+                state[nc:].view(self.bh, max(self.n, 0), 16))
 
 
 def _c(t: torch.Tensor) -> torch.Tensor:

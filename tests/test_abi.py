@@ -44,7 +44,7 @@ def test_segmentation_and_sizes():
     d = _desc()
     nseg, seg = _lib.segments(d)
     assert seg % 128 == 0 and nseg * seg >= 131072 > (nseg - 1) * seg
-    assert _lib.state_elems(d) == 4 * nseg * 8 * 129 + 2 * 4 * 131072
+    assert _lib.state_elems(d) == 4 * nseg * 8 * 129 + 16 * 4 * 131072  # carries + sketch rows
     assert _lib.state_elems(_desc(causal=False)) == 4 * 8 * 129
     assert _lib.workspace_bytes(d) >= 4 * 4 * nseg * 8 * 129
     assert _lib.segments(_desc(n=1)) == (1, 128)
