@@ -297,12 +297,16 @@ def gpt_train_step(dev, steps=5, warmup=3):
 # ---------------------------------------------------------------------------
 # algorithmic bytes per token-head of each kernel (e = element bytes)
 def kernel_bytes(e, causal):
+    """Algorithmic bytes per token-head of each launched kernel (what it must read and write;
+    DESIGN.md section 4).  Causal: the forward also saves the 64-byte sketch row per token,
+    which lets each backward pass skip one of the four N x d operands."""
     d = dv = DIM
+    rows = 64  # sketch row: 16 fp32 (q and k projections + norms)
     if causal:
-        return {"kside_partials": (d + dv) * e,                          # read K, V
-                "fwd_causal": (2 * d + dv) * e + dv * e + 4,            # read Q, K, V; write O, den
-                "bwd_causal_q": (2 * d + 2 * dv) * e + d * e + 8,       # read Q, K, V, dO; write dQ, rden, gden
-                "bwd_causal_k": (2 * d + 2 * dv) * e + 8 + (d + dv) * e}  # read Q, K, V, dO, rden, gden; write dK, dV
+        return {"kside_partials": (d + dv) * e,                              # read K, V
+                "fwd_causal": (2 * d + dv) * e + dv * e + 4 + rows,         # read Q, K, V; write O, den, rows
+                "bwd_causal_q": (d + 2 * dv) * e + rows + d * e + 8,        # read Q, V, dO, rows; write dQ, rden, gden
+                "bwd_causal_k": (d + 2 * dv) * e + rows + 8 + (d + dv) * e}  # read K, V, dO, rows, rden, gden; write dK, dV
     return {"kside_partials": (d + dv) * e, "fwd_readout": d * e + dv * e + 4,
             "bwd_qside": (d + dv) * e + d * e, "bwd_kside": 2 * (d + dv) * e}
 
