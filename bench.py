@@ -409,7 +409,7 @@ def run_ours(args, world, rank, local_rank):
     o = torch.empty_like(v)
     den = torch.empty((1, HEADS, n), device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    rden = torch.empty((pr.bh, n), device=dev)
+    rden = torch.empty((pr.bh, (n + 3) // 4 * 4), device=dev)  # row pitch N rounded up to 4 (race_b200.h)
     gden = torch.empty_like(rden)
     norms = torch.empty((pr.bh, n, 16), device=dev)  # sketch rows
     S = _stream()

@@ -160,7 +160,8 @@ int race_bwd_kside(const race_desc_t* desc, const void* k, const void* v,
                    void* workspace, void* stream);
 
 /* Causal backward, forward-direction scan: dq, per-token normaliser terms
- * rden = 1/(T*den), gden = -(dO.O)/(T*den), and per-segment dS totals
+ * rden = 1/(T*den), gden = -(dO.O)/(T*den) ([BH, Np] float32, row pitch
+ * Np = N rounded up to a multiple of 4), and per-segment dS totals
  * (ra/backward.py:142-168).  rownorms (may be NULL = recompute into the
  * workspace) is what race_fwd_causal wrote (sketch rows).                 */
 int race_bwd_causal_q(const race_desc_t* desc, const void* q, const void* k,

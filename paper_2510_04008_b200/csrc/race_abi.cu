@@ -125,6 +125,7 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
   const int64_t E = table_elems(g);
   const int64_t segE = g.BH * g.nseg * E;
   const int64_t tok = g.BH * (g.N > 0 ? g.N : 1);
+  const int64_t ptok = g.BH * (g.N > 0 ? (g.N + 3) & ~int64_t(3) : 4);  // rden / gden rows padded to 16 bytes
   auto al = [](int64_t n) { return (n + 63) & ~int64_t(63); };
   WsLayout w{};
   char* p = static_cast<char*>(base);
@@ -134,8 +135,8 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
   w.tables = take(segE);
   w.dpart = take(segE);
   w.dtables = take(segE);
-  w.rden = take(tok);
-  w.gden = take(tok);
+  w.rden = take(ptok);
+  w.gden = take(ptok);
   w.rows = take(16 * tok);
   w.bytes = off;
   return w;

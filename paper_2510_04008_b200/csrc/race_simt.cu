@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restric
       rowv[kRD * TILE + r] = rD;
       rowv[kRho * TILE + r] = rho;
       if (r < rows) {
-        rden[bh * g.N + t0 + r] = rD;
-        gden[bh * g.N + t0 + r] = -rho * rD;
+        rden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] = rD;  // row pitch N rounded up to 4 (race_b200.h)
+        gden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] = -rho * rD;
       }
     }
     __syncthreads();
@@ -624,8 +624,8 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restric
     load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
     load_rows<Tin>(d_o + (bh * g.N + t0) * g.dv, rows, g.dv, gs, pl.ldv, nullptr, false);
     for (int r = threadIdx.x; r < TILE; r += NT) {
-      rowv[kRD * TILE + r] = r < rows ? rden[bh * g.N + t0 + r] : 0.f;
-      rowv[kGD * TILE + r] = r < rows ? gden[bh * g.N + t0 + r] : 0.f;
+      rowv[kRD * TILE + r] = r < rows ? rden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] : 0.f;
+      rowv[kGD * TILE + r] = r < rows ? gden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] : 0.f;
     }
     __syncthreads();
     tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);

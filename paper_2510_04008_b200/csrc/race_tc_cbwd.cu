@@ -477,8 +477,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(et_ready);
         if (h == 0 && valid) {
-          rden[m.bh * a.N + t + r] = rD;
-          gden[m.bh * a.N + t + r] = -rho * rD;
+          rden[m.bh * a.Np + t + r] = rD;  // row pitch Np (multiple of 4: 16-byte TMA tiles)
+          gden[m.bh * a.Np + t + r] = -rho * rD;
         }
         // ---- dphi_q -> dproj
         mbar_wait(c3, par);
@@ -719,10 +719,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         {  // per-token rden, gden, row norms of this chunk (parity buffer s)
           uint8_t* tok = smem + OFF_TOK + s * TOK_BYTES;
           const int row = bh * int(a.N) + t;
+          const int prow = bh * int(a.Np) + t;  // rden / gden: row pitch Np keeps every tile 16-byte aligned
           mbar_wait(&emptyT[s], ((gc >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
-          tma_load_1d(tok, &tmRD, &fullT[s], row, pol);
-          tma_load_1d(tok + 512, &tmGD, &fullT[s], row, pol);
+          tma_load_1d(tok, &tmRD, &fullT[s], prow, pol);
+          tma_load_1d(tok + 512, &tmGD, &fullT[s], prow, pol);
           tma_load_2d(tok + 1024, &tmROWS, &fullT[s], 0, row, pol);
         }
         if (gc >= 2) {  // dV of chunk gc - 2 is staged in this V buffer: store it, then refill
@@ -1107,7 +1108,8 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   if (!nrm) return cudaErrorInvalidValue;
   CUtensorMap mrd, mgd, mrows, mdv2;
   if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
-  if (!make_map_f32_1d(&mrd, rden, g.BH * g.N, 128) || !make_map_f32_1d(&mgd, gden, g.BH * g.N, 128) ||
+  const int64_t np = (g.N + 3) & ~int64_t(3);
+  if (!make_map_f32_1d(&mrd, rden, g.BH * np, 128) || !make_map_f32_1d(&mgd, gden, g.BH * np, 128) ||
       !make_map_rows(&mrows, nrm, g.BH * g.N))
     return cudaErrorInvalidValue;
   switch (g.P) {

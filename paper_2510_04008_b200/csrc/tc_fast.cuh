@@ -42,6 +42,7 @@ constexpr uint32_t TM_PROJQ = 0, TM_PROJK = 16, TM_SACC = 32, TM_PM = 64, TM_NUM
 struct Args {
   unsigned* dbg;  // optional host-mapped progress words (RACE_DEBUG_PROGRESS=1), [grid][256]
   int64_t BH, H, N, nseg, seg_tokens;
+  int64_t Np;  // row pitch of the per-token rden / gden arrays: N rounded up to a multiple of 4
   int P, T, TP;
   float beta;
   int normalize, w_per_head;
@@ -963,6 +964,7 @@ inline Args make_args(const Geo& g) {
   a.BH = g.BH;
   a.H = g.H;
   a.N = g.N;
+  a.Np = (g.N + 3) & ~int64_t(3);
   a.nseg = g.nseg;
   a.seg_tokens = g.seg_tokens;
   a.P = g.P;

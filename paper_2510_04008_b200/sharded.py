@@ -130,7 +130,7 @@ def sharded_backward(q, k, v, w, d_o, p: SketchParams, state, group=None, comm=N
             _lib.check(L.race_bwd_kside(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(dtables), _vp(dk), _vp(dv),
                                         _vp(ws), _stream()), "race_bwd_kside")
         return dq, dk, dv
-    rden = torch.empty((pr.bh, max(pr.n, 1)), dtype=torch.float32, device=dev)
+    rden = torch.empty((pr.bh, max((pr.n + 3) // 4 * 4, 4)), dtype=torch.float32, device=dev)  # row pitch: N up to x4
     gden = torch.empty_like(rden)
     carries, norms = pr.split_causal_state(state)
     if pr.n:

@@ -3,7 +3,9 @@ sys.path.insert(0, os.getcwd())
 import torch
 import paper_2510_04008_b200 as rb
 dev = torch.device("cuda", 0)
-for (H, n) in [(1, 130), (1, 128), (1, 256), (1, 1000), (4, 4096), (4, 131072)]:
+sizes = [int(x) for x in sys.argv[1:]] or [130, 1000, 16666, 16667, 131072]
+for n in sizes:
+    H = 4
     cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=0, causal=True)
     w = rb.head_hyperplanes(cfg, H, 128).to(dev)
     p = cfg.params()
@@ -12,10 +14,10 @@ for (H, n) in [(1, 130), (1, 128), (1, 256), (1, 1000), (4, 4096), (4, 131072)]:
     try:
         o, den, st = rb.race_forward(q, k, v, w, p)
         torch.cuda.synchronize()
-        print("fwd ok", H, n, flush=True)
+        print("fwd ok", n, flush=True)
         dq, dk, dv = rb.race_backward(q, k, v, w, do, p, state=st)
         torch.cuda.synchronize()
-        print("bwd ok", H, n, flush=True)
+        print("ok", n, flush=True)
     except Exception as e:
-        print("FAIL", H, n, e, flush=True)
+        print("FAIL", n, str(e)[:200], flush=True)
         break
