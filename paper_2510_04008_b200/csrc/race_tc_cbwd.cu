@@ -211,18 +211,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_store_wait_all<0>();
     }
   } else if (warp == 1) {
-    // projection + E / Y of chunk `gc` (issued one step ahead of its use)
+    // E / Y of chunk `gc` (issued one step ahead of its use; the q projections come from the
+    // forward's sketch rows, so there is no projection MMA here)
     auto issue_front = [&](uint32_t gc) {
       const int s = gc & 1;
-      mbar_wait(&fullQ[s], (gc >> 1) & 1);
-      RACE_TRACE(a, 4, gc);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_PQ, desc_tile_k(sb + OFF_Q + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-      }
-      __syncwarp();
       mbar_wait(fullV, gc & 1);
       mbar_wait(&fullO[s], (gc >> 1) & 1);
       RACE_TRACE(a, 5, gc);
@@ -360,31 +352,25 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const bool valid = t + r < m.t1;
         mbar_wait(&fullT[s], (gc >> 1) & 1);
         const float* trow = reinterpret_cast<const float*>(smem + OFF_TOK + s * TOK_BYTES) + r * ROWW;
-        float hatk[5];
+        float hq[5], hatk[5];  // x^.w_j of this q row and of this k row (the forward's sketch row)
 #pragma unroll
-        for (int j = 0; j < 5; ++j) hatk[j] = trow[8 + j];
+        for (int j = 0; j < 5; ++j) {
+          hq[j] = trow[j];
+          hatk[j] = trow[8 + j];
+        }
         const Scale scq = row_scale(valid ? trow[7] : 0.f, a.normalize);
         mbar_arrive(&emptyT[s]);
-        mbar_wait(c1, par);
         if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
-        tc_fence_after();
-        float pq[16], yv[16];
-        float phq[FP], uq[5], hq[5];
+        float phq[FP], uq[5];
         if (h == 0) {
-          tmem_ld16(tmem + lb + TM_PQ, pq);
-          tmem_ld16(tmem + lb + TM_Y, yv);
-          tmem_ld_wait();
-          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+          row_features_hat<P>(a, hq, valid, phq, uq);
           write_phi_q(sb + OFF_PHIQ, r, phq);
           fence_proxy_async();
           tc_fence_before();
           mbar_arrive(phi_ready);
         } else {
           float phk[FP], uk[5];
-          tmem_ld16(tmem + lb + TM_PQ, pq);
-          tmem_ld16(tmem + lb + TM_Y, yv);
-          tmem_ld_wait();
-          row_features_hat<P>(a, hatk, valid, phk, uk);  // phi_k from the forward's sketch row
+          row_features_hat<P>(a, hatk, valid, phk, uk);
           write_phi_k(sb + OFF_PHIK, r, phk);
           fence_proxy_async();
           tc_fence_before();
@@ -398,8 +384,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
           }
-          row_features_u<P>(a, pq, scq.inv, valid, phq, uq, hq);
+          row_features_hat<P>(a, hq, valid, phq, uq);
         }
+        float yv[16];
+        mbar_wait(c1, par);
+        tc_fence_after();
+        tmem_ld16(tmem + lb + TM_Y, yv);
+        tmem_ld_wait();
         float y[FP], Dint = 0.f, ydot = 0.f;
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
@@ -504,6 +495,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(c4, par);
         if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
         tc_fence_after();
+        mbar_wait(&fullQ[s], (gc >> 1) & 1);  // q itself is only read here (x^ of the tangent step)
         tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
         fence_proxy_async();
         tc_fence_before();
@@ -758,16 +750,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         ++nr;
         tc_fence_after();
       }
-      mbar_wait(&fullK[s], (gc >> 1) & 1);
-      RACE_TRACE(a, 4, gc);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_PK, desc_tile_k(sb + OFF_K + s * TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-        umma_commit(projf);
-      }
-      __syncwarp();
+      // (no projection MMA: phi_q, phi_k and the tanh values come from the forward's sketch rows;
+      // the K tile is only needed for the sphere-tangent step and as dK staging)
       if (gc > 0) mbar_wait(dxfree, (gc - 1) & 1);  // E aliases the previous chunk's dX
       mbar_wait(&fullV[s], (gc >> 1) & 1);
       mbar_wait(fullO, par);
@@ -897,23 +881,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(&fullT[gc & 1], (gc >> 1) & 1);
       const float rdr_c = valid ? tok[r] : 0.f, gdr_c = valid ? tok[128 + r] : 0.f;
       const float* trow = tok + 256 + r * ROWW;  // this token's sketch row
-      float hatq[5];
+      float hatq[5], hk[5];  // x^.w_j of this q row and this k row
 #pragma unroll
-      for (int j = 0; j < 5; ++j) hatq[j] = trow[j];
+      for (int j = 0; j < 5; ++j) {
+        hatq[j] = trow[j];
+        hk[j] = trow[8 + j];
+      }
       const Scale sck = row_scale(valid ? trow[15] : 0.f, a.normalize);
-      mbar_wait(projf, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
-      tc_fence_after();
-      float phq[FP], uq[5], phk[FP], uk[5], hk[5];
+      float phq[FP], uq[5], phk[FP], uk[5];
       {
-        float pk[16];
-        tmem_ld16(tmem + lb + TM_PK, pk);
-        tmem_ld_wait();
         if (h == 0) {
-          row_features_hat<P>(a, hatq, valid, phq, uq);  // phi_q from the forward's sketch row
+          row_features_hat<P>(a, hatq, valid, phq, uq);
           write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
         } else {
-          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);
+          row_features_hat<P>(a, hk, valid, phk, uk);
           write_phi_q(sb + OFF_PHIK, r, phk);  // [hi|lo|hi|0]
         }
         fence_proxy_async();
@@ -936,7 +918,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xpar[256 + qw * FP + f] = dac[f];
           }
-          row_features_u<P>(a, pk, sck.inv, valid, phk, uk, hk);  // for dk (off the MMA path)
+          row_features_hat<P>(a, hk, valid, phk, uk);  // for dk (off the MMA path)
         }
       }
       if (threadIdx.x == CT0) RACE_TRACE(a, 24, gc);
@@ -1051,6 +1033,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(c4, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
       tc_fence_after();
+      mbar_wait(&fullK[s], (gc >> 1) & 1);  // k itself is only read here (x^ of the tangent step)
       tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
       fence_proxy_async();
       tc_fence_before();
