@@ -303,8 +303,8 @@ def kernel_bytes(e, causal):
     d = dv = DIM
     rows = 64  # sketch row: 16 fp32 (q and k projections + norms)
     if causal:
-        return {"kside_partials": (d + dv) * e,                              # read K, V
-                "fwd_causal": (2 * d + dv) * e + dv * e + 4 + rows,         # read Q, K, V; write O, den, rows
+        return {"kside_partials": (d + dv) * e + rows // 2,                 # read K, V; write k half rows
+                "fwd_causal": (d + dv) * e + rows + dv * e + 4 + rows // 2,  # read Q, V, rows; write O, den, q half
                 "bwd_causal_q": (d + 2 * dv) * e + rows + d * e + 8,        # read Q, V, dO, rows; write dQ, rden, gden
                 "bwd_causal_k": (d + 2 * dv) * e + rows + 8 + (d + dv) * e}  # read K, V, dO, rows, rden, gden; write dK, dV
     return {"kside_partials": (d + dv) * e, "fwd_readout": d * e + dv * e + 4,
@@ -416,9 +416,10 @@ def run_ours(args, world, rank, local_rank):
     ptr = _vp
     if causal:
         calls = [
-            ("kside_partials", lambda: L.race_kside_partials(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(part), ptr(ws), S)),
+            ("kside_partials", lambda: L.race_kside_partials_rows(pr.dref, ptr(k), ptr(v), ptr(pr.w), ptr(part),
+                                                                  ptr(norms), ptr(ws), S)),
             ("combine", lambda: L.race_combine(pr.dref, 1, ptr(part), None, ptr(tabs), S)),
-            ("fwd_causal", lambda: L.race_fwd_causal(pr.dref, ptr(q), ptr(k), ptr(v), ptr(pr.w), ptr(tabs), ptr(o),
+            ("fwd_causal", lambda: L.race_fwd_causal_krows(pr.dref, ptr(q), ptr(k), ptr(v), ptr(pr.w), ptr(tabs), ptr(o),
                                                      ptr(den), ptr(norms), ptr(ws), S)),
             ("bwd_causal_q", lambda: L.race_bwd_causal_q(pr.dref, ptr(q), ptr(k), ptr(v), ptr(g), ptr(pr.w), ptr(tabs),
                                                          ptr(norms), ptr(dq), ptr(rden), ptr(gden), ptr(dpart),

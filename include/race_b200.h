@@ -128,6 +128,13 @@ int race_kside_partials(const race_desc_t* desc, const void* k, const void* v,
                         const float* w, float* part, void* workspace,
                         void* stream);
 
+/* race_kside_partials that also writes the k halves (floats 8..15) of the
+ * causal sketch rows [BH, N, 16] into rownorms, for race_fwd_causal_krows.
+ * Non-causal descs and the generic path leave rownorms untouched.         */
+int race_kside_partials_rows(const race_desc_t* desc, const void* k,
+                             const void* v, const float* w, float* part,
+                             float* rownorms, void* workspace, void* stream);
+
 /* Fixed-order (deterministic) reduction of per-segment tables; carry may
  * be NULL (= 0) and is [BH, F, dv+1].  out is [BH, F, dv+1] for TOTAL and
  * [BH, nseg, F, dv+1] for PREFIX / SUFFIX.                                */
@@ -147,6 +154,15 @@ int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k,
                     const void* v, const float* w, const float* carries,
                     void* o, float* den, float* rownorms, void* workspace,
                     void* stream);
+
+/* race_fwd_causal given rownorms whose k halves race_kside_partials_rows
+ * wrote: the fast path then reads Q, V and those rows instead of K (the k
+ * projections are not recomputed) and fills in the q halves.  Same
+ * outputs as race_fwd_causal.                                             */
+int race_fwd_causal_krows(const race_desc_t* desc, const void* q,
+                          const void* k, const void* v, const float* w,
+                          const float* carries, void* o, float* den,
+                          float* rownorms, void* workspace, void* stream);
 
 /* Non-causal backward, query side: dq and per-segment partial dS
  * (ra/backward.py:109-118 + the d_num/d_den prologue 201-209).           */

@@ -27,6 +27,7 @@ EXPORTS = (
     "race_workspace_bytes", "race_state_elems", "race_fwd", "race_bwd",
     "race_kside_partials", "race_combine", "race_fwd_readout", "race_fwd_causal",
     "race_bwd_qside", "race_bwd_kside", "race_bwd_causal_q", "race_bwd_causal_k",
+    "race_kside_partials_rows", "race_fwd_causal_krows",
 )
 
 
@@ -81,6 +82,8 @@ _SIGS = {
     "race_bwd_kside": ([_P] * 9, ctypes.c_int),
     "race_bwd_causal_q": ([_P] * 14, ctypes.c_int),
     "race_bwd_causal_k": ([_P] * 14, ctypes.c_int),
+    "race_kside_partials_rows": ([_P] * 8, ctypes.c_int),
+    "race_fwd_causal_krows": ([_P] * 11, ctypes.c_int),
 }
 
 

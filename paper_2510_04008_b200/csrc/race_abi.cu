@@ -1,3 +1,4 @@
+#include <cstdlib>
 // race_abi.cu -- the extern "C" boundary declared in include/race_b200.h.
 //
 // Validation mirrors the reference's ValueError rules (SketchConfig
@@ -17,7 +18,8 @@
 namespace race {
 // fast path (race_tc.cu)
 bool tc_supported(const Geo& g);
-cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st);
+cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, float* rows,
+                         cudaStream_t st);
 cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float* tab, void* o, float* den,
                        cudaStream_t st);
 cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* w, const float* tab, void* dq,
@@ -32,7 +34,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
                             const float* nrm, void* dk, void* dv, cudaStream_t st);
 cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* w, float* rows, cudaStream_t st);
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                          const float* car, void* o, float* den, float* nrm, cudaStream_t st);
+                          const float* car, void* o, float* den, float* nrm, bool krows, cudaStream_t st);
 }  // namespace race
 
 namespace race {
@@ -186,8 +188,18 @@ int race_kside_partials(const race_desc_t* desc, const void* k, const void* v, c
   race::Geo g;
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
-  if (race::tc_supported(g)) return cuda_status(race::tc_aggregate(g, k, v, w, part, S(stream)), "tc_aggregate");
+  if (race::tc_supported(g)) return cuda_status(race::tc_aggregate(g, k, v, w, part, nullptr, S(stream)), "tc_aggregate");
   return cuda_status(race::simt_aggregate(g, k, v, w, part, S(stream)), "aggregate");
+}
+
+int race_kside_partials_rows(const race_desc_t* desc, const void* k, const void* v, const float* w, float* part,
+                             float* rownorms, void* workspace, void* stream) {
+  race::Geo g;
+  if (int rc = resolve(desc, &g)) return rc;
+  if (g.N == 0) return RACE_OK;
+  if (!g.causal || !race::tc_supported(g) || !rownorms)
+    return race_kside_partials(desc, k, v, w, part, workspace, stream);
+  return cuda_status(race::tc_aggregate(g, k, v, w, part, rownorms, S(stream)), "tc_aggregate");
 }
 
 int race_combine(const race_desc_t* desc, int32_t mode, const float* part, const float* carry, float* out,
@@ -223,8 +235,22 @@ int race_fwd_causal(const race_desc_t* desc, const void* q, const void* k, const
   if (int rc = resolve(desc, &g)) return rc;
   if (g.N == 0) return RACE_OK;
   if (race::tc_supported(g))
-    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, S(stream)), "tc_causal_fwd");
+    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, false, S(stream)), "tc_causal_fwd");
   return cuda_status(race::simt_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, S(stream)), "causal_fwd");
+}
+
+int race_fwd_causal_krows(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w,
+                          const float* carries, void* o, float* den, float* rownorms, void* workspace,
+                          void* stream) {
+  race::Geo g;
+  if (int rc = resolve(desc, &g)) return rc;
+  if (g.N == 0) return RACE_OK;
+  if (!g.causal) return fail(RACE_EBADSHAPE, "race_fwd_causal_krows needs a causal desc");
+  if (!rownorms) return fail(RACE_EBADSHAPE, "race_fwd_causal_krows needs the sketch rows");
+  if (race::tc_supported(g))
+    return cuda_status(race::tc_causal_fwd(g, q, k, v, w, carries, o, den, rownorms, true, S(stream)),
+                       "tc_causal_fwd");
+  return race_fwd_causal(desc, q, k, v, w, carries, o, den, rownorms, workspace, stream);
 }
 
 int race_bwd_qside(const race_desc_t* desc, const void* q, const void* d_o, const float* w, const float* tables,
@@ -297,14 +323,22 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
   WsLayout ws = ws_layout(g, workspace);
   float* tabs = state ? state : ws.tables;
-  if (int rc = race_kside_partials(desc, k, v, w, ws.part, workspace, stream)) return rc;
-  if (!g.causal) {
-    if (int rc = race_combine(desc, RACE_COMBINE_TOTAL, ws.part, nullptr, tabs, stream)) return rc;
-    return race_fwd_readout(desc, q, w, tabs, o, den, workspace, stream);
+  static const bool no_krows = getenv("RACE_NO_KROWS") != nullptr;  // A/B diagnostic
+  if (g.causal && !no_krows) {
+    // the aggregation also writes the k halves of the sketch rows, so the scan reads Q, V and those rows
+    float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : ws.rows;
+    if (int rc = race_kside_partials_rows(desc, k, v, w, ws.part, nrm, workspace, stream)) return rc;
+    if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
+    return race_fwd_causal_krows(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
   }
-  if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
-  float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
-  return race_fwd_causal(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
+  if (int rc = race_kside_partials(desc, k, v, w, ws.part, workspace, stream)) return rc;
+  if (g.causal) {
+    if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
+    float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
+    return race_fwd_causal(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
+  }
+  if (int rc = race_combine(desc, RACE_COMBINE_TOTAL, ws.part, nullptr, tabs, stream)) return rc;
+  return race_fwd_readout(desc, q, w, tabs, o, den, workspace, stream);
 }
 
 int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, const void* d_o,

@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int s = gc % STAGES;
         const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
         mbar_wait(&full[s], (gc / STAGES) & 1);
-        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
+        const float sumsq = tile_row_sumsq(stage, r);
+        const float inv = inv_scale(sumsq, a.normalize);
         mbar_wait(proj_full, gc & 1);
         tc_fence_after();
         float proj[16];
@@ -346,6 +347,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(phi_full);
+        if (a.rows_out && t + r < m.t1) {  // causal: the k half of this key's sketch row (off the MMA chain)
+          float hat[5];
+          row_hat(a, proj, inv, hat);
+          store_row_half(a.rows_out + (int64_t(m.bh) * a.N + t + r) * ROWW + 8, hat, sumsq);
+        }
       }
       // segment done: S^T (lane r = value column r) from its TMEM buffer, A by a block sum
       mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
@@ -821,10 +827,13 @@ constexpr uint32_t TM_PA = 192;  // P~ as bf16 pairs: 128 lanes x 64 columns
 static_assert(SMEM <= 232448, "k_causal_fwd8 shared memory");
 }  // namespace cfw8
 
-template <int P>
+// KR: the k halves of the sketch rows were written by the key-side aggregation (k_aggregate2),
+// so this pass reads Q, V and those rows instead of K (no K tile, no K projection).
+template <int P, bool KR>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_causal_fwd8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Args a) {
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                  const __grid_constant__ CUtensorMap tmROWS, Args a) {
   using namespace cfw8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -900,10 +909,16 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         mbar_wait(&emptyqk[s], ((gc >> 1) & 1) ^ 1);
         RACE_TRACE(a, 0, gc);
-        mbar_arrive_expect_tx(&fullqk[s], 2 * TILE);
-        for (int h = 0; h < 2; ++h) {
-          tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
-          tma_load_3d(st + TILE + h * SUB, &tmK, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+        if (KR) {  // Q tile + the chunk's sketch rows (in the unused K slot)
+          mbar_arrive_expect_tx(&fullqk[s], TILE + CH * ROWW * 4);
+          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+          tma_load_2d(st + TILE, &tmROWS, &fullqk[s], 0, int(cur.m.bh) * int(a.N) + int(cur.t), pol);
+        } else {
+          mbar_arrive_expect_tx(&fullqk[s], 2 * TILE);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+            tma_load_3d(st + TILE + h * SUB, &tmK, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+          }
         }
         if (gc >= 2) {
           store_o(gc - 2);
@@ -939,7 +954,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+            if (!KR) umma_bf16(tmem + TM_PROJK, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
           }
           umma_commit(proj_full);
           umma_commit(&emptyqk[s]);
@@ -996,13 +1011,25 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     }
     float A[FP], snext[FP];
     float sqq = 0.f, sqk = 0.f;  // row norms^2 of the current chunk
+    float hk[5];                 // KR: stored k projections of the current chunk (h == 1)
+    // row norm^2 of my row of the chunk held by stage sn; KR + h == 1: read from the sketch row
+    auto stage_norm = [&](int sn) -> float {
+      if (KR && h == 1) {
+        const float* rw = reinterpret_cast<const float*>(smem + OFF_STAGE + sn * STAGE_BYTES + TILE) + r * ROWW + 8;
+        const float4 x0 = reinterpret_cast<const float4*>(rw)[0];
+        const float4 x1 = reinterpret_cast<const float4*>(rw)[1];
+        hk[0] = x0.x; hk[1] = x0.y; hk[2] = x0.z; hk[3] = x0.w; hk[4] = x1.x;
+        return x1.w;
+      }
+      return tile_row_sumsq(sb + OFF_STAGE + sn * STAGE_BYTES + h * TILE, r);
+    };
     uint32_t gc = 0;
     int64_t prev_bh = -1;
     Cursor cur;
     cur.start(a, i0, i1);
     if (cur.ok()) {  // norms of the very first chunk
       mbar_wait(&fullqk[0], 0);
-      const float sq = tile_row_sumsq(sb + OFF_STAGE + h * TILE, r);
+      const float sq = stage_norm(0);
       xbase[h * 128 + r] = sq;
       compute_bar256();
       if (threadIdx.x == CT0) mbar_arrive(&emptyqk[0]);
@@ -1064,16 +1091,25 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(phi_full);
       } else {
-        float pq[16], pk[16], phk[FP];
-        tmem_ld16(tmem + lb + TM_PROJK, pk);
-        tmem_ld16(tmem + lb + TM_PROJQ, pq);
-        tmem_ld_wait();
-        row_features<P>(a, pk, invk, valid, phk);
-        write_phi_k(sb + OFF_PHIK, r, phk);
-        if (a.rows_out && valid) {  // sketch row, k half
-          float hat[5];
-          row_hat(a, pk, invk, hat);
-          store_row_half(a.rows_out + (m.bh * a.N + t + r) * ROWW + 8, hat, sqk);
+        float pq[16], phk[FP];
+        if (KR) {
+          float u[5];
+          row_features_hat<P>(a, hk, valid, phk, u);
+          tmem_ld16(tmem + lb + TM_PROJQ, pq);
+          write_phi_k(sb + OFF_PHIK, r, phk);
+          tmem_ld_wait();
+        } else {
+          float pk[16];
+          tmem_ld16(tmem + lb + TM_PROJK, pk);
+          tmem_ld16(tmem + lb + TM_PROJQ, pq);
+          tmem_ld_wait();
+          row_features<P>(a, pk, invk, valid, phk);
+          write_phi_k(sb + OFF_PHIK, r, phk);
+          if (a.rows_out && valid) {  // sketch row, k half
+            float hat[5];
+            row_hat(a, pk, invk, hat);
+            store_row_half(a.rows_out + (m.bh * a.N + t + r) * ROWW + 8, hat, sqk);
+          }
         }
         fence_proxy_async();
         tc_fence_before();
@@ -1132,7 +1168,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       if (cur.ok()) {
         const int sn = (gc + 1) & 1;
         mbar_wait(&fullqk[sn], ((gc + 1) >> 1) & 1);
-        const float sq = tile_row_sumsq(sb + OFF_STAGE + sn * STAGE_BYTES + h * TILE, r);
+        const float sq = stage_norm(sn);
         xpar[h * 128 + r] = sq;
       }
       compute_bar256();
@@ -1342,13 +1378,15 @@ bool tc_supported(const Geo& g) {
          g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 && tcfast::encode_fn() != nullptr;
 }
 
-cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, cudaStream_t st) {
+cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, float* rows,
+                         cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv;
   if (!make_map(&mk, k, g) || !make_map(&mv, v, g)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tout = part;
+  a.rows_out = rows;
   const char* v1 = getenv("RACE_AGG_V1");
   if (!(v1 && v1[0] == '1')) {
     switch (g.P) {
@@ -1403,12 +1441,15 @@ cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* 
   }
 }
 
+// krows: the k halves of nrm were written by tc_aggregate (then K is not read)
 cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* w,
-                          const float* car, void* o, float* den, float* nrm, cudaStream_t st) {
+                          const float* car, void* o, float* den, float* nrm, bool krows, cudaStream_t st) {
   using namespace tcfast;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv, mo, mr;
   if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mo, o, g))
     return cudaErrorInvalidValue;
+  if (krows && (!nrm || !make_map_rows(&mr, nrm, g.BH * g.N))) return cudaErrorInvalidValue;
+  if (!krows) mr = mq;  // unused
   Args a = make_args(g);
   a.w = w;
   a.tin = car;
@@ -1416,9 +1457,13 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.rows_out = nrm;
   a.dbg = trace_for("fwd");
   switch (g.P) {
-    case 1: return launch_nt(k_causal_fwd8<1>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-    case 2: return launch_nt(k_causal_fwd8<2>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
-    default: return launch_nt(k_causal_fwd8<3>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, a);
+#define RACE_FWD8(PP)                                                                                     \
+  return krows ? launch_nt(k_causal_fwd8<PP, true>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
+               : launch_nt(k_causal_fwd8<PP, false>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)
+    case 1: RACE_FWD8(1);
+    case 2: RACE_FWD8(2);
+    default: RACE_FWD8(3);
+#undef RACE_FWD8
   }
 }
 

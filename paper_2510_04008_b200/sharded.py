@@ -88,9 +88,16 @@ def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
     ws = pr.ws()
     part = torch.empty((pr.bh, pr.nseg, E), dtype=torch.float32, device=dev)
     local = torch.zeros((pr.bh, E), dtype=torch.float32, device=dev)
+    if p.causal:
+        state = torch.empty(pr.state_shape(), dtype=torch.float32, device=dev)
+        carries, norms = pr.split_causal_state(state)
     if pr.n:
-        _lib.check(L.race_kside_partials(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(part), _vp(ws), _stream()),
-                   "race_kside_partials")
+        if p.causal:  # the aggregation also writes the k halves of the sketch rows
+            _lib.check(L.race_kside_partials_rows(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(part), _vp(norms),
+                                                  _vp(ws), _stream()), "race_kside_partials_rows")
+        else:
+            _lib.check(L.race_kside_partials(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(part), _vp(ws), _stream()),
+                       "race_kside_partials")
         _combine(pr, _lib.COMBINE_TOTAL, part, None, local)
     if not p.causal:
         tables = comm.allreduce(local)
@@ -99,12 +106,10 @@ def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
                                           _stream()), "race_fwd_readout")
         return o, den, tables.view(pr.state_shape())
     carry = comm.carry(local, "prefix")
-    state = torch.empty(pr.state_shape(), dtype=torch.float32, device=dev)
-    carries, norms = pr.split_causal_state(state)
     if pr.n:
         _combine(pr, _lib.COMBINE_PREFIX, part, carry, carries)
-        _lib.check(L.race_fwd_causal(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(carries), _vp(o), _vp(den),
-                                     _vp(norms), _vp(ws), _stream()), "race_fwd_causal")
+        _lib.check(L.race_fwd_causal_krows(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(carries), _vp(o), _vp(den),
+                                     _vp(norms), _vp(ws), _stream()), "race_fwd_causal_krows")
     return o, den, state
 
 

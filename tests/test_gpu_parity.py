@@ -388,3 +388,41 @@ def test_long_context_prefix_and_oracle():
     assert rel_err(o0[0, 0].float().cpu(), o_r) <= TOL_BF16
     assert rel_err(den0[0, 0].cpu(), den_r) <= TOL_F32
     assert rel_err(dq0[0, 0].float().cpu(), dq_r) <= TOL_BF16
+
+
+@pytest.mark.parametrize("n", [1000, 4099, 70000])
+@pytest.mark.parametrize("pl", [(2, 2), (1, 3), (3, 1)], ids=["P2L2", "P1L3", "P3L1"])
+def test_causal_forward_from_kside_rows(n, pl):
+    """race_kside_partials_rows + race_fwd_causal_krows (k projections taken from the rows the
+    aggregation wrote; K not re-read) == race_kside_partials + race_fwd_causal."""
+    from paper_2510_04008_b200.functional import Problem, _stream, _vp
+
+    q, k, v, g, w, p = _big(n=n, causal=True)
+    P, L = pl
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=7, causal=True)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(q.device)
+    p = cfg.params()
+    pr = Problem(q, k, v, w, p)
+    lib, S, ws = _lib.lib(), _stream(), pr.ws()
+    outs = []
+    for krows in (False, True):
+        part = torch.empty((pr.bh, pr.nseg, pr.table_elems), device=q.device)
+        state = torch.full(pr.state_shape(), float("nan"), device=q.device)
+        car, rows = pr.split_causal_state(state)
+        o, den = torch.empty_like(v), torch.empty((1, 4, n), device=q.device)
+        if krows:
+            _lib.check(lib.race_kside_partials_rows(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(part), _vp(rows),
+                                                    _vp(ws), S), "kside_rows")
+        else:
+            _lib.check(lib.race_kside_partials(pr.dref, _vp(k), _vp(v), _vp(pr.w), _vp(part), _vp(ws), S), "kside")
+        _lib.check(lib.race_combine(pr.dref, _lib.COMBINE_PREFIX, _vp(part), None, _vp(car), S), "combine")
+        fn = lib.race_fwd_causal_krows if krows else lib.race_fwd_causal
+        _lib.check(fn(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(car), _vp(o), _vp(den), _vp(rows), _vp(ws), S),
+                   "fwd")
+        torch.cuda.synchronize()
+        outs.append((o.float().cpu(), den.cpu(), state.cpu()))
+    (o0, d0, s0), (o1, d1, s1) = outs
+    assert torch.isfinite(s1).all()
+    assert rel_err(s1, s0) <= 1e-6
+    assert rel_err(d1, d0) <= 1e-5
+    assert rel_err(o1, o0) <= 1e-2
