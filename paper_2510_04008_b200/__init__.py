@@ -33,6 +33,35 @@ from .functional import (
 )
 from .module import RaceAttention, head_hyperplanes
 from .sharded import sharded_backward, sharded_forward, shard_bounds
+from .sketch import (
+    BucketStats,
+    HashTable,
+    bucket_stats,
+    corner_matrix,
+    corner_vector,
+    dominant_corner_mass,
+    hard_hash,
+    make_hash_table,
+    soft_features,
+)
+from .exact import (
+    angular_attention,
+    angular_attention_vjp,
+    angular_kernel_matrix,
+    angular_similarity,
+    softmax_attention,
+    softmax_attention_vjp,
+)
+from .theory import (
+    bias_sweep,
+    collision_identity_check,
+    hard_race_attention,
+    kernel_deviation,
+    output_rms_error,
+    race_kernel,
+    row_sum_stability,
+    variance_sweep,
+)
 
 __version__ = "0.1.0"
 
@@ -42,4 +71,10 @@ __all__ = [
     "all_hyperplanes", "derive_table_rng", "gaussian_matrix", "head_hyperplanes", "race_attention",
     "race_attention_torch", "race_attention_vjp", "race_backward", "race_forward", "shard_bounds",
     "sharded_backward", "sharded_forward", "table_hyperplanes",
+    # validation side (sketch.py, exact.py, theory.py, benchmark.py)
+    "BucketStats", "HashTable", "angular_attention", "angular_attention_vjp", "angular_kernel_matrix",
+    "angular_similarity", "bias_sweep", "bucket_stats", "collision_identity_check", "corner_matrix",
+    "corner_vector", "dominant_corner_mass", "hard_hash", "hard_race_attention", "kernel_deviation",
+    "make_hash_table", "output_rms_error", "race_kernel", "row_sum_stability", "soft_features",
+    "softmax_attention", "softmax_attention_vjp", "variance_sweep",
 ]

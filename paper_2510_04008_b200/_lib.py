@@ -85,6 +85,22 @@ _SIGS = {
     "race_kside_partials_rows": ([_P] * 8, ctypes.c_int),
     "race_fwd_causal_krows": ([_P] * 11, ctypes.c_int),
 }
+_I32, _I64, _F64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+# include/race_aux.h (validation-side GPU functions; float64 compute)
+RACE_F64 = 2
+AUX_SIGS = {
+    "race_aux_soft_features": ([_I32, _I64, _I32, _P, _P, _I32, _I32, _F64, _I32, _P, _P], ctypes.c_int),
+    "race_aux_hard_hash": ([_I32, _I64, _I32, _P, _P, _I32, _I32, _I32, _P, _P], ctypes.c_int),
+    "race_aux_feature_gram": ([_I64, _I64, _I32, _P, _P, _F64, _P, _P], ctypes.c_int),
+    "race_aux_hard_workspace_bytes": ([_I32, _I32, _I32], ctypes.c_size_t),
+    "race_aux_hard_attention": ([_I32, _I64, _I32, _P, _P, _P, _I32, _I32, _P, _P, _P, _P], ctypes.c_int),
+    "race_aux_angular_kernel": ([_I32, _I64, _I64, _I32, _P, _P, _I32, _P, _P], ctypes.c_int),
+    "race_aux_angular_fwd": ([_I32, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "race_aux_angular_bwd": ([_I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P],
+                             ctypes.c_int),
+}
+AUX_EXPORTS = tuple(AUX_SIGS)
+_SIGS.update(AUX_SIGS)
 
 
 def lib() -> ctypes.CDLL:

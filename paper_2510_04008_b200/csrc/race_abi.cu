@@ -11,6 +11,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <type_traits>
+
+#include "race_common.cuh"
 
 #include "race_b200.h"
 #include "race_internal.h"
@@ -64,9 +67,18 @@ int cuda_status(cudaError_t e, const char* where) {
   return fail(RACE_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
+}  // namespace
+
+namespace race {  // error reporting for race_aux.cu
+int report(int code, const char* msg) { return fail(code, "%s", msg); }
+int report_cuda(cudaError_t e, const char* where) { return cuda_status(e, where); }
+}  // namespace race
+
+namespace {
+
 constexpr int64_t kSegTarget = 148 * 8;  // CTAs to aim for across all (b, h)
 
-int resolve(const race_desc_t* d, race::Geo* g) {
+int resolve_shape(const race_desc_t* d, race::Geo* g) {
   if (!d) return fail(RACE_EBADSHAPE, "null descriptor");
   if (d->abi_version != RACE_ABI_VERSION)
     return fail(RACE_EBADSHAPE, "abi_version %d != %d", d->abi_version, RACE_ABI_VERSION);
@@ -93,9 +105,6 @@ int resolve(const race_desc_t* d, race::Geo* g) {
   g->w_per_head = d->w_per_head ? 1 : 0;
   g->dtype = d->dtype;
   g->causal = d->causal ? 1 : 0;
-  const int64_t F = int64_t(d->tables) << d->hyperplanes;
-  if (F > 4096 || F * (d->dim_v + 1) > (1 << 22))
-    return fail(RACE_EUNSUPPORTED, "F=%lld buckets x dv=%d too large for the GPU path", (long long)F, d->dim_v);
   int64_t target = (kSegTarget + g->BH - 1) / g->BH;
   if (target < 1) target = 1;
   int64_t per = (g->N + target - 1) / target;
@@ -104,9 +113,40 @@ int resolve(const race_desc_t* d, race::Geo* g) {
   g->seg_tokens = per;
   g->nseg = g->N > 0 ? (g->N + per - 1) / per : 1;
   if (g->nseg > 0x7fffffff) return fail(RACE_EUNSUPPORTED, "too many segments");
-  if (race::simt_max_smem(*g) > 227 * 1024 && !race::tc_supported(*g))
-    return fail(RACE_EUNSUPPORTED, "d=%d dv=%d F=%lld exceed the shared-memory budget of the generic path", g->d,
-                g->dv, (long long)F);
+  return RACE_OK;
+}
+
+// one pass of the kernels holds all F = T * 2^P buckets of a row in shared memory
+bool fits(const race::Geo& g) {
+  const int64_t F = int64_t(g.T) << g.P;
+  if (F > 4096 || F * (g.dv + 1) > (1 << 22)) return false;
+  return race::tc_supported(g) || race::simt_max_smem(g) <= 227 * 1024;
+}
+
+int resolve(const race_desc_t* d, race::Geo* g) {
+  if (int rc = resolve_shape(d, g)) return rc;
+  if (!fits(*g))
+    return fail(RACE_EUNSUPPORTED, "d=%d dv=%d with F=%lld buckets exceeds one pass of the GPU kernels", g->d,
+                g->dv, (long long)(int64_t(g->T) << g->P));
+  return RACE_OK;
+}
+
+// Table groups: the estimator is a sum over tables (ra/forward.py:124-144), so a
+// config whose F does not fit one pass runs as groups of *tg tables each.  tg == T
+// means no grouping.
+int group_plan(const race_desc_t* d, race::Geo* g, int* tg) {
+  if (int rc = resolve_shape(d, g)) return rc;
+  if (fits(*g)) {
+    *tg = g->T;
+    return RACE_OK;
+  }
+  race::Geo s = *g;
+  for (s.T = g->T - 1; s.T >= 1 && !fits(s); --s.T) {
+  }
+  if (s.T < 1)
+    return fail(RACE_EUNSUPPORTED, "d=%d dv=%d P=%d: even one table exceeds one pass of the GPU kernels", g->d,
+                g->dv, g->P);
+  *tg = s.T;
   return RACE_OK;
 }
 
@@ -146,6 +186,140 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// ---------------------------------------------------------------------------
+// Table groups (group_plan): scratch layout and the elementwise kernels that
+// sum the groups' numerators / denominators and gradients.
+// ---------------------------------------------------------------------------
+struct GroupWs {
+  void* sub;        // workspace of one group's sub-problem
+  float* w;         // [H, tg * P, d] hyperplanes of the group (w_per_head)
+  void* o;          // [BH, N, dv] one group's output (dtype)
+  float* den;       // [BH, N]
+  float* num_acc;   // [BH, N, dv] sum of numerators
+  float* d_acc;     // [BH, N] sum of (unaveraged) denominators
+  float* rden;      // [BH, Np] 1 / D of the whole estimator
+  float* gden;      // [BH, Np] -(dO . O) / D
+  void* dq;         // [BH, N, d] one group's gradients (dtype)
+  void* dk;
+  void* dv;
+  float* dq_acc;    // fp32 sums
+  float* dk_acc;
+  float* dv_acc;
+  size_t bytes;
+};
+
+GroupWs group_ws(const race::Geo& g, int tg, void* base) {
+  race::Geo s = g;
+  s.T = tg;
+  const int64_t tok = g.BH * (g.N > 0 ? g.N : 1);
+  const int64_t ptok = g.BH * (g.N > 0 ? (g.N + 3) & ~int64_t(3) : 4);
+  const size_t e = g.dtype == RACE_BF16 ? 2 : 4;
+  GroupWs w{};
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t n) -> void* { void* r = p ? p + off : nullptr; off += (n + 255) & ~size_t(255); return r; };
+  w.sub = take(ws_layout(s, nullptr).bytes);
+  w.w = static_cast<float*>(take(sizeof(float) * size_t(g.H) * tg * g.P * g.d));
+  w.o = take(e * tok * g.dv);
+  w.den = static_cast<float*>(take(sizeof(float) * tok));
+  w.num_acc = static_cast<float*>(take(sizeof(float) * tok * g.dv));
+  w.d_acc = static_cast<float*>(take(sizeof(float) * tok));
+  w.rden = static_cast<float*>(take(sizeof(float) * ptok));
+  w.gden = static_cast<float*>(take(sizeof(float) * ptok));
+  w.dq = take(e * tok * g.d);
+  w.dk = take(e * tok * g.d);
+  w.dv = take(e * tok * g.dv);
+  w.dq_acc = static_cast<float*>(take(sizeof(float) * tok * g.d));
+  w.dk_acc = static_cast<float*>(take(sizeof(float) * tok * g.d));
+  w.dv_acc = static_cast<float*>(take(sizeof(float) * tok * g.dv));
+  w.bytes = off;
+  return w;
+}
+
+using race::from_f32;
+using race::to_f32;
+
+// num_acc (+)= o_g * D_g, d_acc (+)= D_g with D_g = den_g * tg (den_g is the group's averaged den)
+template <typename T>
+__global__ void k_group_fwd_acc(int64_t rows, int dv, const T* __restrict__ o, const float* __restrict__ den, float tg,
+                                int first, float* __restrict__ num_acc, float* __restrict__ d_acc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows * dv) return;
+  const int64_t r = i / dv;
+  const float D = den[r] * tg;
+  const float x = to_f32(o[i]) * D;
+  num_acc[i] = first ? x : num_acc[i] + x;
+  if (i % dv == 0) d_acc[r] = first ? D : d_acc[r] + D;
+}
+
+// o = num / D (zero when the averaged den is degenerate, ra/forward.py:157-163), den = D / T
+template <typename T>
+__global__ void k_group_fwd_out(int64_t rows, int dv, const float* __restrict__ num_acc,
+                                const float* __restrict__ d_acc, float T_, T* __restrict__ o, float* __restrict__ den) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows * dv) return;
+  const int64_t r = i / dv;
+  const float D = d_acc[r];
+  const bool live = D / T_ > race::kDegenerateDenEps;
+  o[i] = from_f32<T>(live ? num_acc[i] / D : 0.f);
+  if (i % dv == 0) den[r] = D / T_;
+}
+
+// rden = 1 / D, gden = -(dO . O) / D of the whole estimator; one warp per row
+template <typename T>
+__global__ void k_group_rg(int64_t BH, int64_t N, int dv, const float* __restrict__ num_acc,
+                           const float* __restrict__ d_acc, const T* __restrict__ d_o, float T_,
+                           float* __restrict__ rden, float* __restrict__ gden) {
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= BH * N) return;
+  const float D = d_acc[r];
+  const bool live = D / T_ > race::kDegenerateDenEps;
+  const float rD = live ? 1.f / D : 0.f;
+  float dot = 0.f;
+  for (int c = lane; c < dv; c += 32) dot = fmaf(to_f32(d_o[r * dv + c]), num_acc[r * dv + c] * rD, dot);
+  dot = race::warp_sum(dot);
+  if (lane == 0) {
+    const int64_t i = (r / N) * ((N + 3) & ~int64_t(3)) + r % N;
+    rden[i] = rD;
+    gden[i] = -dot * rD;
+  }
+}
+
+template <typename T>
+__global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int first, float* __restrict__ acc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) acc[i] = first ? to_f32(x[i]) : acc[i] + to_f32(x[i]);
+}
+
+template <typename T>
+__global__ void k_group_cast(int64_t n, const float* __restrict__ acc, T* __restrict__ x) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = from_f32<T>(acc[i]);
+}
+
+unsigned blocks_for(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+template <typename F>
+cudaError_t by_dtype(int dtype, F&& f) {
+  return dtype == RACE_BF16 ? f(static_cast<__nv_bfloat16*>(nullptr)) : f(static_cast<float*>(nullptr));
+}
+
+// (sub-descriptor, hyperplanes) of the group of `cnt` tables starting at table t0
+const float* group_w(const race::Geo& g, const float* w, int t0, int cnt, const GroupWs& ws, cudaStream_t st,
+                     cudaError_t* err) {
+  const size_t row = size_t(g.P) * g.d * sizeof(float);
+  if (!g.w_per_head) return w + size_t(t0) * g.P * g.d;
+  *err = cudaMemcpy2DAsync(ws.w, cnt * row, w + size_t(t0) * g.P * g.d, size_t(g.T) * row, cnt * row, size_t(g.H),
+                           cudaMemcpyDeviceToDevice, st);
+  return ws.w;
+}
+
+int fwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
+                const float* w, void* o, float* den, void* workspace, void* stream, bool final_out);
+int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
+                const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -162,7 +336,8 @@ int race_fast_path(const race_desc_t* desc) {
 
 int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens) {
   race::Geo g;
-  if (int rc = resolve(desc, &g)) return rc;
+  int tg;
+  if (int rc = group_plan(desc, &g, &tg)) return rc;
   if (nseg) *nseg = g.nseg;
   if (seg_tokens) *seg_tokens = g.seg_tokens;
   return RACE_OK;
@@ -170,14 +345,20 @@ int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens) {
 
 int race_workspace_bytes(const race_desc_t* desc, size_t* bytes) {
   race::Geo g;
-  if (int rc = resolve(desc, &g)) return rc;
-  *bytes = ws_layout(g, nullptr).bytes;
+  int tg;
+  if (int rc = group_plan(desc, &g, &tg)) return rc;
+  *bytes = tg == g.T ? ws_layout(g, nullptr).bytes : group_ws(g, tg, nullptr).bytes;
   return RACE_OK;
 }
 
 int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   race::Geo g;
-  if (int rc = resolve(desc, &g)) return rc;
+  int tg;
+  if (int rc = group_plan(desc, &g, &tg)) return rc;
+  if (tg < g.T) {  // table groups: race_bwd recomputes, there is no saved state
+    *elems = 0;
+    return RACE_OK;
+  }
   *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g) + (g.causal ? 16 * g.BH * g.N : 0);
   return RACE_OK;
 }
@@ -318,9 +499,14 @@ int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, con
 int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, void* o,
              float* den, float* state, void* workspace, void* stream) {
   race::Geo g;
-  if (int rc = resolve(desc, &g)) return rc;
+  int tg;
+  if (int rc = group_plan(desc, &g, &tg)) return rc;
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
+  if (tg < g.T) {
+    if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
+    return fwd_grouped(desc, g, tg, q, k, v, w, o, den, workspace, stream, true);
+  }
   WsLayout ws = ws_layout(g, workspace);
   float* tabs = state ? state : ws.tables;
   static const bool no_krows = getenv("RACE_NO_KROWS") != nullptr;  // A/B diagnostic
@@ -344,9 +530,14 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
 int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, const void* d_o,
              const float* state, void* dq, void* dk, void* dv, void* workspace, void* stream) {
   race::Geo g;
-  if (int rc = resolve(desc, &g)) return rc;
+  int tg;
+  if (int rc = group_plan(desc, &g, &tg)) return rc;
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
+  if (tg < g.T) {
+    if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
+    return bwd_grouped(desc, g, tg, q, k, v, w, d_o, dq, dk, dv, workspace, stream);
+  }
   WsLayout ws = ws_layout(g, workspace);
   const float* tabs = state;
   if (!tabs) {
@@ -374,3 +565,108 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
 }
 
 }  // extern "C"
+
+namespace {
+
+int fwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
+                const float* w, void* o, float* den, void* workspace, void* stream, bool final_out) {
+  const GroupWs ws = group_ws(g, tg, workspace);
+  const int64_t rows = g.BH * g.N;
+  for (int t0 = 0; t0 < g.T; t0 += tg) {
+    const int cnt = g.T - t0 < tg ? g.T - t0 : tg;
+    race_desc_t sd = *desc;
+    sd.tables = cnt;
+    cudaError_t e = cudaSuccess;
+    const float* wg = group_w(g, w, t0, cnt, ws, S(stream), &e);
+    if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
+    if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, nullptr, ws.sub, stream)) return rc;
+    e = by_dtype(g.dtype, [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      k_group_fwd_acc<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(
+          rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), t0 == 0, ws.num_acc, ws.d_acc);
+      race::note_launch();
+      return cudaGetLastError();
+    });
+    if (int rc = cuda_status(e, "table group sum")) return rc;
+  }
+  if (!final_out) return RACE_OK;
+  cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    k_group_fwd_out<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc, float(g.T),
+                                                                       static_cast<T*>(o), den);
+    race::note_launch();
+    return cudaGetLastError();
+  });
+  return cuda_status(e, "table group output");
+}
+
+// Backward with table groups: the per-token normalisers 1/D and -(dO.O)/D of the whole
+// estimator come from a grouped forward; each group then runs the generic backward kernels
+// with those normalisers (Geo::ext_rden/ext_gden) and the groups' gradients are summed.
+int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
+                const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace, void* stream) {
+  const GroupWs ws = group_ws(g, tg, workspace);
+  const int64_t rows = g.BH * g.N;
+  if (int rc = fwd_grouped(desc, g, tg, q, k, v, w, nullptr, nullptr, workspace, stream, false)) return rc;
+  cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    k_group_rg<T><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
+                                                                static_cast<const T*>(d_o), float(g.T), ws.rden,
+                                                                ws.gden);
+    race::note_launch();
+    return cudaGetLastError();
+  });
+  if (int rc = cuda_status(e, "table group normalisers")) return rc;
+  for (int t0 = 0; t0 < g.T; t0 += tg) {
+    const int cnt = g.T - t0 < tg ? g.T - t0 : tg;
+    race_desc_t sd = *desc;
+    sd.tables = cnt;
+    race::Geo gs;
+    if (int rc = resolve(&sd, &gs)) return rc;
+    gs.ext_rden = ws.rden;
+    gs.ext_gden = ws.gden;
+    const float* wg = group_w(g, w, t0, cnt, ws, S(stream), &e);
+    if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
+    const WsLayout sub = ws_layout(gs, ws.sub);
+    const cudaStream_t st = S(stream);
+    e = race::simt_aggregate(gs, k, v, wg, sub.part, st);
+    if (!g.causal) {
+      if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
+      if (e == cudaSuccess) e = race::simt_bwd_q(gs, q, d_o, wg, sub.tables, ws.dq, sub.dpart, st);
+      if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.dpart, nullptr, sub.dtables, st);
+      if (e == cudaSuccess) e = race::simt_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, ws.dv, st);
+    } else {
+      if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_PREFIX, sub.part, nullptr, sub.tables, st);
+      if (e == cudaSuccess)
+        e = race::simt_bwd_causal_q(gs, q, k, v, d_o, wg, sub.tables, ws.dq, nullptr, nullptr, sub.dpart, st);
+      if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_SUFFIX, sub.dpart, nullptr, sub.dtables, st);
+      if (e == cudaSuccess)
+        e = race::simt_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, ws.dk, ws.dv, st);
+    }
+    if (int rc = cuda_status(e, "table group backward")) return rc;
+    e = by_dtype(g.dtype, [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      const int first = t0 == 0;
+      k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dq), first,
+                                                                  ws.dq_acc);
+      k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dk), first,
+                                                                  ws.dk_acc);
+      k_group_grad_acc<T><<<blocks_for(rows * g.dv), 256, 0, st>>>(rows * g.dv, static_cast<const T*>(ws.dv), first,
+                                                                   ws.dv_acc);
+      race::note_launch(3);
+      return cudaGetLastError();
+    });
+    if (int rc = cuda_status(e, "table group gradient sum")) return rc;
+  }
+  e = by_dtype(g.dtype, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    k_group_cast<T><<<blocks_for(rows * g.d), 256, 0, S(stream)>>>(rows * g.d, ws.dq_acc, static_cast<T*>(dq));
+    k_group_cast<T><<<blocks_for(rows * g.d), 256, 0, S(stream)>>>(rows * g.d, ws.dk_acc, static_cast<T*>(dk));
+    k_group_cast<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(rows * g.dv, ws.dv_acc, static_cast<T*>(dv));
+    race::note_launch(3);
+    return cudaGetLastError();
+  });
+  return cuda_status(e, "table group gradients");
+}
+
+}  // namespace

@@ -14,6 +14,10 @@ struct Geo {
   float beta;
   int normalize, w_per_head, dtype, causal;
   int64_t nseg, seg_tokens;
+  // table groups (race_abi.cu): per-token 1/D and -(dO.O)/D of the WHOLE estimator, [BH, Np];
+  // when set, the generic backward kernels use them instead of their own group's D and O
+  const float* ext_rden = nullptr;
+  const float* ext_gden = nullptr;
 };
 
 // every kernel launch in the library bumps this (race_launch_count)

@@ -436,19 +436,24 @@ __global__ void __launch_bounds__(NT) k_bwd_q(Geo g, const Tin* __restrict__ q, 
         num = fmaf(phq[r * pl.ldf + f], ys[r * pl.ldf + f], num);
       }
       const bool live = r < rows && D * invT > kDegenerateDenEps;
-      const float rD = live ? 1.f / D : 0.f;
+      float rD = live ? 1.f / D : 0.f;
+      float gD = live ? -num * rD * rD : 0.f;  // -(dO . O) / D
+      if (g.ext_rden) {  // table group: normalisers of the whole estimator
+        const int64_t i = bh * ((g.N + 3) & ~int64_t(3)) + t0 + r;
+        rD = r < rows ? g.ext_rden[i] : 0.f;
+        gD = r < rows ? g.ext_gden[i] : 0.f;
+      }
       rowv[kRD * TILE + r] = rD;
-      rowv[kRho * TILE + r] = live ? num * rD : 0.f;  // rho = dO . O
+      rowv[kGD * TILE + r] = gD;
     }
     __syncthreads();
     for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
       const int r = it / pl.F, f = it % pl.F;
-      dph[r * pl.ldf + f] = (ys[r * pl.ldf + f] - rowv[kRho * TILE + r] * S[f * pl.ldS + g.dv]) * rowv[kRD * TILE + r];
+      dph[r * pl.ldf + f] = ys[r * pl.ldf + f] * rowv[kRD * TILE + r] + rowv[kGD * TILE + r] * S[f * pl.ldS + g.dv];
     }
     for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
       const int r = it / (g.dv + 1), c = it % (g.dv + 1);
-      const float rD = rowv[kRD * TILE + r];
-      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rD : -rowv[kRho * TILE + r] * rD;
+      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rowv[kRD * TILE + r] : rowv[kGD * TILE + r];
     }
     __syncthreads();
     tile_feature_vjp<Tin>(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us, dph, dproj, dx,
@@ -561,28 +566,31 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restric
         num = fmaf(Pm[r * pl.ldp + j], Em[r * pl.ldp + j], num);
       }
       const bool live = r < rows && D * invT > kDegenerateDenEps;
-      const float rD = live ? 1.f / D : 0.f;
-      const float rho = live ? num * rD : 0.f;
-      rowv[kRD * TILE + r] = rD;
-      rowv[kRho * TILE + r] = rho;
-      if (r < rows) {
-        rden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] = rD;  // row pitch N rounded up to 4 (race_b200.h)
-        gden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] = -rho * rD;
+      float rD = live ? 1.f / D : 0.f;
+      float gD = live ? -num * rD * rD : 0.f;  // -(dO . O) / D
+      const int64_t i = bh * ((g.N + 3) & ~int64_t(3)) + t0 + r;  // row pitch N rounded up to 4 (race_b200.h)
+      if (g.ext_rden) {  // table group: normalisers of the whole estimator
+        rD = r < rows ? g.ext_rden[i] : 0.f;
+        gD = r < rows ? g.ext_gden[i] : 0.f;
+      } else if (r < rows) {
+        rden[i] = rD;
+        gden[i] = gD;
       }
+      rowv[kRD * TILE + r] = rD;
+      rowv[kGD * TILE + r] = gD;
     }
     __syncthreads();
     for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
       const int r = it / pl.F, f = it % pl.F;
-      const float rho = rowv[kRho * TILE + r];
-      float a = ys[r * pl.ldf + f] - rho * S[f * pl.ldS + g.dv];
+      const float rD = rowv[kRD * TILE + r], gD = rowv[kGD * TILE + r];
+      float a = ys[r * pl.ldf + f] * rD + gD * S[f * pl.ldS + g.dv];
       const int jmax = r < rows ? r : rows - 1;
-      for (int j = 0; j <= jmax; ++j) a = fmaf(Em[r * pl.ldp + j] - rho, phk[j * pl.ldf + f], a);
-      dph[r * pl.ldf + f] = a * rowv[kRD * TILE + r];
+      for (int j = 0; j <= jmax; ++j) a = fmaf(fmaf(Em[r * pl.ldp + j], rD, gD), phk[j * pl.ldf + f], a);
+      dph[r * pl.ldf + f] = a;
     }
     for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
       const int r = it / (g.dv + 1), c = it % (g.dv + 1);
-      const float rD = rowv[kRD * TILE + r];
-      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rD : -rowv[kRho * TILE + r] * rD;
+      gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rowv[kRD * TILE + r] : rowv[kGD * TILE + r];
     }
     __syncthreads();
     tile_feature_vjp<Tin>(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us, dph, dproj, dx,

@@ -114,10 +114,14 @@ class Problem:
     def ws(self) -> torch.Tensor:
         return workspace(_lib.workspace_bytes(self.desc), self.device)
 
-    def state_shape(self) -> tuple[int, ...]:
+    def state_shape(self) -> tuple[int, ...] | None:
         """Non-causal: the global tables [BH, F, dv+1].  Causal: a flat buffer holding the
         per-segment carries [BH, nseg, F, dv+1] then the q/k sketch rows [BH, N, 16]
-        (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h)."""
+        (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h).
+        None when the tables run in groups (F beyond one kernel pass): the backward
+        then recomputes, as the reference does (ra/backward.py:200)."""
+        if _lib.state_elems(self.desc) == 0:
+            return None
         f = self.p.tables << self.p.hyperplanes
         if self.p.causal:
             return (self.bh * self.nseg * f * (self.dv + 1) + 16 * self.bh * self.n,)
@@ -144,7 +148,8 @@ def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
     pr = Problem(q, k, v, w, p)
     o = torch.empty_like(v)
     den = torch.empty(pr.lead + (pr.n,), dtype=torch.float32, device=pr.device)
-    state = torch.empty(pr.state_shape(), dtype=torch.float32, device=pr.device) if want_state else None
+    shape = pr.state_shape() if want_state else None
+    state = torch.empty(shape, dtype=torch.float32, device=pr.device) if shape is not None else None
     if pr.n == 0 or pr.bh == 0:
         if state is not None:
             state.zero_()

@@ -15,22 +15,34 @@ from conftest import ROOT
 from paper_2510_04008_b200 import _lib
 
 HEADER = os.path.join(ROOT, "include", "race_b200.h")
+AUX_HEADER = os.path.join(ROOT, "include", "race_aux.h")
 
 
-def declared_symbols():
-    src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(race_\w+)\s*\(", src, flags=re.M)))
+def declared_symbols(header=HEADER):
+    src = open(header).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(race_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_matches_binding():
     assert set(declared_symbols()) == set(_lib.EXPORTS)
+    assert set(declared_symbols(AUX_HEADER)) == set(_lib.AUX_EXPORTS)
 
 
 def test_library_exports_every_symbol():
     so = ctypes.CDLL(_lib.LIB_PATH)
-    for name in declared_symbols():
+    for name in declared_symbols() + declared_symbols(AUX_HEADER):
         assert hasattr(so, name), name
     assert _lib.lib().race_abi_version() == _lib.ABI_VERSION
+
+
+def test_aux_validation_without_gpu():
+    L = _lib.lib()
+    # bad shapes are rejected on the host before any launch
+    assert L.race_aux_soft_features(0, 4, 8, None, None, 0, 1, 8.0, 1, None, None) == _lib.RACE_EBADSHAPE
+    assert L.race_aux_soft_features(0, 4, 8, None, None, 2, 1, 0.0, 1, None, None) == _lib.RACE_EBADSHAPE
+    assert L.race_aux_angular_fwd(0, 4, 512, 8, None, None, None, 2, 0, None, None, None) == _lib.RACE_EUNSUPPORTED
+    assert L.race_aux_hard_attention(0, 4, 8, None, None, None, 2, 1, None, None, None, None) == _lib.RACE_EBADSHAPE
+    assert L.race_aux_hard_workspace_bytes(8, 2, 3) == 8 * 3 * 4 * 9
 
 
 def _desc(**kw):

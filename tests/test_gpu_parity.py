@@ -426,3 +426,33 @@ def test_causal_forward_from_kside_rows(n, pl):
     assert rel_err(s1, s0) <= 1e-6
     assert rel_err(d1, d0) <= 1e-5
     assert rel_err(o1, o0) <= 1e-2
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("shape", [(300, 16, 16, 2, 300), (130, 128, 64, 3, 40)], ids=["L300", "P3L40"])
+def test_table_groups_match_oracle(causal, shape):
+    """F beyond one kernel pass (the reference's own criteria 4/5 use P=2 with up to 2048 tables):
+    tables run in groups whose numerators, denominators and gradients are summed."""
+    n, d, dv, P, L = shape
+    dev = _cuda()
+    rng = np.random.default_rng(5)
+    q, k, v, g = (rng.standard_normal((n, x)) for x in (d, d, dv, dv))
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=9, causal=causal)
+    from paper_2510_04008_b200.functional import Problem
+
+    t = [torch.tensor(x, dtype=torch.float32, device=dev)[None] for x in (q, k, v, g)]
+    w = torch.tensor(rb.all_hyperplanes(cfg, d), dtype=torch.float32, device=dev)
+    assert Problem(t[0], t[1], t[2], w, cfg.params()).state_shape() is None  # grouped: no saved state
+    o, den, st = rb.race_forward(t[0], t[1], t[2], w, cfg.params())
+    assert st is None
+    dq, dk, dvv = rb.race_backward(t[0], t[1], t[2], w, t[3], cfg.params())
+    wr = rb.all_hyperplanes(cfg, d)
+    o_r, den_r, _ = ro.forward(q, k, v, wr, cfg.beta, causal)
+    assert rel_err(o[0].cpu(), o_r) <= TOL_F32
+    assert rel_err(den[0].cpu(), den_r) <= TOL_F32
+    ref = ro.vjp(q, k, v, wr, cfg.beta, g, causal)
+    errs = grad_errs([x[0].cpu().numpy() for x in (dq, dk, dvv)], ref, GRAD_FLOOR)
+    assert max(errs) <= TOL_F32, errs
+    # the drop-in API runs the same configs (ra/acceptance.py criteria 4-5 use L up to 2048)
+    out = rb.race_attention(rb.AttnInputs(q, k, v), cfg, w=wr)
+    assert rel_err(out.o, o_r) <= TOL_F32
