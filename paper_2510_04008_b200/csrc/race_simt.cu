@@ -681,6 +681,7 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restric
 // shared memory, then each thread emits its group's prefixes/suffixes.  The
 // association is fixed by (nseg, CG), so results are bit-reproducible.
 constexpr int CG = 16;
+constexpr int CPER = 16;  // segments per group held in registers (nseg <= CG * CPER); longer groups loop
 __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, int64_t E, int mode,
                                                      const float* __restrict__ part, const float* __restrict__ carry,
                                                      float* __restrict__ out) {
@@ -692,9 +693,17 @@ __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, i
   const int64_t s0 = gy * per, s1 = s0 + per < nseg ? s0 + per : nseg;
   const bool ok = e < E;
   const float* p = part + bh * nseg * E + e;
+  const bool regs = per <= CPER;
+  float x[CPER];  // this group's segment values, all loads in flight at once
   float sum = 0.f;
-  if (ok)
+  if (regs) {
+#pragma unroll
+    for (int j = 0; j < CPER; ++j) x[j] = (ok && s0 + j < s1) ? p[(s0 + j) * E] : 0.f;
+#pragma unroll
+    for (int j = 0; j < CPER; ++j) sum += x[j];
+  } else if (ok) {
     for (int64_t i = s0; i < s1; ++i) sum += p[i * E];
+  }
   gs[gy][lx] = sum;
   __syncthreads();
   const float c = (ok && carry) ? carry[bh * E + e] : 0.f;
@@ -710,15 +719,33 @@ __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, i
   float base = c;
   if (mode == 1) {
     for (int g = 0; g < gy; ++g) base += gs[g][lx];
-    for (int64_t i = s0; i < s1; ++i) {
-      out[(bh * nseg + i) * E + e] = base;
-      base += p[i * E];
+    if (regs) {
+#pragma unroll
+      for (int j = 0; j < CPER; ++j)
+        if (s0 + j < s1) {
+          out[(bh * nseg + s0 + j) * E + e] = base;
+          base += x[j];
+        }
+    } else {
+      for (int64_t i = s0; i < s1; ++i) {
+        out[(bh * nseg + i) * E + e] = base;
+        base += p[i * E];
+      }
     }
   } else {
     for (int g = CG - 1; g > gy; --g) base += gs[g][lx];
-    for (int64_t i = s1 - 1; i >= s0; --i) {
-      out[(bh * nseg + i) * E + e] = base;
-      base += p[i * E];
+    if (regs) {
+#pragma unroll
+      for (int j = CPER - 1; j >= 0; --j)
+        if (s0 + j < s1) {
+          out[(bh * nseg + s0 + j) * E + e] = base;
+          base += x[j];
+        }
+    } else {
+      for (int64_t i = s1 - 1; i >= s0; --i) {
+        out[(bh * nseg + i) * E + e] = base;
+        base += p[i * E];
+      }
     }
   }
 }
