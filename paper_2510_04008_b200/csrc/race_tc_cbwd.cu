@@ -547,9 +547,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 // dV goes straight from TMEM to global memory.  Row norms are required.
 // ===========================================================================
 namespace ck8 {
-constexpr int OFF_K = 0;                   // two buffers (dK staged in place)
-constexpr int OFF_V = 2 * TILE;            // two buffers (dV staged in place once E / z are done)
-constexpr int OFF_DO = 4 * TILE;
+constexpr int OFF_K = 0;                   // one buffer (read by the tangent step only; dK staged in place)
+constexpr int OFF_V = TILE;                // two buffers (dV staged in place once E / z are done)
+constexpr int OFF_DO = 3 * TILE;           // two buffers
 constexpr int OFF_W = 5 * TILE;            // W' (projection; read MN-major as the B of dx^)
 constexpr int OFF_DSOPT = OFF_W + WOP;     // [16 x 128] B of z = V dS_v^T
 constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // [128 x 32] B of dV_a = Phi_k dS_v
@@ -604,11 +604,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* fullK = bars + 0;     // [2]
-  uint64_t* dkstaged = bars + 2;  // [2]
+  uint64_t* fullK = bars + 0;     // K landed (one buffer)
+  uint64_t* dkstaged = bars + 2;  // dK staged in the K buffer (256 arrivals)
   uint64_t* fullV = bars + 4;     // [2]
-  uint64_t* fullO = bars + 6;
-  uint64_t* emptyO = bars + 9;
+  uint64_t* fullO = bars + 6;     // [2]
+  uint64_t* emptyO = bars + 8;    // [2]
   uint64_t* projf = bars + 10;
   uint64_t* c1 = bars + 11;
   uint64_t* c2 = bars + 12;
@@ -628,10 +628,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&fullK[i], 1);
-      mbar_init(&dkstaged[i], 256);
-    }
+    mbar_init(fullK, 1);
+    mbar_init(dkstaged, 256);
     for (int i = 4; i < 15; ++i) mbar_init(&bars[i], 1);
     mbar_init(phi_ready, 256);
     mbar_init(pt_ready, 256);
@@ -668,7 +666,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tma_prefetch_desc(&tmROWS);
       tma_prefetch_desc(&tmDV);
       const uint64_t pol = policy_evict_first();
-      int kt0 = 0, kb0 = 0, kt1 = 0, kb1 = 0;
+      int kt = 0, kb = 0;                  // coordinates of the dK tile staged in the K buffer
       int vt[2] = {0, 0}, vb[2] = {0, 0};  // coordinates of the dV tile held by each V buffer
       auto store_dv = [&](uint32_t j) {
         const int s = j & 1;
@@ -678,11 +676,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tma_store_commit();
       };
       auto store_dk = [&](uint32_t j) {
-        const int s = j & 1;
-        mbar_wait(&dkstaged[s], (j >> 1) & 1);
-        const int kt = int(s ? kt1 : kt0), kb = int(s ? kb1 : kb0);
+        mbar_wait(dkstaged, j & 1);
         for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + s * TILE + h * SUB), h * 64, kt, kb);
+          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, kt, kb);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -697,17 +693,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
               tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
             }
         }
-        const uint32_t par = (gc & 1) ^ 1;
         const int s = gc & 1;
         const int t = int(cur.t), bh = int(cur.m.bh);
-        if (gc >= 2) {
-          store_dk(gc - 2);
-          tma_store_wait_read<0>();
-        }
-        RACE_TRACE(a, 3, gc);
-        mbar_arrive_expect_tx(&fullK[s], TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + s * TILE + h * SUB, &tmK, &fullK[s], h * 64, t, bh, pol);
-        if (s) { kt1 = t; kb1 = bh; } else { kt0 = t; kb0 = bh; }
         {  // per-token rden, gden, row norms of this chunk (parity buffer s)
           uint8_t* tok = smem + OFF_TOK + s * TOK_BYTES;
           const int row = bh * int(a.N) + t;
@@ -728,13 +715,25 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&fullV[s], TILE);
         for (int h = 0; h < 2; ++h)
           tma_load_3d(smem + OFF_V + s * TILE + h * SUB, &tmV, &fullV[s], h * 64, t, bh, pol);
-        mbar_wait(emptyO, par);
+        mbar_wait(&emptyO[s], ((gc >> 1) & 1) ^ 1);
         RACE_TRACE(a, 2, gc);
-        mbar_arrive_expect_tx(fullO, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_DO + h * SUB, &tmDO, fullO, h * 64, t, bh, pol);
+        mbar_arrive_expect_tx(&fullO[s], TILE);
+        for (int h = 0; h < 2; ++h)
+          tma_load_3d(smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
+        // K last: its one buffer holds the previous chunk's dK until that is stored (K is only
+        // needed by the tangent step, late in the chunk)
+        if (gc >= 1) {
+          store_dk(gc - 1);
+          tma_store_wait_read<0>();
+        }
+        RACE_TRACE(a, 3, gc);
+        kt = t;
+        kb = bh;
+        mbar_arrive_expect_tx(fullK, TILE);
+        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dv(j);
-      for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dk(j);
+      if (gc >= 1) store_dk(gc - 1);
       tma_store_wait_all<0>();
     }
   } else if (warp == 1) {
@@ -754,14 +753,15 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       // the K tile is only needed for the sphere-tangent step and as dK staging)
       if (gc > 0) mbar_wait(dxfree, (gc - 1) & 1);  // E aliases the previous chunk's dX
       mbar_wait(&fullV[s], (gc >> 1) & 1);
-      mbar_wait(fullO, par);
+      mbar_wait(&fullO[s], (gc >> 1) & 1);
       RACE_TRACE(a, 5, gc);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           umma_bf16(tmem + TM_ZV, desc_tile_k(sb + OFF_V + s * TILE, kk), desc_w(sb + OFF_DSOPT, kk), IDC_Y, kk > 0);
-          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V + s * TILE, kk), desc_tile_k(sb + OFF_DO, kk), IDC_E, kk > 0);
+          umma_bf16(tmem + TM_E, desc_tile_k(sb + OFF_V + s * TILE, kk), desc_tile_k(sb + OFF_DO + s * TILE, kk), IDC_E,
+                    kk > 0);
         }
         umma_commit(c1);
       }
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           umma_bf16_ts(tmem + TM_Z, tmem + TM_EG + kk * 8, desc_phi_mn(sb + OFF_PHIQ, kk), IDC_Z, kk > 0);
-          umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
+          umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO + s * TILE, kk), desc_phi_mn(sb + OFF_PHIT, kk), IDC_ST, 1u);
         }
         umma_commit(c3);
       }
@@ -796,9 +796,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), IDC_DVA, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tmem + TM_DV, tmem + TM_PT + kk * 8, desc_tile_mn(sb + OFF_DO, kk), IDC_DVB, 1u);
+          umma_bf16_ts(tmem + TM_DV, tmem + TM_PT + kk * 8, desc_tile_mn(sb + OFF_DO + s * TILE, kk), IDC_DVB, 1u);
         umma_commit(cdv);
-        umma_commit(emptyO);
+        umma_commit(&emptyO[s]);
       }
       __syncwarp();
       RACE_TRACE(a, 22, gc);
@@ -1033,11 +1033,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(c4, par);
       if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
       tc_fence_after();
-      mbar_wait(&fullK[s], (gc >> 1) & 1);  // k itself is only read here (x^ of the tangent step)
-      tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K + s * TILE, r, h, sck, dotk);
+      mbar_wait(fullK, gc & 1);  // k itself is only read here (x^ of the tangent step)
+      tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K, r, h, sck, dotk);
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(&dkstaged[s]);
+      mbar_arrive(dkstaged);
       mbar_arrive(dxfree);
       if (threadIdx.x == CT0) RACE_TRACE(a, 13, gc);
     }
