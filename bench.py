@@ -171,13 +171,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # max context (BASELINE configs[2]): largest N whose fwd+bwd runs on this GPU
 # ---------------------------------------------------------------------------
-def max_context(dev, causal, dtype):
+def max_context(dev, causal, dtype, inplace=False):
     """Largest N (multiple of 2^20) whose RACE layer fwd+bwd (B=1, H=4, d=128)
     completes on one GPU with every tensor resident in HBM, and its speed.
 
-    Starts from the free-memory estimate (~8.4 KB per token in bf16: Q, K, V,
-    dO, O, dQ, dK, dV plus den / row norms / normaliser terms) and steps down
-    1 Mi tokens on each out-of-memory."""
+    allocating: Q, K, V, dO, O, dQ, dK, dV all live (~8.4 KB per token in bf16
+    with den / sketch rows / normaliser terms).  inplace: the layer as a
+    training step runs it -- O is handed on after the forward (dropped here)
+    and the backward writes dQ, dK, dV over the dead Q, K, V (race_bwd allows
+    the aliasing), so the peak is the forward's Q, K, V, dO, O (~5.7 KB per
+    token).  Starts from the free-memory estimate and steps down 1 Mi tokens
+    on each out-of-memory."""
     import torch
 
     import paper_2510_04008_b200 as rb
@@ -186,38 +190,50 @@ def max_context(dev, causal, dtype):
     w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
     p = cfg.params()
     e = 2 if dtype == torch.bfloat16 else 4
-    per_token = HEADS * (8 * DIM * e + 96)
+    per_token = HEADS * ((5 if inplace else 8) * DIM * e + (170 if inplace else 96))
     free, _ = torch.cuda.mem_get_info(dev)
     n = int(free * 0.97 / per_token) >> 20 << 20
     gen = torch.Generator(device=dev).manual_seed(7)
+
+    def step(q, k, v, g):
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        if inplace:
+            del o
+            grads = rb.race_backward(q, k, v, w, g, p, state=st, inplace=True)
+        else:
+            grads = rb.race_backward(q, k, v, w, g, p, state=st)
+            del o
+        del den, st
+        return grads
+
+    q = k = v = g = grads = None
     while n >= 1 << 20:
         tensors = []
         try:
             shape = (1, HEADS, n, DIM)
             q, k, v, g = (torch.randn(shape, generator=gen, device=dev, dtype=dtype) for _ in range(4))
             tensors = [q, k, v, g]
-            o, den, st = rb.race_forward(q, k, v, w, p)
-            dq, dk, dv = rb.race_backward(q, k, v, w, g, p, state=st)
-            del o, den, st, dq, dk, dv
+            grads = step(q, k, v, g)  # warm-up (in-place: q, k, v now hold gradients)
+            del grads
+            if inplace:
+                for t in (q, k, v):
+                    t.normal_(generator=gen)
             torch.cuda.synchronize()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             ev[0].record()
-            reps = 2
-            for _ in range(reps):
-                o, den, st = rb.race_forward(q, k, v, w, p)
-                dq, dk, dv = rb.race_backward(q, k, v, w, g, p, state=st)
-                del o, den, st, dq, dk, dv
+            grads = step(q, k, v, g)
             ev[1].record()
             torch.cuda.synchronize()
-            ms = ev[0].elapsed_time(ev[1]) / reps
-            ok = bool(torch.isfinite(q[0, 0, -1].float()).all())
-            del q, k, v, g, tensors
+            ms = ev[0].elapsed_time(ev[1])
+            ok = bool(torch.isfinite(grads[0][0, 0, -1].float()).all())
+            del q, k, v, g, tensors, grads
             torch.cuda.empty_cache()
-            return {"tokens": n, "causal": causal, "dtype": "bf16" if e == 2 else "f32", "ms_fwd_bwd": ms,
-                    "tokens_per_s": n / (ms / 1e3), "finite": ok,
-                    "hbm_gb_used_est": round(n * per_token / 1e9, 1)}
+            return {"tokens": n, "causal": causal, "dtype": "bf16" if e == 2 else "f32",
+                    "mode": "inplace" if inplace else "allocating", "ms_fwd_bwd": ms,
+                    "tokens_per_s": n / (ms / 1e3), "finite": ok, "hbm_gb_used_est": round(n * per_token / 1e9, 1)}
         except torch.cuda.OutOfMemoryError:
-            del tensors
+            q = k = v = g = grads = None
+            tensors = []
             torch.cuda.empty_cache()
             n -= 1 << 20
     return {"tokens": 0, "causal": causal, "error": "nothing fits"}
@@ -566,7 +582,8 @@ def main():
                 torch.cuda.empty_cache()
                 dev = torch.device("cuda", local_rank)
                 dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-                line["max_context"] = [max_context(dev, c, dt) for c in (True, False)]
+                line["max_context"] = [max_context(dev, c, dt) for c in (True, False)] + [
+                    max_context(dev, True, dt, inplace=True)]
                 line["scale_sweep"] = scale_sweep(dev, dt)
                 line["gpt_train_step"] = gpt_train_step(dev)
             print(json.dumps(line), flush=True)

@@ -114,7 +114,9 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k,
 
 /* Backward (ra/backward.py:184-235).  If state is NULL it is recomputed
  * from k, v exactly as race_fwd would (the reference recomputes too,
- * ra/backward.py:200).                                                    */
+ * ra/backward.py:200).  dq, dk, dv may alias q, k, v respectively
+ * (in-place backward: the inputs are dead after it, so a training step can
+ * hold 4 instead of 7 N x d tensors during the backward).                 */
 int race_bwd(const race_desc_t* desc, const void* q, const void* k,
              const void* v, const float* w, const void* d_o,
              const float* state, void* dq, void* dk, void* dv,

@@ -160,6 +160,7 @@ struct WsLayout {
   float* rden;
   float* gden;
   float* rows;     // [BH, N, 16] sketch rows when the caller has no forward state
+  void* dqtmp;     // [BH, N, d] generic causal path only: dq when it aliases q (in-place backward)
   size_t bytes;
 };
 
@@ -180,6 +181,9 @@ WsLayout ws_layout(const race::Geo& g, void* base) {
   w.rden = take(ptok);
   w.gden = take(ptok);
   w.rows = take(16 * tok);
+  // the generic causal key-side pass re-reads q after the query-side pass wrote dq
+  w.dqtmp = (g.causal && !race::tc_supported(g)) ? take((tok * g.d * (g.dtype == RACE_BF16 ? 2 : 4) + 3) / 4)
+                                                  : nullptr;
   w.bytes = off;
   return w;
 }
@@ -557,11 +561,18 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     if (int rc = cuda_status(race::tc_project(g, q, k, w, ws.rows, S(stream)), "tc_project")) return rc;
     nrm = ws.rows;
   }
-  if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, nrm, dq, ws.rden, ws.gden, ws.dpart, workspace,
+  // in-place backward (dq == q): the generic key-side pass still reads q, so dq goes through scratch
+  const bool dq_later = dq == q && ws.dqtmp;
+  void* dq1 = dq_later ? ws.dqtmp : dq;
+  if (int rc = race_bwd_causal_q(desc, q, k, v, d_o, w, tabs, nrm, dq1, ws.rden, ws.gden, ws.dpart, workspace,
                                  stream))
     return rc;
   if (int rc = race_combine(desc, RACE_COMBINE_SUFFIX, ws.dpart, nullptr, ws.dtables, stream)) return rc;
-  return race_bwd_causal_k(desc, q, k, v, d_o, w, ws.rden, ws.gden, ws.dtables, nrm, dk, dv, workspace, stream);
+  if (int rc = race_bwd_causal_k(desc, q, k, v, d_o, w, ws.rden, ws.gden, ws.dtables, nrm, dk, dv, workspace, stream))
+    return rc;
+  if (!dq_later) return RACE_OK;
+  const size_t n = size_t(g.BH * g.N) * g.d * (g.dtype == RACE_BF16 ? 2 : 4);
+  return cuda_status(cudaMemcpyAsync(dq, ws.dqtmp, n, cudaMemcpyDeviceToDevice, S(stream)), "dq copy");
 }
 
 }  // extern "C"

@@ -160,13 +160,22 @@ def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
     return o, den, state
 
 
-def race_backward(q, k, v, w, d_o, p: SketchParams, state=None):
-    """(dq, dk, dv).  ``state`` from race_forward avoids re-aggregating K/V."""
+def race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: bool = False):
+    """(dq, dk, dv).  ``state`` from race_forward avoids re-aggregating K/V.
+
+    ``inplace=True`` writes the gradients over q, k, v (which must be contiguous) and returns
+    those tensors: the inputs are dead after the backward, so the layer holds 4 instead of 7
+    N x d tensors (race_bwd allows dq, dk, dv to alias q, k, v)."""
+    if inplace and not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+        raise ValueError("inplace backward needs contiguous q, k, v")
     q, k, v, d_o = _c(q), _c(k), _c(v), _c(d_o)
     pr = Problem(q, k, v, w, p)
     if d_o.shape != v.shape or d_o.dtype != v.dtype:
         raise ValueError(f"d_out shape {tuple(d_o.shape)} does not match output shape {tuple(v.shape)}")
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    if inplace:
+        dq, dk, dv = q, k, v
+    else:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     if pr.n == 0 or pr.bh == 0:
         return dq, dk, dv
     if state is not None:

@@ -456,3 +456,29 @@ def test_table_groups_match_oracle(causal, shape):
     # the drop-in API runs the same configs (ra/acceptance.py criteria 4-5 use L up to 2048)
     out = rb.race_attention(rb.AttnInputs(q, k, v), cfg, w=wr)
     assert rel_err(out.o, o_r) <= TOL_F32
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("kind", ["fast", "generic", "groups"])
+def test_inplace_backward_matches(causal, kind):
+    """race_bwd with dq, dk, dv aliasing q, k, v gives the allocating backward's results bit for bit."""
+    dev = _cuda()
+    n = 5000
+    if kind == "fast":
+        q, k, v, g, w, p = _big(n=n, causal=causal)
+    else:
+        d = 32
+        P, L = (2, 2) if kind == "generic" else (2, 300)
+        gen = torch.Generator(device=dev).manual_seed(3)
+        q, k, v, g = (torch.randn(1, 2, n if kind == "generic" else 300, d, generator=gen, device=dev)
+                      for _ in range(4))
+        cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=1, causal=causal)
+        w = rb.head_hyperplanes(cfg, 2, d).to(dev)
+        p = cfg.params()
+    o, den, st = rb.race_forward(q, k, v, w, p)
+    ref = rb.race_backward(q, k, v, w, g, p, state=st)
+    qc, kc, vc = q.clone(), k.clone(), v.clone()
+    got = rb.race_backward(qc, kc, vc, w, g, p, state=st, inplace=True)
+    assert got[0].data_ptr() == qc.data_ptr() and got[2].data_ptr() == vc.data_ptr()
+    for a, b in zip(got, ref):
+        assert torch.equal(a, b)
