@@ -209,12 +209,14 @@ using agg::OFF_STAGE;
 using agg::OFF_W;
 using agg::OFF_PHI;
 constexpr int OFF_BAR = agg::OFF_BAR;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int OFF_XS = OFF_BAR + 256;  // [2 segment parities][8 warps][FP] phi column sums
+constexpr int SMEM = OFF_XS + 2 * 8 * FP * 4 + 1024;
+static_assert(SMEM <= 232448, "k_aggregate2 shared memory");
 constexpr uint32_t TM_PK = 0, TM_ACC = 32;  // accumulators at 32 and 64
 }  // namespace agg2
 
 template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS8, 1)
     k_aggregate2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   using namespace agg2;
   extern __shared__ uint8_t smem_raw[];
@@ -223,26 +225,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* full = bars;               // [STAGES]
   uint64_t* empty = bars + STAGES;     // [STAGES]
-  uint64_t* proj_full = bars + 2 * STAGES;
-  uint64_t* phi_full = proj_full + 1;
-  uint64_t* phi_empty = phi_full + 1;  // [2]
+  uint64_t* proj_full = bars + 2 * STAGES;  // [2] projections of chunk g in TM_PK + 16 (g & 1)
+  uint64_t* phi_full = proj_full + 2;  // [2] (128 arrivals: the warp group owning the chunk)
+  uint64_t* phi_empty = phi_full + 2;  // [2]
   uint64_t* wready = phi_empty + 2;
   uint64_t* acc_full = wready + 1;     // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
+  uint64_t* pk_empty = acc_empty + 2;  // [2] projection buffer read (128 arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pk_empty + 2);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(proj_full, 1);
-    mbar_init(phi_full, 128);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&phi_full[i], 128);
+      mbar_init(&proj_full[i], 1);
       mbar_init(&phi_empty[i], 1);
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 128);
+      mbar_init(&pk_empty[i], 128);
     }
-    mbar_init(wready, 128);
+    mbar_init(wready, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<128>(tslot);
@@ -272,31 +275,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    uint32_t gc = 0, nr = 0, ns = 0;
-    int prev_bh = -1;
-    for (int64_t it = i0; it < i1; ++it, ++ns) {
-      const Item m = item_of(a, it);
-      if (m.bh != prev_bh) {
-        prev_bh = m.bh;
+    // The projection of chunk g + 1 is issued before the state MMA of chunk g waits for phi (two
+    // TMEM projection buffers), so the compute warps find it ready; never across a sequence
+    // change, where W' is rebuilt by the compute warps.
+    uint32_t gc = 0, nr = 0, ns = 0, pg = 0;
+    int pbh = -1;
+    Cursor pc;
+    pc.start(a, i0, i1);
+    auto issue_proj = [&]() {  // projection of chunk pg (cursor pc)
+      if (pc.m.bh != pbh) {
+        pbh = pc.m.bh;
         mbar_wait(wready, nr & 1);
         ++nr;
       }
+      const int s = pg % STAGES;
+      mbar_wait(&full[s], (pg / STAGES) & 1);
+      if (pg >= 2) mbar_wait(&pk_empty[pg & 1], ((pg >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_PK + 16 * (pg & 1), desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
+        umma_commit(&proj_full[pg & 1]);
+      }
+      __syncwarp();
+      pc.next(a);
+      ++pg;
+    };
+    for (int64_t it = i0; it < i1; ++it, ++ns) {
+      const Item m = item_of(a, it);
       if (ns >= 2) mbar_wait(&acc_empty[ns & 1], ((ns >> 1) - 1) & 1);  // segment ns - 2 read out
       tc_fence_after();
       const uint32_t acc = tmem + TM_ACC + 32 * (ns & 1);
       for (int t = m.t0; t < m.t1; t += CH, ++gc) {
         const int s = gc % STAGES;
         const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc / STAGES) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_PK, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          umma_commit(proj_full);
-        }
-        __syncwarp();
-        mbar_wait(phi_full, gc & 1);
+        if (pg == gc) issue_proj();                              // this chunk (first, or new sequence)
+        if (pc.ok() && pc.m.bh == int64_t(m.bh)) issue_proj();  // the next one, same sequence
+        mbar_wait(&phi_full[gc & 1], (gc >> 1) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
@@ -312,15 +329,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
+    // 8 compute warps in two groups: warps 2-5 take the even chunks, warps 6-9 the odd ones, so
+    // one group's features overlap the other's waits (each SMSP holds one warp of each group)
     const int r = crow();
+    const int grp = chalf();
     const int F = a.T << a.P;
+    float* xs = reinterpret_cast<float*>(smem + OFF_XS);
     uint32_t gc = 0, ns = 0;
     int prev_bh = -1;
     for (int64_t it = i0; it < i1; ++it, ++ns) {
       const Item m = item_of(a, it);
       if (m.bh != prev_bh) {
         prev_bh = m.bh;
-        build_wop(a, m.bh, sb + OFF_W);
+        build_wop<256, CT0>(a, m.bh, sb + OFF_W);
         fence_proxy_async();
         mbar_arrive(wready);
       }
@@ -328,16 +349,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int f = 0; f < FP; ++f) asum[f] = 0.f;
       for (int t = m.t0; t < m.t1; t += CH, ++gc) {
+        if (int(gc & 1) != grp) continue;
         const int s = gc % STAGES;
         const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
         mbar_wait(&full[s], (gc / STAGES) & 1);
         const float sumsq = tile_row_sumsq(stage, r);
         const float inv = inv_scale(sumsq, a.normalize);
-        mbar_wait(proj_full, gc & 1);
+        mbar_wait(&proj_full[gc & 1], (gc >> 1) & 1);
         tc_fence_after();
         float proj[16];
-        tmem_ld16(tmem + lane_base() + TM_PK, proj);
+        tmem_ld16(tmem + lane_base() + TM_PK + 16 * (gc & 1), proj);
         tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&pk_empty[gc & 1]);
         float phi[FP];
         row_features<P>(a, proj, inv, t + r < m.t1, phi);
 #pragma unroll
@@ -346,29 +370,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         write_phi_k(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(phi_full);
+        mbar_arrive(&phi_full[gc & 1]);
         if (a.rows_out && t + r < m.t1) {  // causal: the k half of this key's sketch row (off the MMA chain)
           float hat[5];
           row_hat(a, proj, inv, hat);
           store_row_half(a.rows_out + (int64_t(m.bh) * a.N + t + r) * ROWW + 8, hat, sumsq);
         }
       }
-      // segment done: S^T (lane r = value column r) from its TMEM buffer, A by a block sum
-      mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
-      tc_fence_after();
-      float acc[32];
-      tmem_ld32(tmem + lane_base() + TM_ACC + 32 * (ns & 1), acc);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&acc_empty[ns & 1]);
-      csum8(asum, scratch);
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      // segment done: phi column sums of both groups (fixed order), S^T (lane r = value column r)
+      // from its TMEM buffer read out by group 0
+      float* xp = xs + (ns & 1) * 8 * FP;
 #pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+      for (int f = 0; f < FP; ++f) {
 #pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F && r == f) out[f * LDS_T + DH] = asum[f];
+        for (int o = 16; o > 0; o >>= 1) asum[f] += __shfl_xor_sync(0xffffffffu, asum[f], o);
+      }
+      if (lane_id() == 0) {
+#pragma unroll
+        for (int f = 0; f < FP; ++f) xp[(warp - 2) * FP + f] = asum[f];
+      }
+      compute_bar256();
+      if (grp == 0) {
+        mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
+        tc_fence_after();
+        float acc[32];
+        tmem_ld32(tmem + lane_base() + TM_ACC + 32 * (ns & 1), acc);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&acc_empty[ns & 1]);
+        float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+#pragma unroll
+        for (int f = 0; f < FP; ++f)
+          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+        if (r < F) {
+          float tot = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) tot += xp[w * FP + r];
+          out[r * LDS_T + DH] = tot;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -1390,9 +1430,9 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
   const char* v1 = getenv("RACE_AGG_V1");
   if (!(v1 && v1[0] == '1')) {
     switch (g.P) {
-      case 1: return launch(k_aggregate2<1>, agg2::SMEM, grid_for(g), st, mk, mv, a);
-      case 2: return launch(k_aggregate2<2>, agg2::SMEM, grid_for(g), st, mk, mv, a);
-      default: return launch(k_aggregate2<3>, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      default: return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
     }
   }
   switch (g.P) {
