@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* acc_empty = bars + 23;
   uint64_t* dp_ready = bars + 24;  // dproj staged (256 arrivals)
   uint64_t* c4 = bars + 25;        // dx^ MMA
+  uint64_t* dsdone = bars + 12;    // dS MMAs (after dx^) done: phi_q / D buffer free
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = warp_id();
@@ -260,27 +261,29 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         __syncwarp();
         mbar_wait(et_ready, par);
         RACE_TRACE(a, 7, gc);
-        if (first && ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);  // dS of the previous segment read out
         tc_fence_after();
-        if (elect_one()) {
+        if (elect_one()) {  // Z (dphi_q's intra-chunk term): on the dq-critical path
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
+          for (int kk = 0; kk < 8; ++kk)
             umma_bf16_ts(tmem + TM_Z, tmem + TM_ET + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
-            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO + s * TILE, kk), desc_phi_mn(sb + OFF_PHIQ, kk), IDC_ST,
-                      (!first || kk > 0) ? 1u : 0u);
-          }
           umma_commit(c3);
-          umma_commit(&emptyO[s]);
-          if (t + CH >= m.t1) umma_commit(acc_full);
         }
         __syncwarp();
         mbar_wait(dp_ready, par);
         RACE_TRACE(a, 8, gc);
+        if (first && ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);  // dS of the previous segment read out
         tc_fence_after();
         if (elect_one()) {  // dx^ = dproj . W (hi and lo halves of dproj against W' read MN-major)
           umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIK, 0), desc_wT(sb + OFF_W), IDC_DX, 0u);
           umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIK, 1), desc_wT(sb + OFF_W), IDC_DX, 1u);
           umma_commit(c4);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // the segment's dS total, off the critical path
+            umma_bf16(tmem + TM_DS, desc_tile_mn(sb + OFF_DO + s * TILE, kk), desc_phi_mn(sb + OFF_PHIQ, kk), IDC_ST,
+                      (!first || kk > 0) ? 1u : 0u);
+          umma_commit(&emptyO[s]);
+          umma_commit(dsdone);
+          if (t + CH >= m.t1) umma_commit(acc_full);
         }
         __syncwarp();
         // the next chunk's front MMAs, unless it starts a new sequence (then W' changes first)
@@ -501,6 +504,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
         if (threadIdx.x == 64) RACE_TRACE(a, 13, gc);
+        mbar_wait(dsdone, par);  // the dS MMA has read phi_q / D: the next chunk may overwrite it
       }
       // ---- segment done: dS total (TMEM) and dA total (block reduction)
       mbar_wait(acc_full, ni & 1);
