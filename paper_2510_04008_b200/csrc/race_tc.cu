@@ -889,7 +889,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* pt_full = bars + 11;
   uint64_t* num_full = bars + 12;
   uint64_t* wready = bars + 13;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* st_full = bars + 14;  // state MMA S += V^T phi_k done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = warp_id();
   if (threadIdx.x == 0) {
@@ -904,6 +905,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     mbar_init(pm_full, 1);
     mbar_init(pt_full, 256);
     mbar_init(num_full, 1);
+    mbar_init(st_full, 1);
     mbar_init(wready, 256);
     fence_barrier_init();
   }
@@ -1007,6 +1009,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk)
             umma_bf16(tmem + TM_PM, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), ID_PM, kk > 0);
+          umma_commit(pm_full);  // P~ staging needs only Pm; the state update runs behind it
         }
         __syncwarp();
         mbar_wait(&fullv[s], (gc >> 1) & 1);
@@ -1015,7 +1018,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + 2 * TILE, kk), desc_phi_mn(sb + OFF_PHIK, kk), ID_STATE, 1u);
-          umma_commit(pm_full);
+          umma_commit(st_full);
         }
         __syncwarp();
         mbar_wait(pt_full, gc & 1);
@@ -1193,16 +1196,18 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
       }
       xpar[256 + h * 128 + r] = rs;
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(pt_full);
       if (h == 1) {
+        mbar_wait(st_full, gc & 1);
+        tc_fence_after();
         float sacc[32];
         tmem_ld32(tmem + lb + TM_SACC, sacc);  // S_<=c (value column r)
         tmem_ld_wait();
 #pragma unroll
         for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
       }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(pt_full);
       // ---- while the numerator MMA runs: row norms of the next chunk
       cur.next(a);
       if (cur.ok()) {
