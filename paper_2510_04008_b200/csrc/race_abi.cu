@@ -513,8 +513,7 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   }
   WsLayout ws = ws_layout(g, workspace);
   float* tabs = state ? state : ws.tables;
-  static const bool no_krows = getenv("RACE_NO_KROWS") != nullptr;  // A/B diagnostic
-  if (g.causal && !no_krows) {
+  if (g.causal) {
     // the aggregation also writes the k halves of the sketch rows, so the scan reads Q, V and those rows
     float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : ws.rows;
     if (int rc = race_kside_partials_rows(desc, k, v, w, ws.part, nrm, workspace, stream)) return rc;
@@ -522,11 +521,6 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     return race_fwd_causal_krows(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
   }
   if (int rc = race_kside_partials(desc, k, v, w, ws.part, workspace, stream)) return rc;
-  if (g.causal) {
-    if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
-    float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
-    return race_fwd_causal(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
-  }
   if (int rc = race_combine(desc, RACE_COMBINE_TOTAL, ws.part, nullptr, tabs, stream)) return rc;
   return race_fwd_readout(desc, q, w, tabs, o, den, workspace, stream);
 }

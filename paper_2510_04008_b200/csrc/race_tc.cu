@@ -41,159 +41,6 @@ constexpr int OFF_BAR = OFF_PHI + 2 * PHI;
 constexpr int SMEM = OFF_BAR + 256 + 1024;   // + alignment slack
 }  // namespace agg
 
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_aggregate(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
-  using namespace agg;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;               // [STAGES]
-  uint64_t* empty = bars + STAGES;     // [STAGES]
-  uint64_t* proj_full = bars + 2 * STAGES;
-  uint64_t* phi_full = proj_full + 1;
-  uint64_t* phi_empty = phi_full + 1;  // [2]
-  uint64_t* wready = phi_empty + 2;
-  uint64_t* acc_full = wready + 1;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(proj_full, 1);
-    mbar_init(phi_full, 128);
-    mbar_init(&phi_empty[0], 1);
-    mbar_init(&phi_empty[1], 1);
-    mbar_init(wready, 128);
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<64>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-
-  if (warp == 0) {
-    // ------------------------------ TMA producer
-    if (elect_one()) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const int s = gc % STAGES;
-          const uint32_t u = gc / STAGES;
-          mbar_wait(&empty[s], (u & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
-          for (int h = 0; h < 2; ++h) {
-            tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, int(t), int(m.bh), pol);
-            tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, int(t), int(m.bh), pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------ MMA issuer
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
-      tc_fence_after();
-      bool first = true;
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc % STAGES;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc / STAGES) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_PROJK, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          umma_commit(proj_full);
-        }
-        __syncwarp();
-        mbar_wait(phi_full, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_SACC, desc_tile_mn(stage + TILE, kk), desc_phi_mn(phib, kk), ID_STATE,
-                      (!first || kk > 0) ? 1u : 0u);
-          umma_commit(&empty[s]);
-          umma_commit(&phi_empty[gc & 1]);
-          if (t + CH >= m.t1) umma_commit(acc_full);
-        }
-        __syncwarp();
-        first = false;
-      }
-    }
-  } else {
-    // ------------------------------ compute warps
-    const int r = crow();
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      build_wop(a, m.bh, sb + OFF_W);
-      fence_proxy_async();
-      mbar_arrive(wready);
-      float asum[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) asum[f] = 0.f;
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc % STAGES;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc / STAGES) & 1);
-        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
-        mbar_wait(proj_full, gc & 1);
-        tc_fence_after();
-        float proj[16];
-        tmem_ld16(tmem + lane_base() + TM_PROJK, proj);
-        tmem_ld_wait();
-        float phi[FP];
-        row_features<P>(a, proj, inv, t + r < m.t1, phi);
-#pragma unroll
-        for (int f = 0; f < FP; ++f) asum[f] += phi[f];
-        if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
-        write_phi_k(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(phi_full);
-      }
-      // item done: read S^T (lane r = value column r) and write the partial table
-      mbar_wait(acc_full, ni & 1);
-      tc_fence_after();
-      float acc[32];
-      tmem_ld32(tmem + lane_base() + TM_SACC, acc);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(acc_empty);
-      csum8(asum, scratch);
-      const int F = a.T << a.P;
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F && r == f) out[f * LDS_T + DH] = asum[f];
-      // bump past the phi_empty phases consumed by this item's last chunks (tracked via gc)
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<64>(tmem);
-}
 
 // ---------------------------------------------------------------------------
 // K1, contiguous-range version (the one launched).  Each CTA walks a
@@ -430,161 +277,6 @@ constexpr int OFF_BAR = OFF_SOP + PHI;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace rdo
 
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_readout(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
-  using namespace rdo;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* proj_full = bars + 2 * STAGES;
-  uint64_t* phi_full = proj_full + 1;
-  uint64_t* phi_empty = phi_full + 1;  // [2]
-  uint64_t* wready = phi_empty + 2;
-  uint64_t* num_full = wready + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(num_full + 1);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(proj_full, 1);
-    mbar_init(phi_full, 128);
-    mbar_init(&phi_empty[0], 1);
-    mbar_init(&phi_empty[1], 1);
-    mbar_init(wready, 128);
-    mbar_init(num_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<256>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-  constexpr uint32_t TM_NUM_R = 128;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmO);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const int s = gc % STAGES;
-          mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
-          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, int(t), int(m.bh), pol);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      tc_fence_after();
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc % STAGES;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc / STAGES) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_PROJQ, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-          umma_commit(proj_full);
-        }
-        __syncwarp();
-        mbar_wait(phi_full, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t phib = sb + OFF_PHI + (gc & 1) * PHI;
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_NUM_R, desc_phi_k(phib, kk), desc_phi_k(sb + OFF_SOP, kk), ID_NUMA, kk > 0);
-          umma_commit(num_full);
-          umma_commit(&phi_empty[gc & 1]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int r = crow();
-    const float invT = 1.f / float(a.T);
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const int F = a.T << a.P;
-      const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
-      // previous item's last num read is complete (program order); rebuild W' and S operand
-      build_wop(a, m.bh, sb + OFF_W);
-      float srow[FP], A[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        srow[f] = f < F ? tab[f * LDS_T + r] : 0.f;
-        A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
-      }
-      write_sop(sb + OFF_SOP, r, srow);
-      fence_proxy_async();
-      mbar_arrive(wready);
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc % STAGES;
-        const uint32_t stage = sb + OFF_STAGE + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc / STAGES) & 1);
-        const float inv = inv_scale(tile_row_sumsq(stage, r), a.normalize);
-        mbar_wait(proj_full, gc & 1);
-        tc_fence_after();
-        float proj[16];
-        tmem_ld16(tmem + lane_base() + TM_PROJQ, proj);
-        tmem_ld_wait();
-        const bool valid = t + r < m.t1;
-        float phi[FP];
-        row_features<P>(a, proj, inv, valid, phi);
-        float D = 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
-        if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
-        write_phi_q(sb + OFF_PHI + (gc & 1) * PHI, r, phi);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(phi_full);
-        if (valid) a.den[m.bh * a.N + t + r] = D * invT;
-        const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
-        mbar_wait(num_full, gc & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base() + TM_NUM_R + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= rD;
-          stage_row_bf16(stage, r, v, c0);  // Q tile is dead: reuse as O staging
-        }
-        tc_fence_before();
-        fence_proxy_async();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          for (int h = 0; h < 2; ++h) tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + h * SUB),
-                                                  h * 64, int(t), int(m.bh));
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          mbar_arrive(&empty[s]);
-        }
-      }
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
-}
 
 // ---------------------------------------------------------------------------
 // K2, 8-compute-warp contiguous-range version (the one launched): W' and the
@@ -1432,18 +1124,10 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
   a.w = w;
   a.tout = part;
   a.rows_out = rows;
-  const char* v1 = getenv("RACE_AGG_V1");
-  if (!(v1 && v1[0] == '1')) {
-    switch (g.P) {
-      case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
-      case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
-      default: return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
-    }
-  }
   switch (g.P) {
-    case 1: return launch(k_aggregate<1>, agg::SMEM, grid_for(g), st, mk, mv, a);
-    case 2: return launch(k_aggregate<2>, agg::SMEM, grid_for(g), st, mk, mv, a);
-    default: return launch(k_aggregate<3>, agg::SMEM, grid_for(g), st, mk, mv, a);
+    case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+    case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+    default: return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
   }
 }
 
@@ -1456,18 +1140,10 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
   a.w = w;
   a.tin = tab;
   a.den = den;
-  const char* v1 = getenv("RACE_RDO_V1");
-  if (!(v1 && v1[0] == '1')) {
-    switch (g.P) {
-      case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
-      case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
-      default: return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
-    }
-  }
   switch (g.P) {
-    case 1: return launch(k_readout<1>, rdo::SMEM, grid_for(g), st, mq, mo, a);
-    case 2: return launch(k_readout<2>, rdo::SMEM, grid_for(g), st, mq, mo, a);
-    default: return launch(k_readout<3>, rdo::SMEM, grid_for(g), st, mq, mo, a);
+    case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+    case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+    default: return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
   }
 }
 

@@ -37,200 +37,6 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;
 }  // namespace bq
 
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_bwd_q(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
-            const __grid_constant__ CUtensorMap tmDQ, Args a) {
-  using namespace bq;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;          // [2]
-  uint64_t* empty = bars + 2;     // [2]: MMA (dO consumed) + store drained (Q/dQ tile)
-  uint64_t* c1 = bars + 4;        // proj + y ready
-  uint64_t* ready = bars + 5;     // threads wrote Phi~ and dProj
-  uint64_t* c2 = bars + 6;        // dS += ..., dx^ ready
-  uint64_t* wready = bars + 7;
-  uint64_t* acc_full = bars + 8;
-  uint64_t* acc_empty = bars + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
-  float* scratch = reinterpret_cast<float*>(tslot + 4);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 2); }
-    mbar_init(c1, 1);
-    mbar_init(ready, 128);
-    mbar_init(c2, 1);
-    mbar_init(wready, 128);
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<256>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmDO);
-      tma_prefetch_desc(&tmDQ);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const int s = gc & 1;
-          mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          uint8_t* st = smem + s * STAGE_BYTES;
-          for (int h = 0; h < 2; ++h) {
-            tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, int(t), int(m.bh), pol);
-            tma_load_3d(st + TILE + h * SUB, &tmDO, &full[s], h * 64, int(t), int(m.bh), pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      if (ni > 0) mbar_wait(acc_empty, (ni - 1) & 1);
-      tc_fence_after();
-      bool first = true;
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_P, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_Y, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_SOPT, kk), ID_Y, kk > 0);
-          }
-          umma_commit(c1);
-        }
-        __syncwarp();
-        mbar_wait(ready, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_DS, desc_tile_mn(stage + TILE, kk), desc_phi_mn(sb + OFF_PHIT, kk), ID_DS,
-                      (!first || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), ID_DX, kk > 0);
-          umma_commit(c2);
-          umma_commit(&empty[s]);
-          if (t + CH >= m.t1) umma_commit(acc_full);
-        }
-        __syncwarp();
-        first = false;
-      }
-    }
-  } else {
-    const int r = crow();
-    const float invT = 1.f / float(a.T);
-    const int F = a.T << a.P;
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
-      build_wop(a, m.bh, sb + OFF_W);
-      build_w2(a, m.bh, sb + OFF_W2);
-      float scol[FP], A[FP], dA[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        scol[f] = f < F ? tab[f * LDS_T + r] : 0.f;
-        A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
-        dA[f] = 0.f;
-      }
-      write_sopT(sb + OFF_SOPT, r, scol);
-      fence_proxy_async();
-      mbar_arrive(wready);
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        const Scale sc = row_scale(tile_row_sumsq(stage, r), a.normalize);
-        const bool valid = t + r < m.t1;
-        mbar_wait(c1, gc & 1);
-        tc_fence_after();
-        float proj[16], yv[16];
-        tmem_ld16(tmem + lane_base() + TM_P, proj);
-        tmem_ld16(tmem + lane_base() + TM_Y, yv);
-        tmem_ld_wait();
-        float phi[FP], u[5], ph[5];
-        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
-        float y[FP], D = 0.f, num = 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          y[f] = yv[f] + yv[8 + f];
-          D = fmaf(phi[f], A[f], D);
-          num = fmaf(phi[f], y[f], num);
-        }
-        const bool live = valid && D * invT > kDegenerateDenEps;
-        const float rD = live ? 1.f / D : 0.f;
-        const float rho = num * rD;
-        float dphi[FP], phit[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          dphi[f] = (y[f] - rho * A[f]) * rD;
-          phit[f] = phi[f] * rD;
-          dA[f] = fmaf(phi[f], -rho * rD, dA[f]);
-        }
-        float dproj[8];
-        row_feature_vjp<P>(a, u, phi, dphi, dproj);
-        write_phi_k(sb + OFF_PHIT, r, phit);  // [hi | hi | lo | 0]: MN-major B of dS += dO^T Phi~
-        write_dproj(sb + OFF_DPROJ, r, dproj);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(ready);
-        mbar_wait(c2, gc & 1);
-        tc_fence_after();
-        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc, dot_from_proj(dproj, ph));
-        tc_fence_before();
-        fence_proxy_async();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, int(t), int(m.bh));
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          mbar_arrive(&empty[s]);
-        }
-      }
-      // item done: partial dS (lane r = value column r) and dA
-      mbar_wait(acc_full, ni & 1);
-      tc_fence_after();
-      float acc[32];
-      tmem_ld32(tmem + lane_base() + TM_DS, acc);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(acc_empty);
-      csum8(dA, scratch);
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
-#pragma unroll
-      for (int f = 0; f < FP; ++f)
-        if (f < F && r == f) out[f * LDS_T + DH] = dA[f];
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
-}
 
 // ===========================================================================
 // bwd key side (non-causal)
@@ -249,165 +55,6 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Z = 16, TM_DV = 128, TM_DX = 256;
 }  // namespace bk
 
-template <int P>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_bwd_k(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-            const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a) {
-  using namespace bk;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  uint64_t* c1 = bars + 4;
-  uint64_t* ready = bars + 5;
-  uint64_t* c2 = bars + 6;
-  uint64_t* wready = bars + 7;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
-
-  const int warp = warp_id();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(c1, 1);
-    mbar_init(ready, 128);
-    mbar_init(c2, 1);
-    mbar_init(wready, 128);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const int64_t nitems = a.BH * a.nseg;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      const uint64_t pol = policy_evict_first();
-      uint32_t gc = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item m = item_of(a, it);
-        for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-          const int s = gc & 1;
-          mbar_wait(&empty[s], ((gc >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          uint8_t* st = smem + s * STAGE_BYTES;
-          for (int h = 0; h < 2; ++h) {
-            tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, int(t), int(m.bh), pol);
-            tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, int(t), int(m.bh), pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      mbar_wait(wready, ni & 1);
-      tc_fence_after();
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + TM_P, desc_tile_k(stage, kk), desc_w(sb + OFF_W, kk), ID_PROJ, kk > 0);
-            umma_bf16(tmem + TM_Z, desc_tile_k(stage + TILE, kk), desc_w(sb + OFF_DSOPT, kk), ID_Y, kk > 0);
-          }
-          umma_commit(c1);
-        }
-        __syncwarp();
-        mbar_wait(ready, gc & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            umma_bf16(tmem + TM_DV, desc_phi_k(sb + OFF_PHIK, kk), desc_phi_k(sb + OFF_DSOP, kk), ID_DV, kk > 0);
-            umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_DPROJ, kk), desc_w2(sb + OFF_W2, kk), ID_DX, kk > 0);
-          }
-          umma_commit(c2);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int r = crow();
-    const int F = a.T << a.P;
-    uint32_t gc = 0, ni = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ni) {
-      const Item m = item_of(a, it);
-      const float* dtab = a.tin + m.bh * int64_t(F) * LDS_T;
-      build_wop(a, m.bh, sb + OFF_W);
-      build_w2(a, m.bh, sb + OFF_W2);
-      float dcol[FP], dA[FP];
-#pragma unroll
-      for (int f = 0; f < FP; ++f) {
-        dcol[f] = f < F ? dtab[f * LDS_T + r] : 0.f;
-        dA[f] = f < F ? dtab[f * LDS_T + DH] : 0.f;
-      }
-      write_sopT(sb + OFF_DSOPT, r, dcol);
-      write_sop(sb + OFF_DSOP, r, dcol);
-      fence_proxy_async();
-      mbar_arrive(wready);
-      for (int64_t t = m.t0; t < m.t1; t += CH, ++gc) {
-        const int s = gc & 1;
-        const uint32_t stage = sb + s * STAGE_BYTES;
-        mbar_wait(&full[s], (gc >> 1) & 1);
-        const Scale sc = row_scale(tile_row_sumsq(stage, r), a.normalize);
-        const bool valid = t + r < m.t1;
-        mbar_wait(c1, gc & 1);
-        tc_fence_after();
-        float proj[16], zv[16];
-        tmem_ld16(tmem + lane_base() + TM_P, proj);
-        tmem_ld16(tmem + lane_base() + TM_Z, zv);
-        tmem_ld_wait();
-        float phi[FP], u[5], ph[5], dphi[FP];
-        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
-#pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
-        float dproj[8];
-        row_feature_vjp<P>(a, u, phi, dphi, dproj);
-        write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
-        write_dproj(sb + OFF_DPROJ, r, dproj);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(ready);
-        mbar_wait(c2, gc & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base() + TM_DV + c0, v);
-          tmem_ld_wait();
-          stage_row_bf16(stage + TILE, r, v, c0);  // dV over the dead V row
-        }
-        tangent_row_inplace(tmem + lane_base() + TM_DX, stage, r, sc, dot_from_proj(dproj, ph));
-        tc_fence_before();
-        fence_proxy_async();
-        compute_bar();
-        if (threadIdx.x == 64) {
-          for (int h = 0; h < 2; ++h) {
-            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, int(t), int(m.bh));
-            tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + s * STAGE_BYTES + TILE + h * SUB), h * 64, int(t),
-                         int(m.bh));
-          }
-          tma_store_commit();
-          tma_store_wait_read<0>();
-          mbar_arrive(&empty[s]);
-        }
-      }
-    }
-    if (threadIdx.x == 64) tma_store_wait_all<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
 
 // ===========================================================================
 // Non-causal backward, 8-compute-warp contiguous-range versions (launched).
@@ -892,18 +539,10 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   a.w = w;
   a.tin = tab;
   a.tout = dpart;
-  const char* v1 = getenv("RACE_BWDNC_V1");
-  if (!(v1 && v1[0] == '1')) {
-    switch (g.P) {
-      case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-      case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-      default: return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-    }
-  }
   switch (g.P) {
-    case 1: return launch(k_bwd_q<1>, bq::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-    case 2: return launch(k_bwd_q<2>, bq::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-    default: return launch(k_bwd_q<3>, bq::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    default: return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
   }
 }
 
@@ -916,18 +555,10 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
   Args a = make_args(g);
   a.w = w;
   a.tin = dtab;
-  const char* v1 = getenv("RACE_BWDNC_V1");
-  if (!(v1 && v1[0] == '1')) {
-    switch (g.P) {
-      case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-      case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-      default: return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-    }
-  }
   switch (g.P) {
-    case 1: return launch(k_bwd_k<1>, bk::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-    case 2: return launch(k_bwd_k<2>, bk::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-    default: return launch(k_bwd_k<3>, bk::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    default: return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
   }
 }
 
