@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const bool valid = t + r < m.t1;
       if (m.bh != prev_bh) {  // (re)load the sequence state: W', S_in (TMEM + S operand), A_in
         prev_bh = m.bh;
-        if (threadIdx.x == CT0) RACE_TRACE(a, 10, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 10, gc);
         const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
         float srow[FP];
 #pragma unroll
@@ -803,12 +803,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(wready);
-        if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
       }
       const float invq = inv_scale(sqq, a.normalize);
       const float invk = inv_scale(sqk, a.normalize);
       mbar_wait(proj_full, gc & 1);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 5, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 5, gc);
       tc_fence_after();
       float phq[FP];
       if (h == 0) {
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
       // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 pairs into TMEM (my 64 columns)
       mbar_wait(pm_full, gc & 1);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 6, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 6, gc);
       tc_fence_after();
       float rs = 0.f;
 #pragma unroll
@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
       // ---- numerator -> O (my 64 columns, staged in the consumed V tile), next S operand
       mbar_wait(num_full, gc & 1);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 7, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 7, gc);
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&ostaged[s]);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 8, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 8, gc);
     }
   }
   tc_fence_before();

@@ -53,6 +53,7 @@ struct Args {
   const float* rows_in;  // [BH, N, ROWW] sketch rows saved by the causal forward (see ROWW)
   float* rows_out;
   int pf;               // chunks of L2 prefetch (cp.async.bulk.prefetch) ahead of the TMA loads
+  int ttid;             // compute thread that records the per-chunk trace (RACE_TRACE_TID, default 64)
 };
 
 #define RACE_DBG(a_, slot_, val_)                                                        \
@@ -975,6 +976,8 @@ inline Args make_args(const Geo& g) {
   a.w_per_head = g.w_per_head;
   const char* pf = getenv("RACE_PF");  // tuning knob, off by default
   a.pf = pf && pf[0] ? atoi(pf) : 0;  // measured: L2 prefetch slows every kernel here (r01)
+  const char* tt = getenv("RACE_TRACE_TID");
+  a.ttid = tt && tt[0] ? atoi(tt) : 64;
   return a;
 }
 
