@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         const Scale scq = row_scale(valid ? trow[7] : 0.f, a.normalize);
         mbar_arrive(&emptyT[s]);
-        if (threadIdx.x == 64) RACE_TRACE(a, 9, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 9, gc);
         float phq[FP], uq[5];
         if (h == 0) {
           row_features_hat<P>(a, hq, valid, phq, uq);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- row statistics from Pm and E over my 64 columns
         mbar_wait(c2, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 10, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 10, gc);
         tc_fence_after();
         float rs = 0.f, nd = 0.f;
 #pragma unroll
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         // ---- dphi_q -> dproj
         mbar_wait(c3, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 11, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
         tc_fence_after();
         float zz[32];
         tmem_ld32(tmem + lb + TM_Z, zz);
@@ -496,14 +496,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive(dp_ready);
         // ---- dq (my 64 columns) in place of q; the producer stores it
         mbar_wait(c4, par);
-        if (threadIdx.x == 64) RACE_TRACE(a, 12, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 12, gc);
         tc_fence_after();
         mbar_wait(&fullQ[s], (gc >> 1) & 1);  // q itself is only read here (x^ of the tangent step)
         tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
-        if (threadIdx.x == 64) RACE_TRACE(a, 13, gc);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 13, gc);
         mbar_wait(dsdone, par);  // the dS MMA has read phi_q / D: the next chunk may overwrite it
       }
       // ---- segment done: dS total (TMEM) and dA total (block reduction)
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         hk[j] = trow[8 + j];
       }
       const Scale sck = row_scale(valid ? trow[15] : 0.f, a.normalize);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 9, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 9, gc);
       float phq[FP], uq[5], phk[FP], uk[5];
       {
         if (h == 0) {
@@ -925,9 +925,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           row_features_hat<P>(a, hk, valid, phk, uk);  // for dk (off the MMA path)
         }
       }
-      if (threadIdx.x == CT0) RACE_TRACE(a, 24, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 24, gc);
       compute_bar256();  // rd / gd of every query token, dA partials
-      if (threadIdx.x == CT0) RACE_TRACE(a, 25, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 25, gc);
       // ---- EG~ = (E^T rd + gd) masked t >= i, my 64 columns -> TMEM A operand of Z
       mbar_wait(c1, par);
       tc_fence_after();
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(eg_ready);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 26, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 26, gc);
       // ---- P~^T = Pm^T rd masked t >= i -> TMEM A operand of dV
       mbar_wait(c2, par);
       tc_fence_after();
@@ -985,10 +985,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(pt_ready);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 27, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 27, gc);
       // ---- dphi_k -> dproj (Z and the dS update are done at c3)
       mbar_wait(c3, par);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 11, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
       tc_fence_after();
       float zz[32], zv[16];
       tmem_ld32(tmem + lb + TM_Z, zz);
@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dp_ready);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 28, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 28, gc);
 #pragma unroll
       for (int f = 0; f < FP; ++f)
         dA[f] += ((xpar[256 + f] + xpar[256 + FP + f]) + xpar[256 + 2 * FP + f]) + xpar[256 + 3 * FP + f];
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       cur.next(a);
       // ---- dk (my 64 columns) in place of k; the producer stores it
       mbar_wait(c4, par);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 12, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 12, gc);
       tc_fence_after();
       mbar_wait(fullK, gc & 1);  // k itself is only read here (x^ of the tangent step)
       tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K, r, h, sck, dotk);
@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tc_fence_before();
       mbar_arrive(dkstaged);
       mbar_arrive(dxfree);
-      if (threadIdx.x == CT0) RACE_TRACE(a, 13, gc);
+      if (threadIdx.x == a.ttid) RACE_TRACE(a, 13, gc);
     }
   }
   tc_fence_before();
