@@ -90,9 +90,21 @@ def cpu_threads():
         return os.cpu_count()
 
 
+_BLAS_LIMIT = None
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1 per worker; the reference arm (rank 0 alone) gets every host core
+    try:
+        import numpy  # noqa: F401  (loads BLAS so threadpoolctl can see it)
+        from threadpoolctl import threadpool_limits
+
+        global _BLAS_LIMIT
+        _BLAS_LIMIT = threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")  # held for the run
+    except Exception:
+        pass
     causal = not args.noncausal
     n_sample = 4096 if causal else 16384
     times = []
@@ -567,12 +579,17 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    if os.environ.get("RACE_BENCH_ONE_GPU") == "1":  # test hook: every rank on cuda:0 over gloo
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("RACE_BENCH_ONE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         line = run_ours(args, world, rank, local_rank)
         if line is not None:
