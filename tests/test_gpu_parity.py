@@ -482,3 +482,42 @@ def test_inplace_backward_matches(causal, kind):
     assert got[0].data_ptr() == qc.data_ptr() and got[2].data_ptr() == vc.data_ptr()
     for a, b in zip(got, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("dims", [(64, 64), (96, 128), (128, 32)], ids=["d64", "d96dv128", "dv32"])
+def test_narrow_bf16_heads_run_padded_on_fast_path(causal, dims):
+    """bf16 heads narrower than 128 are zero-padded onto the tcgen05 kernels by race_forward /
+    race_backward; results match the generic path at the native width and the oracle."""
+    dev = _cuda()
+    d, dv = dims
+    n = 3000
+    gen = torch.Generator(device=dev).manual_seed(11)
+    q, k = (torch.randn(1, 2, n, d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    v, g = (torch.randn(1, 2, n, dv, generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=4, causal=causal)
+    w = rb.head_hyperplanes(cfg, 2, d).to(dev)
+    p = cfg.params()
+    from paper_2510_04008_b200.functional import _padded_fast
+
+    assert _padded_fast(q, v, w, p)
+
+    def run():
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        return (o, den) + tuple(rb.race_backward(q, k, v, w, g, p, state=st))
+
+    fast, slow = _both_paths(run)
+    assert fast[0].shape == (1, 2, n, dv) and fast[1].shape == (1, 2, n)
+    for x, y in zip(fast, slow):
+        assert rel_err(x.float().cpu(), y.float().cpu()) <= TOL_BF16
+    qh, kh, vh, gh = (t[0, 1].double().cpu().numpy() for t in (q, k, v, g))
+    wh = w[1].double().cpu().numpy()
+    o_r, _, _ = ro.forward(qh, kh, vh, wh, cfg.beta, causal)
+    assert rel_err(fast[0][0, 1].float().cpu(), o_r) <= TOL_BF16
+    ref = ro.vjp(qh, kh, vh, wh, cfg.beta, gh, causal)
+    errs = grad_errs([t[0, 1].float().cpu().numpy() for t in fast[2:]], ref, GRAD_FLOOR)
+    assert max(errs) <= TOL_BF16, errs
+    qc, kc, vc = q.clone(), k.clone(), v.clone()
+    st = rb.race_forward(q, k, v, w, p)[2]
+    got = rb.race_backward(qc, kc, vc, w, g, p, state=st, inplace=True)
+    assert got[0] is qc and torch.equal(qc, fast[2])
