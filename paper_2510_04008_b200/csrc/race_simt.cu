@@ -25,7 +25,7 @@ namespace race {
 namespace simt {
 
 constexpr int TILE = 32;   // tokens per tile
-constexpr int NT = 128;    // threads per CTA
+constexpr int NT = 256;    // threads per CTA
 
 __host__ __device__ inline int odd_ld(int n) { return n | 1; }
 
