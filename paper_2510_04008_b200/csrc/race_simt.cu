@@ -210,6 +210,35 @@ __device__ void tile_feature_vjp(const Plan& pl, const float* xs, const float* s
   }
 }
 
+// out[r][j] = keep(r, j) ? sum_{c < len} X[r][c] * Y[j][c] : 0 over the TILE x TILE grid, one 2 x 2
+// register micro-tile per thread (each smem value loaded feeds two FMAs); fixed summation order
+static_assert(NT == (TILE / 2) * (TILE / 2), "tile_gram: one 2 x 2 micro-tile per thread");
+template <typename Keep>
+__device__ __forceinline__ void tile_gram(const float* X, int ldx, const float* Y, int ldy, int len, float* out,
+                                          int ldo, Keep keep) {
+  const int r0 = 2 * (threadIdx.x / (TILE / 2)), j0 = 2 * (threadIdx.x % (TILE / 2));
+  const bool k00 = keep(r0, j0), k01 = keep(r0, j0 + 1), k10 = keep(r0 + 1, j0), k11 = keep(r0 + 1, j0 + 1);
+  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+  if (k00 || k01 || k10 || k11) {
+    const float* x0 = X + r0 * ldx;
+    const float* x1 = x0 + ldx;
+    const float* y0 = Y + j0 * ldy;
+    const float* y1 = y0 + ldy;
+#pragma unroll 4
+    for (int c = 0; c < len; ++c) {
+      const float u0 = x0[c], u1 = x1[c], w0 = y0[c], w1 = y1[c];
+      a00 = fmaf(u0, w0, a00);
+      a01 = fmaf(u0, w1, a01);
+      a10 = fmaf(u1, w0, a10);
+      a11 = fmaf(u1, w1, a11);
+    }
+  }
+  out[r0 * ldo + j0] = k00 ? a00 : 0.f;
+  out[r0 * ldo + j0 + 1] = k01 ? a01 : 0.f;
+  out[(r0 + 1) * ldo + j0] = k10 ? a10 : 0.f;
+  out[(r0 + 1) * ldo + j0 + 1] = k11 ? a11 : 0.f;
+}
+
 // acc[f][c] += sum_{t<TILE} A[t][f] * B[t][c] for every (f, c <= dv); each
 // output is owned by one thread, so this is a fixed-order reduction.
 __device__ __forceinline__ void owner_accumulate(const Plan& pl, float* acc, const float* A,
@@ -367,13 +396,7 @@ __global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict_
       }
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
-      const int r = it / TILE, j = it % TILE;
-      float p = 0.f;
-      if (j <= r && j < rows)
-        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[r * pl.ldf + f], phk[j * pl.ldf + f], p);
-      Pm[r * pl.ldp + j] = p;
-    }
+    tile_gram(phq, pl.ldf, phk, pl.ldf, pl.F, Pm, pl.ldp, [rows](int r, int j) { return j <= r && j < rows; });
     __syncthreads();
     for (int r = threadIdx.x; r < TILE; r += NT) {
       float D = 0.f;
@@ -538,15 +561,10 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restric
     tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us);
     tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
     __syncthreads();
-    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
-      const int r = it / TILE, j = it % TILE;
-      float p = 0.f, e = 0.f;
-      if (j <= r && j < rows) {
-        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[r * pl.ldf + f], phk[j * pl.ldf + f], p);
-        for (int c = 0; c < g.dv; ++c) e = fmaf(gs[r * pl.ldv + c], vs[j * pl.ldv + c], e);
-      }
-      Pm[r * pl.ldp + j] = p;
-      Em[r * pl.ldp + j] = e;
+    {
+      auto keep = [rows](int r, int j) { return j <= r && j < rows; };
+      tile_gram(phq, pl.ldf, phk, pl.ldf, pl.F, Pm, pl.ldp, keep);
+      tile_gram(gs, pl.ldv, vs, pl.ldv, g.dv, Em, pl.ldp, keep);
     }
     for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
       const int r = it / pl.F, f = it % pl.F;
@@ -643,15 +661,10 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restric
       gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rowv[kRD * TILE + r] : rowv[kGD * TILE + r];
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < TILE * TILE; it += NT) {
-      const int i = it / TILE, t = it % TILE;
-      float p = 0.f, e = 0.f;
-      if (t >= i && t < rows) {
-        for (int f = 0; f < pl.F; ++f) p = fmaf(phq[t * pl.ldf + f], phk[i * pl.ldf + f], p);
-        for (int c = 0; c <= g.dv; ++c) e = fmaf(gs[t * pl.ldv + c], vs[i * pl.ldv + c], e);
-      }
-      PmT[i * pl.ldp + t] = p;
-      EGT[i * pl.ldp + t] = e;
+    {
+      auto keep = [rows](int i, int t) { return t >= i && t < rows; };
+      tile_gram(phk, pl.ldf, phq, pl.ldf, pl.F, PmT, pl.ldp, keep);
+      tile_gram(vs, pl.ldv, gs, pl.ldv, g.dv + 1, EGT, pl.ldp, keep);
     }
     __syncthreads();
     for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
