@@ -36,17 +36,19 @@ class SketchParams:
 
 
 # ---------------------------------------------------------------------------
-# workspace cache (one growing buffer per device; allocate before graph capture)
+# workspace cache: one growing buffer per (device, stream), so calls on different streams never
+# share scratch (allocate before graph capture)
 # ---------------------------------------------------------------------------
-_WS: dict[int, torch.Tensor] = {}
+_WS: dict[tuple[int, int], torch.Tensor] = {}
 
 
 def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    buf = _WS.get(idx)
+    key = (idx, torch.cuda.current_stream(idx).cuda_stream)
+    buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
-        _WS[idx] = buf
+        _WS[key] = buf
     return buf
 
 
