@@ -521,3 +521,32 @@ def test_narrow_bf16_heads_run_padded_on_fast_path(causal, dims):
     st = rb.race_forward(q, k, v, w, p)[2]
     got = rb.race_backward(qc, kc, vc, w, g, p, state=st, inplace=True)
     assert got[0] is qc and torch.equal(qc, fast[2])
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("shape", [(2, 3, 777), (3, 1, 129), (1, 7, 2560), (5, 2, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_fast_path_batch_head_layouts(causal, shape):
+    """B > 1, odd head counts (per-head hyperplanes picked by bh % H), ragged and tiny N: the
+    tcgen05 path matches the generic path, forward and backward."""
+    dev = _cuda()
+    B, H, n = shape
+    gen = torch.Generator(device=dev).manual_seed(B * 100 + H * 10 + n)
+    q, k, v, g = (torch.randn(B, H, n, 128, generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=21, causal=causal)
+    w = rb.head_hyperplanes(cfg, H, 128).to(dev)
+    p = cfg.params()
+
+    def run():
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        return (o, den) + tuple(rb.race_backward(q, k, v, w, g, p, state=st))
+
+    fast, slow = _both_paths(run)
+    for x, y in zip(fast[:2], slow[:2]):
+        assert x.shape == y.shape
+        assert rel_err(x.float().cpu(), y.float().cpu()) <= TOL_BF16
+    # gradients: denominator floored at 5% of the call's largest gradient (N = 1: dq = dk = 0 exactly)
+    scale = max(float(t.float().abs().max()) for t in slow[2:])
+    for x, y in zip(fast[2:], slow[2:]):
+        assert x.shape == y.shape
+        err = float((x.float() - y.float()).abs().max()) / max(float(y.float().abs().max()), GRAD_FLOOR * scale)
+        assert err <= TOL_BF16, err
