@@ -922,15 +922,17 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(num_full, gc & 1);
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 7, gc);
       tc_fence_after();
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const int c0 = 64 * h + 32 * b;
-        float v[32];
-        tmem_ld32(tmem + lb + TM_NUM + c0, v);
+      {
+        float v[2][32];
+        tmem_ld32(tmem + lb + TM_NUM + 64 * h, v[0]);
+        tmem_ld32(tmem + lb + TM_NUM + 64 * h + 32, v[1]);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= rD;
-        stage_row_bf16(stage + 2 * TILE, r, v, c0);
+        for (int b = 0; b < 2; ++b) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[b][j] *= rD;
+          stage_row_bf16(stage + 2 * TILE, r, v[b], 64 * h + 32 * b);
+        }
       }
       if (h == 1) write_sop(sb + OFF_SOP, r, snext);
       fence_proxy_async();
