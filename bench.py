@@ -251,9 +251,9 @@ def max_context(dev, causal, dtype, inplace=False):
     return {"tokens": 0, "causal": causal, "error": "nothing fits"}
 
 
-def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 1 << 24)):
+def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 12 << 20, 1 << 24)):
     """BASELINE configs[2]: fwd+bwd tokens/s of the H=4, d=128 layer for N from 1 Mi to
-    16 Mi tokens on one GPU, causal and non-causal (inputs resident in HBM, 2 timed reps)."""
+    16 Mi tokens (1, 2, 4, 8, 12, 16 Mi) on one GPU, causal and non-causal (inputs resident in HBM, 2 timed reps)."""
     import torch
 
     import paper_2510_04008_b200 as rb
@@ -286,6 +286,39 @@ def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 1 << 24))
             except torch.cuda.OutOfMemoryError:
                 out.append({"tokens": n, "causal": causal, "error": "out of memory"})
             torch.cuda.empty_cache()
+    return out
+
+
+def sketch_sweep(dev, dtype, n=131072):
+    """SURVEY 8(d)'s optional sketch sweep: the headline layer with larger sketches (the
+    tcgen05 kernels cover F <= 8; larger F runs on the generic CUDA-core kernels)."""
+    import torch
+
+    import paper_2510_04008_b200 as rb
+    from paper_2510_04008_b200 import _lib
+    from paper_2510_04008_b200.functional import Problem
+
+    out = []
+    gen = torch.Generator(device=dev).manual_seed(9)
+    q, k, v, g = (torch.randn((1, HEADS, n, DIM), generator=gen, device=dev, dtype=dtype) for _ in range(4))
+    for P, L in ((2, 2), (3, 1), (1, 4), (4, 4)):
+        cfg = rb.SketchConfig(hyperplanes=P, tables=L, beta=BETA, seed=0, causal=True)
+        w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
+        p = cfg.params()
+        fast = _lib.fast_path(Problem(q, k, v, w, p).desc)
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        rb.race_backward(q, k, v, w, g, p, state=st)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(3):
+            o, den, st = rb.race_forward(q, k, v, w, p)
+            rb.race_backward(q, k, v, w, g, p, state=st)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / 3
+        out.append({"P": P, "L": L, "F": L << P, "causal": True, "tokens": n, "fast_path": bool(fast),
+                    "ms_fwd_bwd": round(ms, 3), "tokens_per_s": n / (ms / 1e3)})
     return out
 
 
@@ -602,6 +635,7 @@ def main():
                 line["max_context"] = [max_context(dev, c, dt) for c in (True, False)] + [
                     max_context(dev, True, dt, inplace=True)]
                 line["scale_sweep"] = scale_sweep(dev, dt)
+                line["sketch_sweep"] = sketch_sweep(dev, dt)
                 line["gpt_train_step"] = gpt_train_step(dev)
             print(json.dumps(line), flush=True)
     finally:
