@@ -210,47 +210,70 @@ __device__ void tile_feature_vjp(const Plan& pl, const float* xs, const float* s
   }
 }
 
-// out[r][j] = keep(r, j) ? sum_{c < len} X[r][c] * Y[j][c] : 0 over the TILE x TILE grid, one 2 x 2
-// register micro-tile per thread (each smem value loaded feeds two FMAs); fixed summation order
-static_assert(NT == (TILE / 2) * (TILE / 2), "tile_gram: one 2 x 2 micro-tile per thread");
+// out[r][j] = keep(r, j) ? sum_{c < len} X[r][c] * Y[j][c] : 0 for r < nr, j < nc (both even), in
+// 2 x 2 register micro-tiles (each smem value loaded feeds two FMAs); fixed summation order
+template <typename Keep>
+__device__ __forceinline__ void gram2(const float* X, int ldx, int nr, const float* Y, int ldy, int nc, int len,
+                                      float* out, int ldo, Keep keep) {
+  const int cols = nc / 2;
+  for (int it = threadIdx.x; it < (nr / 2) * cols; it += NT) {
+    const int r0 = 2 * (it / cols), j0 = 2 * (it % cols);
+    const bool k00 = keep(r0, j0), k01 = keep(r0, j0 + 1), k10 = keep(r0 + 1, j0), k11 = keep(r0 + 1, j0 + 1);
+    float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+    if (k00 || k01 || k10 || k11) {
+      const float* x0 = X + r0 * ldx;
+      const float* x1 = x0 + ldx;
+      const float* y0 = Y + j0 * ldy;
+      const float* y1 = y0 + ldy;
+#pragma unroll 4
+      for (int c = 0; c < len; ++c) {
+        const float u0 = x0[c], u1 = x1[c], w0 = y0[c], w1 = y1[c];
+        a00 = fmaf(u0, w0, a00);
+        a01 = fmaf(u0, w1, a01);
+        a10 = fmaf(u1, w0, a10);
+        a11 = fmaf(u1, w1, a11);
+      }
+    }
+    out[r0 * ldo + j0] = k00 ? a00 : 0.f;
+    out[r0 * ldo + j0 + 1] = k01 ? a01 : 0.f;
+    out[(r0 + 1) * ldo + j0] = k10 ? a10 : 0.f;
+    out[(r0 + 1) * ldo + j0 + 1] = k11 ? a11 : 0.f;
+  }
+}
 template <typename Keep>
 __device__ __forceinline__ void tile_gram(const float* X, int ldx, const float* Y, int ldy, int len, float* out,
                                           int ldo, Keep keep) {
-  const int r0 = 2 * (threadIdx.x / (TILE / 2)), j0 = 2 * (threadIdx.x % (TILE / 2));
-  const bool k00 = keep(r0, j0), k01 = keep(r0, j0 + 1), k10 = keep(r0 + 1, j0), k11 = keep(r0 + 1, j0 + 1);
-  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
-  if (k00 || k01 || k10 || k11) {
-    const float* x0 = X + r0 * ldx;
-    const float* x1 = x0 + ldx;
-    const float* y0 = Y + j0 * ldy;
-    const float* y1 = y0 + ldy;
-#pragma unroll 4
-    for (int c = 0; c < len; ++c) {
-      const float u0 = x0[c], u1 = x1[c], w0 = y0[c], w1 = y1[c];
-      a00 = fmaf(u0, w0, a00);
-      a01 = fmaf(u0, w1, a01);
-      a10 = fmaf(u1, w0, a10);
-      a11 = fmaf(u1, w1, a11);
-    }
-  }
-  out[r0 * ldo + j0] = k00 ? a00 : 0.f;
-  out[r0 * ldo + j0 + 1] = k01 ? a01 : 0.f;
-  out[(r0 + 1) * ldo + j0] = k10 ? a10 : 0.f;
-  out[(r0 + 1) * ldo + j0 + 1] = k11 ? a11 : 0.f;
+  gram2(X, ldx, TILE, Y, ldy, TILE, len, out, ldo, keep);
 }
+struct KeepAll {
+  __device__ bool operator()(int, int) const { return true; }
+};
 
 // acc[f][c] += sum_{t<TILE} A[t][f] * B[t][c] for every (f, c <= dv); each
 // output is owned by one thread, so this is a fixed-order reduction.
 __device__ __forceinline__ void owner_accumulate(const Plan& pl, float* acc, const float* A,
                                                  const float* B) {
-  const int nout = pl.F * (pl.dv + 1);
-  for (int o = threadIdx.x; o < nout; o += NT) {
-    const int f = o / (pl.dv + 1), c = o % (pl.dv + 1);
-    float s = acc[f * pl.ldS + c];
-    float part = 0.f;
+  // 2 (f) x 2 (c) outputs per item: each A / B value loaded feeds two FMAs (F is even: T * 2^P)
+  const int nc = pl.dv + 1, cp = (nc + 1) / 2;
+  for (int o = threadIdx.x; o < (pl.F / 2) * cp; o += NT) {
+    const int f0 = 2 * (o / cp), c0 = 2 * (o % cp);
+    const bool c1ok = c0 + 1 < nc;
+    float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
 #pragma unroll 8
-    for (int t = 0; t < TILE; ++t) part = fmaf(A[t * pl.ldf + f], B[t * pl.ldv + c], part);
-    acc[f * pl.ldS + c] = s + part;
+    for (int t = 0; t < TILE; ++t) {
+      const float a0 = A[t * pl.ldf + f0], a1 = A[t * pl.ldf + f0 + 1];
+      const float b0 = B[t * pl.ldv + c0], b1 = c1ok ? B[t * pl.ldv + c0 + 1] : 0.f;
+      p00 = fmaf(a0, b0, p00);
+      p01 = fmaf(a0, b1, p01);
+      p10 = fmaf(a1, b0, p10);
+      p11 = fmaf(a1, b1, p11);
+    }
+    acc[f0 * pl.ldS + c0] += p00;
+    acc[(f0 + 1) * pl.ldS + c0] += p10;
+    if (c1ok) {
+      acc[f0 * pl.ldS + c0 + 1] += p01;
+      acc[(f0 + 1) * pl.ldS + c0 + 1] += p11;
+    }
   }
 }
 
@@ -445,12 +468,7 @@ __global__ void __launch_bounds__(NT) k_bwd_q(Geo g, const Tin* __restrict__ q, 
     __syncthreads();
     tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us);
     // y[t][f] = S_v[f] . dO_t
-    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
-      const int r = it / pl.F, f = it % pl.F;
-      float y = 0.f;
-      for (int c = 0; c < g.dv; ++c) y = fmaf(S[f * pl.ldS + c], gs[r * pl.ldv + c], y);
-      ys[r * pl.ldf + f] = y;
-    }
+    gram2(gs, pl.ldv, TILE, S, pl.ldS, pl.F, g.dv, ys, pl.ldf, KeepAll());  // y[t][f] = S_v[f] . dO_t
     __syncthreads();
     for (int r = threadIdx.x; r < TILE; r += NT) {
       float D = 0.f, num = 0.f;
@@ -510,12 +528,7 @@ __global__ void __launch_bounds__(NT) k_bwd_k(Geo g, const Tin* __restrict__ k, 
     __syncthreads();
     tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us);
     __syncthreads();
-    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
-      const int r = it / pl.F, f = it % pl.F;
-      float z = 0.f;
-      for (int c = 0; c <= g.dv; ++c) z = fmaf(dS[f * pl.ldS + c], vs[r * pl.ldv + c], z);
-      dph[r * pl.ldf + f] = z;
-    }
+    gram2(vs, pl.ldv, TILE, dS, pl.ldS, pl.F, g.dv + 1, dph, pl.ldf, KeepAll());  // z[t][f] = [V|1]_t . dS[f]
     for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
       const int r = it / g.dv, c = it % g.dv;
       float a = 0.f;
@@ -566,12 +579,7 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restric
       tile_gram(phq, pl.ldf, phk, pl.ldf, pl.F, Pm, pl.ldp, keep);
       tile_gram(gs, pl.ldv, vs, pl.ldv, g.dv, Em, pl.ldp, keep);
     }
-    for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
-      const int r = it / pl.F, f = it % pl.F;
-      float y = 0.f;
-      for (int c = 0; c < g.dv; ++c) y = fmaf(S[f * pl.ldS + c], gs[r * pl.ldv + c], y);
-      ys[r * pl.ldf + f] = y;
-    }
+    gram2(gs, pl.ldv, TILE, S, pl.ldS, pl.F, g.dv, ys, pl.ldf, KeepAll());  // y[t][f] = S_v[f] . dO_t
     __syncthreads();
     for (int r = threadIdx.x; r < TILE; r += NT) {
       float D = 0.f, num = 0.f;
@@ -667,10 +675,11 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restric
       tile_gram(vs, pl.ldv, gs, pl.ldv, g.dv + 1, EGT, pl.ldp, keep);
     }
     __syncthreads();
+    gram2(vs, pl.ldv, TILE, dS, pl.ldS, pl.F, g.dv + 1, dph, pl.ldf, KeepAll());  // [V|1]_i . dS_>c[f]
+    __syncthreads();
     for (int it = threadIdx.x; it < TILE * pl.F; it += NT) {
       const int i = it / pl.F, f = it % pl.F;
-      float a = 0.f;
-      for (int c = 0; c <= g.dv; ++c) a = fmaf(dS[f * pl.ldS + c], vs[i * pl.ldv + c], a);
+      float a = dph[i * pl.ldf + f];
       for (int t = i; t < rows; ++t) a = fmaf(EGT[i * pl.ldp + t], phq[t * pl.ldf + f], a);
       dph[i * pl.ldf + f] = a;
     }
