@@ -89,24 +89,43 @@ enum RowSlot { kScQ = 0, kScK = 1, kD = 2, kRho = 3, kRD = 4, kGD = 5, kDot = 6,
 template <typename Tin>
 __device__ void load_rows(const Tin* __restrict__ src, int rows, int cols, float* dst, int ld,
                           float* scale, bool normalize) {
+  // each warp owns RPW rows; all RPW x 4 loads of a 128-column block are issued before any is used
+  constexpr int RPW = TILE / (NT / 32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < TILE; r += NT / 32) {
-    float ss = 0.f;
-    if (r < rows) {
-      const Tin* s = src + size_t(r) * cols;
-      for (int c = lane; c < cols; c += 32) {
-        const float x = to_f32(s[c]);
-        dst[r * ld + c] = x;
-        ss = fmaf(x, x, ss);
+  float ss[RPW];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) ss[i] = 0.f;
+  for (int c0 = 0; c0 < cols; c0 += 128) {
+    float x[RPW][4];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + i * (NT / 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + lane + 32 * j;
+        x[i][j] = (r < rows && c < cols) ? to_f32(src[size_t(r) * cols + c]) : 0.f;
       }
-    } else {
-      for (int c = lane; c < cols; c += 32) dst[r * ld + c] = 0.f;
     }
-    if (scale) {
-      ss = warp_sum(ss);
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + i * (NT / 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + lane + 32 * j;
+        if (c < cols) {
+          dst[r * ld + c] = x[i][j];
+          ss[i] = fmaf(x[i][j], x[i][j], ss[i]);
+        }
+      }
+    }
+  }
+  if (scale) {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const float t = warp_sum(ss[i]);
       if (lane == 0) {
-        const float nrm = sqrtf(ss);
-        scale[r] = normalize ? (nrm < kZeroRowEps ? -1.f : nrm) : 1.f;
+        const float nrm = sqrtf(t);
+        scale[warp + i * (NT / 32)] = normalize ? (nrm < kZeroRowEps ? -1.f : nrm) : 1.f;
       }
     }
   }
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(NT) k_readout(Geo g, const Tin* __restrict__ q
 
 // Causal forward over one segment with carry-in S_<seg.
 template <typename Tin>
-__global__ void __launch_bounds__(NT) k_causal_fwd(Geo g, const Tin* __restrict__ q,
+__global__ void __launch_bounds__(NT, 2) k_causal_fwd(Geo g, const Tin* __restrict__ q,
                                                    const Tin* __restrict__ k, const Tin* __restrict__ v,
                                                    const float* __restrict__ w,
                                                    const float* __restrict__ carries,
@@ -543,7 +562,7 @@ __global__ void __launch_bounds__(NT) k_bwd_k(Geo g, const Tin* __restrict__ k, 
 
 // Causal backward, forward scan: dq, per-token rden / gden, per-segment dS.
 template <typename Tin>
-__global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restrict__ q,
+__global__ void __launch_bounds__(NT, 2) k_bwd_causal_q(Geo g, const Tin* __restrict__ q,
                                                      const Tin* __restrict__ k, const Tin* __restrict__ v,
                                                      const Tin* __restrict__ d_o, const float* __restrict__ w,
                                                      const float* __restrict__ carries, Tin* __restrict__ dq,
@@ -630,7 +649,7 @@ __global__ void __launch_bounds__(NT) k_bwd_causal_q(Geo g, const Tin* __restric
 
 // Causal backward, reverse scan over one segment with suffix carry dS_>seg.
 template <typename Tin>
-__global__ void __launch_bounds__(NT) k_bwd_causal_k(Geo g, const Tin* __restrict__ q,
+__global__ void __launch_bounds__(NT, 2) k_bwd_causal_k(Geo g, const Tin* __restrict__ q,
                                                      const Tin* __restrict__ k, const Tin* __restrict__ v,
                                                      const Tin* __restrict__ d_o, const float* __restrict__ w,
                                                      const float* __restrict__ rden,
