@@ -702,12 +702,37 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_causal_k(Geo g, const Tin* __rest
       for (int t = i; t < rows; ++t) a = fmaf(EGT[i * pl.ldp + t], phq[t * pl.ldf + f], a);
       dph[i * pl.ldf + f] = a;
     }
-    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
-      const int i = it / g.dv, c = it % g.dv;
-      float a = 0.f;
-      for (int f = 0; f < pl.F; ++f) a = fmaf(phk[i * pl.ldf + f], dS[f * pl.ldS + c], a);
-      for (int t = i; t < rows; ++t) a = fmaf(PmT[i * pl.ldp + t], gs[t * pl.ldv + c], a);
-      dvo[(bh * g.N + t0 + i) * g.dv + c] = from_f32<Tin>(a);
+    {  // dV = Phi_k dS_>c,v + P~^T dO, 2 (rows) x 2 (columns) per item (P~^T is zero below its diagonal)
+      const int cp = (g.dv + 1) / 2;
+      for (int it = threadIdx.x; it < (TILE / 2) * cp; it += NT) {
+        const int i0 = 2 * (it / cp), c0 = 2 * (it % cp);
+        if (i0 >= rows) continue;
+        const bool c1 = c0 + 1 < g.dv, i1 = i0 + 1 < rows;
+        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+        for (int f = 0; f < pl.F; ++f) {
+          const float p0 = phk[i0 * pl.ldf + f], p1 = phk[(i0 + 1) * pl.ldf + f];
+          const float d0 = dS[f * pl.ldS + c0], d1 = c1 ? dS[f * pl.ldS + c0 + 1] : 0.f;
+          a00 = fmaf(p0, d0, a00);
+          a01 = fmaf(p0, d1, a01);
+          a10 = fmaf(p1, d0, a10);
+          a11 = fmaf(p1, d1, a11);
+        }
+        for (int t = i0; t < rows; ++t) {
+          const float m0 = PmT[i0 * pl.ldp + t], m1 = PmT[(i0 + 1) * pl.ldp + t];
+          const float g0 = gs[t * pl.ldv + c0], g1 = c1 ? gs[t * pl.ldv + c0 + 1] : 0.f;
+          a00 = fmaf(m0, g0, a00);
+          a01 = fmaf(m0, g1, a01);
+          a10 = fmaf(m1, g0, a10);
+          a11 = fmaf(m1, g1, a11);
+        }
+        Tin* o0 = dvo + (bh * g.N + t0 + i0) * g.dv + c0;
+        o0[0] = from_f32<Tin>(a00);
+        if (c1) o0[1] = from_f32<Tin>(a01);
+        if (i1) {
+          o0[g.dv] = from_f32<Tin>(a10);
+          if (c1) o0[g.dv + 1] = from_f32<Tin>(a11);
+        }
+      }
     }
     __syncthreads();
     tile_feature_vjp<Tin>(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us, dph, dproj, dx,
