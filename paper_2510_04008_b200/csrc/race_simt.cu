@@ -448,13 +448,39 @@ __global__ void __launch_bounds__(NT, 2) k_causal_fwd(Geo g, const Tin* __restri
       if (r < rows) den[bh * g.N + t0 + r] = D * invT;
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
-      const int r = it / g.dv, c = it % g.dv;
-      float num = 0.f;
-      for (int f = 0; f < pl.F; ++f) num = fmaf(phq[r * pl.ldf + f], S[f * pl.ldS + c], num);
-      for (int j = 0; j <= r; ++j) num = fmaf(Pm[r * pl.ldp + j], vs[j * pl.ldv + c], num);
-      const float D = rowv[kD * TILE + r];
-      o[(bh * g.N + t0 + r) * g.dv + c] = from_f32<Tin>(D * invT <= kDegenerateDenEps ? 0.f : num / D);
+    {  // num = phi_q S_<c + tril(Pm) V, 2 (rows) x 2 (columns) per item (Pm is zero above its diagonal)
+      const int cp = (g.dv + 1) / 2;
+      for (int it = threadIdx.x; it < (TILE / 2) * cp; it += NT) {
+        const int r0 = 2 * (it / cp), c0 = 2 * (it % cp);
+        if (r0 >= rows) continue;
+        const bool c1 = c0 + 1 < g.dv, r1 = r0 + 1 < rows;
+        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+        for (int f = 0; f < pl.F; ++f) {
+          const float p0 = phq[r0 * pl.ldf + f], p1 = phq[(r0 + 1) * pl.ldf + f];
+          const float s0 = S[f * pl.ldS + c0], s1 = c1 ? S[f * pl.ldS + c0 + 1] : 0.f;
+          a00 = fmaf(p0, s0, a00);
+          a01 = fmaf(p0, s1, a01);
+          a10 = fmaf(p1, s0, a10);
+          a11 = fmaf(p1, s1, a11);
+        }
+        for (int j = 0; j <= r0 + 1 && j < TILE; ++j) {
+          const float m0 = Pm[r0 * pl.ldp + j], m1 = Pm[(r0 + 1) * pl.ldp + j];
+          const float v0 = vs[j * pl.ldv + c0], v1 = c1 ? vs[j * pl.ldv + c0 + 1] : 0.f;
+          a00 = fmaf(m0, v0, a00);
+          a01 = fmaf(m0, v1, a01);
+          a10 = fmaf(m1, v0, a10);
+          a11 = fmaf(m1, v1, a11);
+        }
+        const float D0 = rowv[kD * TILE + r0], D1 = rowv[kD * TILE + r0 + 1];
+        const bool z0 = D0 * invT <= kDegenerateDenEps, z1 = D1 * invT <= kDegenerateDenEps;
+        Tin* o0 = o + (bh * g.N + t0 + r0) * g.dv + c0;
+        o0[0] = from_f32<Tin>(z0 ? 0.f : a00 / D0);
+        if (c1) o0[1] = from_f32<Tin>(z0 ? 0.f : a01 / D0);
+        if (r1) {
+          o0[g.dv] = from_f32<Tin>(z1 ? 0.f : a10 / D1);
+          if (c1) o0[g.dv + 1] = from_f32<Tin>(z1 ? 0.f : a11 / D1);
+        }
+      }
     }
     __syncthreads();
     owner_accumulate(pl, S, phk, vs);  // S_<next tile
