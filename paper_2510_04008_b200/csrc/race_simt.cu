@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(NT, 2) k_causal_fwd(Geo g, const Tin* __restri
 
 // Non-causal backward, query side.
 template <typename Tin>
-__global__ void __launch_bounds__(NT) k_bwd_q(Geo g, const Tin* __restrict__ q, const Tin* __restrict__ d_o,
+__global__ void __launch_bounds__(NT, 2) k_bwd_q(Geo g, const Tin* __restrict__ q, const Tin* __restrict__ d_o,
                                               const float* __restrict__ w,
                                               const float* __restrict__ tables, Tin* __restrict__ dq,
                                               float* __restrict__ dpart) {
@@ -574,11 +574,29 @@ __global__ void __launch_bounds__(NT) k_bwd_k(Geo g, const Tin* __restrict__ k, 
     tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us);
     __syncthreads();
     gram2(vs, pl.ldv, TILE, dS, pl.ldS, pl.F, g.dv + 1, dph, pl.ldf, KeepAll());  // z[t][f] = [V|1]_t . dS[f]
-    for (int it = threadIdx.x; it < rows * g.dv; it += NT) {
-      const int r = it / g.dv, c = it % g.dv;
-      float a = 0.f;
-      for (int f = 0; f < pl.F; ++f) a = fmaf(phk[r * pl.ldf + f], dS[f * pl.ldS + c], a);
-      dvo[(bh * g.N + t0 + r) * g.dv + c] = from_f32<Tin>(a);
+    {  // dV = Phi_k dS_v, 2 (rows) x 2 (columns) per item
+      const int cp = (g.dv + 1) / 2;
+      for (int it = threadIdx.x; it < (TILE / 2) * cp; it += NT) {
+        const int r0 = 2 * (it / cp), c0 = 2 * (it % cp);
+        if (r0 >= rows) continue;
+        const bool c1 = c0 + 1 < g.dv, r1 = r0 + 1 < rows;
+        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+        for (int f = 0; f < pl.F; ++f) {
+          const float p0 = phk[r0 * pl.ldf + f], p1 = phk[(r0 + 1) * pl.ldf + f];
+          const float d0 = dS[f * pl.ldS + c0], d1 = c1 ? dS[f * pl.ldS + c0 + 1] : 0.f;
+          a00 = fmaf(p0, d0, a00);
+          a01 = fmaf(p0, d1, a01);
+          a10 = fmaf(p1, d0, a10);
+          a11 = fmaf(p1, d1, a11);
+        }
+        Tin* o0 = dvo + (bh * g.N + t0 + r0) * g.dv + c0;
+        o0[0] = from_f32<Tin>(a00);
+        if (c1) o0[1] = from_f32<Tin>(a01);
+        if (r1) {
+          o0[g.dv] = from_f32<Tin>(a10);
+          if (c1) o0[g.dv + 1] = from_f32<Tin>(a11);
+        }
+      }
     }
     __syncthreads();
     tile_feature_vjp<Tin>(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us, dph, dproj, dx,
