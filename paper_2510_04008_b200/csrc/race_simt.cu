@@ -195,37 +195,31 @@ __device__ void tile_feature_vjp(const Plan& pl, const float* xs, const float* s
     }
   }
   __syncthreads();
-  // (2) dx^ = dproj . W  (items (row, col)); the projection used x^ = x / scale
-  for (int it = threadIdx.x; it < TILE * pl.d; it += NT) {
-    const int r = it / pl.d, c = it % pl.d;
-    const float* dpr = dproj + r * pl.ldu;
-    float acc = 0.f;
-    for (int j = 0; j < pl.TP; ++j) acc = fmaf(dpr[j], ws[j * pl.d + c], acc);
-    dx[r * pl.ldx + c] = acc;
-  }
-  __syncthreads();
-  // (3) radial component (dx^ . x^) per row, warp per row
+  // (2)-(4) a warp per row (lanes over columns, no cross-warp dependency): dx^ = dproj . W, the
+  // radial component (dx^ . x^), then the sphere-tangent projection scaled by 1/||x||
+  // (pass-through rows keep dx^); the projection used x^ = x / scale
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < TILE; r += NT / 32) {
+    const float* dpr = dproj + r * pl.ldu;
     const float sc = scale[r];
-    float acc = 0.f;
-    if (normalize && sc > 0.f) {
-      for (int c = lane; c < pl.d; c += 32) acc = fmaf(dx[r * pl.ldx + c], xs[r * pl.ldx + c], acc);
-      acc = warp_sum(acc) / sc;
+    const bool tang = normalize && sc > 0.f;
+    float dot = 0.f;
+    for (int c = lane; c < pl.d; c += 32) {
+      float acc = 0.f;
+      for (int j = 0; j < pl.TP; ++j) acc = fmaf(dpr[j], ws[j * pl.d + c], acc);
+      dx[r * pl.ldx + c] = acc;
+      if (tang) dot = fmaf(acc, xs[r * pl.ldx + c], dot);
     }
-    if (lane == 0) dots[r] = acc;
-  }
-  __syncthreads();
-  // (4) sphere-tangent projection, scaled by 1/||x||; pass-through rows keep dx^
-  for (int it = threadIdx.x; it < rows * pl.d; it += NT) {
-    const int r = it / pl.d, c = it % pl.d;
-    const float sc = scale[r];
-    float g = dx[r * pl.ldx + c];
-    if (normalize && sc > 0.f) {
-      const float rs = 1.f / sc;
-      g = (g - dots[r] * xs[r * pl.ldx + c] * rs) * rs;
+    dot = tang ? warp_sum(dot) / sc : 0.f;
+    if (lane == 0) dots[r] = dot;
+    if (r < rows) {
+      const float rs = tang ? 1.f / sc : 1.f;
+      for (int c = lane; c < pl.d; c += 32) {
+        float g = dx[r * pl.ldx + c];  // this lane's own value
+        if (tang) g = (g - dot * xs[r * pl.ldx + c] * rs) * rs;
+        dst[size_t(r) * pl.d + c] = from_f32<Tout>(g);
+      }
     }
-    dst[size_t(r) * pl.d + c] = from_f32<Tout>(g);
   }
 }
 
