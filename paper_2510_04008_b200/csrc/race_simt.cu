@@ -44,6 +44,7 @@ struct Plan {
   int ldx, ldv, ldf, ldS, ldu, ldp;
   // float offsets (all buffers are float)
   int oW, oS, oAcc, oXq, oXk, oDx, oV, oG, oPhq, oPhk, oDph, oY, oU, oDproj, oPm, oEm;
+  int oPj;       // [2][TILE][ldu] projection scratch
   int oRow;      // 8 row-scalar arrays of TILE floats
   int total;     // floats
 
@@ -69,11 +70,14 @@ struct Plan {
     oDproj = take(kDproj, TILE * ldu);
     oPm = take(kPm, TILE * ldp);
     oEm = take(kEm, TILE * ldp);
+    oPj = o; o += (2 * TILE * ldu + 3) & ~3;  // projections of up to two tiles (tile_features scratch)
     oRow = o; o += 8 * TILE;
     total = o;
   }
   __host__ __device__ size_t bytes() const { return size_t(total) * sizeof(float); }
 };
+
+extern __shared__ float4 smem_f4[];
 
 // row-scalar slots inside Plan::oRow
 enum RowSlot { kScQ = 0, kScK = 1, kD = 2, kRho = 3, kRD = 4, kGD = 5, kDot = 6, kTmp = 7 };
@@ -138,7 +142,11 @@ __device__ void load_v_ones(const Tin* __restrict__ src, int rows, int dv, float
   for (int r = threadIdx.x; r < TILE; r += NT) dst[r * ld + dv] = r < rows ? 1.f : 0.f;
 }
 
-// phi (and optionally u) for the TILE rows in xs.  Items are (row, table).
+// phi (and optionally u) for the TILE rows of one or two tiles (n = 1, 2).  Two phases so that
+// every thread has work: (1) items (tile, hyperplane, row): one projection x . w_j each (rows of a
+// warp share w_j: broadcast; odd row stride: conflict-free), (2) items (tile, table, row): tanh and
+// the corner softmax.
+// one tile: items (row, table), each computing its P projections (no scratch, no barrier)
 __device__ void tile_features(const Plan& pl, const float* xs, const float* scale, const float* ws,
                               float beta, float* phi, float* u_out) {
   for (int it = threadIdx.x; it < TILE * pl.T; it += NT) {
@@ -159,6 +167,40 @@ __device__ void tile_features(const Plan& pl, const float* xs, const float* scal
     }
     corner_softmax(u, pl.P, beta, phi + r * pl.ldf + tau * pl.R);
   }
+}
+
+__device__ void tile_features_n(const Plan& pl, int n, const float* xs0, const float* sc0, float* phi0, float* u0,
+                                const float* xs1, const float* sc1, float* phi1, float* u1, const float* ws,
+                                float beta) {
+  float* pj = reinterpret_cast<float*>(smem_f4) + pl.oPj;
+  const int per = TILE * pl.TP;
+  for (int it = threadIdx.x; it < n * per; it += NT) {
+    const int t = it / per, rem = it % per, j = rem / TILE, r = rem % TILE;
+    const float* x = (t ? xs1 : xs0) + r * pl.ldx;
+    const float* w = ws + j * pl.d;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < pl.d; ++c) acc = fmaf(x[c], w[c], acc);
+    pj[(t * TILE + r) * pl.ldu + j] = acc;
+  }
+  __syncthreads();
+  const int per2 = TILE * pl.T;
+  for (int it = threadIdx.x; it < n * per2; it += NT) {
+    const int t = it / per2, rem = it % per2, tau = rem / TILE, r = rem % TILE;
+    const float sc = (t ? sc1 : sc0)[r];
+    const float inv = sc > 0.f ? 1.f / sc : 1.f;
+    float* u_out = t ? u1 : u0;
+    float u[kPMax];
+#pragma unroll
+    for (int p = 0; p < kPMax; ++p) {
+      if (p < pl.P) {
+        u[p] = tanhf(pj[(t * TILE + r) * pl.ldu + tau * pl.P + p] * inv);
+        if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = u[p];
+      }
+    }
+    corner_softmax(u, pl.P, beta, (t ? phi1 : phi0) + r * pl.ldf + tau * pl.R);
+  }
+  __syncthreads();  // pj is reused by the next call
 }
 
 // Feature VJP for the TILE rows: given dphi (smem [TILE][ldf]) produce dx
@@ -322,7 +364,6 @@ __device__ __forceinline__ const float* w_of(const Geo& g, const float* w, int64
   return w + (g.w_per_head ? (bh % g.H) * int64_t(g.T * g.P * g.d) : 0);
 }
 
-extern __shared__ float4 smem_f4[];
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -420,8 +461,7 @@ __global__ void __launch_bounds__(NT, 2) k_causal_fwd(Geo g, const Tin* __restri
     load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
     load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
     __syncthreads();
-    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
-    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    tile_features_n(pl, 2, xq, rowv + kScQ * TILE, phq, nullptr, xk, rowv + kScK * TILE, phk, nullptr, ws, g.beta);
     if (nrm) {  // sketch rows (race_b200.h): the generic backward only uses the row norms
       for (int r = threadIdx.x; r < rows; r += NT) {
         const float sq = rowv[kScQ * TILE + r], sk = rowv[kScK * TILE + r];
@@ -628,8 +668,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_causal_q(Geo g, const Tin* __rest
     load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
     load_rows<Tin>(d_o + (bh * g.N + t0) * g.dv, rows, g.dv, gs, pl.ldv, nullptr, false);
     __syncthreads();
-    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, us);
-    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, nullptr);
+    tile_features_n(pl, 2, xq, rowv + kScQ * TILE, phq, us, xk, rowv + kScK * TILE, phk, nullptr, ws, g.beta);
     __syncthreads();
     {
       auto keep = [rows](int r, int j) { return j <= r && j < rows; };
@@ -719,8 +758,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_causal_k(Geo g, const Tin* __rest
       rowv[kGD * TILE + r] = r < rows ? gden[bh * ((g.N + 3) & ~int64_t(3)) + t0 + r] : 0.f;
     }
     __syncthreads();
-    tile_features(pl, xq, rowv + kScQ * TILE, ws, g.beta, phq, nullptr);
-    tile_features(pl, xk, rowv + kScK * TILE, ws, g.beta, phk, us);
+    tile_features_n(pl, 2, xq, rowv + kScQ * TILE, phq, nullptr, xk, rowv + kScK * TILE, phk, us, ws, g.beta);
     for (int it = threadIdx.x; it < TILE * (g.dv + 1); it += NT) {
       const int r = it / (g.dv + 1), c = it % (g.dv + 1);
       gs[r * pl.ldv + c] = c < g.dv ? gs[r * pl.ldv + c] * rowv[kRD * TILE + r] : rowv[kGD * TILE + r];
