@@ -159,9 +159,16 @@ __device__ void tile_features(const Plan& pl, const float* xs, const float* scal
     for (int p = 0; p < kPMax; ++p) {
       if (p < pl.P) {
         const float* w = ws + (tau * pl.P + p) * pl.d;
-        float acc = 0.f;
-        for (int c = 0; c < pl.d; ++c) acc = fmaf(x[c], w[c], acc);
-        u[p] = tanhf(acc * inv);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent chains (fixed order)
+        int c = 0;
+        for (; c + 4 <= pl.d; c += 4) {
+          a0 = fmaf(x[c], w[c], a0);
+          a1 = fmaf(x[c + 1], w[c + 1], a1);
+          a2 = fmaf(x[c + 2], w[c + 2], a2);
+          a3 = fmaf(x[c + 3], w[c + 3], a3);
+        }
+        for (; c < pl.d; ++c) a0 = fmaf(x[c], w[c], a0);
+        u[p] = tanhf(((a0 + a1) + (a2 + a3)) * inv);
         if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = u[p];
       }
     }
@@ -178,10 +185,16 @@ __device__ void tile_features_n(const Plan& pl, int n, const float* xs0, const f
     const int t = it / per, rem = it % per, j = rem / TILE, r = rem % TILE;
     const float* x = (t ? xs1 : xs0) + r * pl.ldx;
     const float* w = ws + j * pl.d;
-    float acc = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < pl.d; ++c) acc = fmaf(x[c], w[c], acc);
-    pj[(t * TILE + r) * pl.ldu + j] = acc;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent chains (fixed order)
+    int c = 0;
+    for (; c + 4 <= pl.d; c += 4) {
+      a0 = fmaf(x[c], w[c], a0);
+      a1 = fmaf(x[c + 1], w[c + 1], a1);
+      a2 = fmaf(x[c + 2], w[c + 2], a2);
+      a3 = fmaf(x[c + 3], w[c + 3], a3);
+    }
+    for (; c < pl.d; ++c) a0 = fmaf(x[c], w[c], a0);
+    pj[(t * TILE + r) * pl.ldu + j] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
   const int per2 = TILE * pl.T;
