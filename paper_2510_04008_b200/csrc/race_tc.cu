@@ -38,7 +38,6 @@ constexpr int OFF_STAGE = 0;
 constexpr int OFF_W = STAGES * STAGE_BYTES;
 constexpr int OFF_PHI = OFF_W + WOP;         // 2 buffers
 constexpr int OFF_BAR = OFF_PHI + 2 * PHI;
-constexpr int SMEM = OFF_BAR + 256 + 1024;   // + alignment slack
 }  // namespace agg
 
 
@@ -269,12 +268,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 namespace rdo {
 constexpr int STAGES = 3;
 constexpr int STAGE_BYTES = TILE;  // Q, reused as O staging
-constexpr int OFF_STAGE = 0;
 constexpr int OFF_W = STAGES * STAGE_BYTES;
 constexpr int OFF_PHI = OFF_W + WOP;   // 2 buffers
-constexpr int OFF_SOP = OFF_PHI + 2 * PHI;
-constexpr int OFF_BAR = OFF_SOP + PHI;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace rdo
 
 
@@ -517,7 +512,6 @@ constexpr int OFF_PHIQ = OFF_W + WOP;
 constexpr int OFF_PHIK = OFF_PHIQ + PHI;
 constexpr int OFF_SOP = OFF_PHIK + PHI;
 constexpr int OFF_BAR = OFF_SOP + PHI;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace cfw
 
 // ---------------------------------------------------------------------------

@@ -33,8 +33,6 @@ constexpr int OFF_SOPT = OFF_W2 + W2OP;
 constexpr int OFF_PHIT = OFF_SOPT + WOP;  // Phi_q / D   (MN-major B of dS)
 constexpr int OFF_DPROJ = OFF_PHIT + PHI;
 constexpr int OFF_BAR = OFF_DPROJ + PHI;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
-constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;
 }  // namespace bq
 
 
@@ -51,7 +49,6 @@ constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // dS operand [128 x 32] (B of dV = P
 constexpr int OFF_PHIK = OFF_DSOP + PHI;
 constexpr int OFF_DPROJ = OFF_PHIK + PHI;
 constexpr int OFF_BAR = OFF_DPROJ + PHI;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Z = 16, TM_DV = 128, TM_DX = 256;
 }  // namespace bk
 

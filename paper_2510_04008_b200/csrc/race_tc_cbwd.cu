@@ -65,7 +65,7 @@ constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_q8 shared memory");
 static_assert(OFF_TOK % 128 == 0, "TMA destination alignment");
-constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_ET = 144, TM_PMC = 256,
+constexpr uint32_t TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_ET = 144, TM_PMC = 256,
                    TM_E = 384, TM_DX = 256;
 // W' [16 x 128] (rows = hyperplane pieces, d contiguous, two SW128 64-column sub-tiles) as an MN-major B
 __device__ __forceinline__ uint64_t desc_wT(uint32_t base) { return smem_desc(base, 2048, 1024, kSw128); }
@@ -567,7 +567,7 @@ constexpr int TOK_BYTES = (256 + CH * ROWW) * 4;
 constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 512 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_k8 shared memory");
-constexpr uint32_t TM_PQ = 0, TM_PK = 16, TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_EG = 128, TM_PT = 192, TM_E = 256,
+constexpr uint32_t TM_ZV = 32, TM_Z = 48, TM_DS = 80, TM_EG = 128, TM_PT = 192, TM_E = 256,
                    TM_DX = 256, TM_PMC = 384, TM_DV = 384;
 }  // namespace ck8
 
@@ -613,7 +613,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* fullV = bars + 4;     // [2]
   uint64_t* fullO = bars + 6;     // [2]
   uint64_t* emptyO = bars + 8;    // [2]
-  uint64_t* projf = bars + 10;
   uint64_t* c1 = bars + 11;
   uint64_t* c2 = bars + 12;
   uint64_t* c3 = bars + 13;
@@ -814,7 +813,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       RACE_TRACE(a, 8, gc);
       tc_fence_after();
       if (elect_one()) {
-#pragma unroll
         // dx^ = dproj . W (hi and lo halves of dproj against W' read MN-major)
         umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIQ, 0), cq8::desc_wT(sb + OFF_W), IDC_DX, 0u);
         umma_bf16(tmem + TM_DX, desc_phi_k(sb + OFF_PHIQ, 1), cq8::desc_wT(sb + OFF_W), IDC_DX, 1u);
