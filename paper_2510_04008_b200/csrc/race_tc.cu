@@ -265,12 +265,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 // ===========================================================================
 // K2: non-causal query-side readout  O = Phi_q S_v / (Phi_q A), den = D / T
 // ===========================================================================
-namespace rdo {
-constexpr int STAGES = 3;
-constexpr int STAGE_BYTES = TILE;  // Q, reused as O staging
-constexpr int OFF_W = STAGES * STAGE_BYTES;
-constexpr int OFF_PHI = OFF_W + WOP;   // 2 buffers
-}  // namespace rdo
 
 
 // ---------------------------------------------------------------------------
