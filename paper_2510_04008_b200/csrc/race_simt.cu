@@ -135,6 +135,62 @@ __device__ void load_rows(const Tin* __restrict__ src, int rows, int cols, float
   }
 }
 
+// two load_rows at once: all loads of both tiles' 128-column blocks are in flight together
+template <typename Tin>
+__device__ void load_rows2(const Tin* __restrict__ srcA, int colsA, float* dstA, int ldA, float* scaleA,
+                           const Tin* __restrict__ srcB, int colsB, float* dstB, int ldB, float* scaleB, int rows,
+                           bool normalize) {
+  constexpr int RPW = TILE / (NT / 32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (colsA > 128 || colsB > 128) {  // wide rows: one tile after the other
+    load_rows<Tin>(srcA, rows, colsA, dstA, ldA, scaleA, normalize);
+    load_rows<Tin>(srcB, rows, colsB, dstB, ldB, scaleB, normalize);
+    return;
+  }
+  float xa[RPW][4], xb[RPW][4];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + i * (NT / 32);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = lane + 32 * j;
+      xa[i][j] = (r < rows && c < colsA) ? to_f32(srcA[size_t(r) * colsA + c]) : 0.f;
+      xb[i][j] = (r < rows && c < colsB) ? to_f32(srcB[size_t(r) * colsB + c]) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + i * (NT / 32);
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = lane + 32 * j;
+      if (c < colsA) {
+        dstA[r * ldA + c] = xa[i][j];
+        sa = fmaf(xa[i][j], xa[i][j], sa);
+      }
+      if (c < colsB) {
+        dstB[r * ldB + c] = xb[i][j];
+        sb = fmaf(xb[i][j], xb[i][j], sb);
+      }
+    }
+    if (scaleA) {
+      sa = warp_sum(sa);
+      if (lane == 0) {
+        const float nrm = sqrtf(sa);
+        scaleA[r] = normalize ? (nrm < kZeroRowEps ? -1.f : nrm) : 1.f;
+      }
+    }
+    if (scaleB) {
+      sb = warp_sum(sb);
+      if (lane == 0) {
+        const float nrm = sqrtf(sb);
+        scaleB[r] = normalize ? (nrm < kZeroRowEps ? -1.f : nrm) : 1.f;
+      }
+    }
+  }
+}
+
 // V (or dO) tile with an appended ones column at index dv (1 for valid rows).
 template <typename Tin>
 __device__ void load_v_ones(const Tin* __restrict__ src, int rows, int dv, float* dst, int ld) {
@@ -470,8 +526,8 @@ __global__ void __launch_bounds__(NT, 2) k_causal_fwd(Geo g, const Tin* __restri
   for (int64_t t0 = rg.begin; t0 < rg.end; t0 += TILE) {
     const int rows = int(rg.end - t0 < TILE ? rg.end - t0 : TILE);
     __syncthreads();
-    load_rows<Tin>(q + (bh * g.N + t0) * g.d, rows, g.d, xq, pl.ldx, rowv + kScQ * TILE, g.normalize);
-    load_rows<Tin>(k + (bh * g.N + t0) * g.d, rows, g.d, xk, pl.ldx, rowv + kScK * TILE, g.normalize);
+    load_rows2<Tin>(q + (bh * g.N + t0) * g.d, g.d, xq, pl.ldx, rowv + kScQ * TILE, k + (bh * g.N + t0) * g.d, g.d,
+                    xk, pl.ldx, rowv + kScK * TILE, rows, g.normalize);
     load_v_ones<Tin>(v + (bh * g.N + t0) * g.dv, rows, g.dv, vs, pl.ldv);
     __syncthreads();
     tile_features_n(pl, 2, xq, rowv + kScQ * TILE, phq, nullptr, xk, rowv + kScK * TILE, phk, nullptr, ws, g.beta);
