@@ -966,8 +966,8 @@ __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, i
 // ---------------------------------------------------------------------------
 template <typename K>
 static cudaError_t prep(K kernel, size_t smem) {
-  if (smem > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  return cudaSuccess;
+  // always set (also below 48 KB): resolves the kernel handle before the first launch
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
 }
 
 #define RACE_LAUNCH(KER, NEED, ...)                                                      \
