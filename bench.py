@@ -49,7 +49,16 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-max-context", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--n-total", type=int, default=0,
+                    help="BASELINE configs[3] mode: tokens of the whole sharded sequence (strong scaling; "
+                         "each rank owns n_total / world); default: --n tokens per GPU (weak scaling)")
+    ap.add_argument("--sharded-64m-total", type=int, default=64 << 20,
+                    help="sequence length of the sharded configs[3] run appended to multi-GPU lines")
+    args = ap.parse_args()
+    if args.n_total:
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        args.n = args.n_total // world
+    return args
 
 
 def _config(args, world):
@@ -59,6 +68,7 @@ def _config(args, world):
         "batch": 1, "heads": HEADS, "head_dim": DIM, "seq_len": args.n * world, "tokens_per_gpu": args.n,
         "P": P_, "L": L_, "M": 1, "beta": BETA, "causal": not args.noncausal,
         "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
+        "scaling_mode": "strong (fixed total sequence, --n-total)" if args.n_total else "weak (fixed tokens per GPU)",
         "l2": "inputs (Q,K,V,dO = 4 x H*N*d) exceed the 126 MB L2; no flush needed",
     }
 
@@ -93,6 +103,69 @@ def cpu_threads():
 _BLAS_LIMIT = None
 
 
+def _host_facts():
+    """CPU model, core count, numpy / BLAS versions of this host."""
+    import platform
+
+    import numpy as np
+
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = []
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [{"api": i.get("internal_api"), "version": i.get("version"), "threads": i.get("num_threads")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
+def _reference_package():
+    """The UNMODIFIED reference from baseline/_ref (pip-installed there), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "race_attention")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import race_attention
+
+        return race_attention
+    except Exception:
+        return None
+
+
+def reference_step(ra, n_sample, causal, seed=0):
+    """One fwd+bwd of the H=4 layer through the reference's public API, exactly as its own
+    benchmark runs a RACE row (ra/bench.py:172-178: per head race_attention + race_attention_vjp with
+    seed + head), on inputs drawn as ra/bench.py:161-169 draws them (float32, ra/bench.py:197)."""
+    import dataclasses
+
+    import numpy as np
+
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(n_sample,)))
+    per_head = []
+    for _ in range(HEADS):
+        q, k, v, g = (rng.standard_normal((n_sample, DIM)).astype(np.float32) for _ in range(4))
+        per_head.append((ra.AttnInputs(q, k, v), g))
+    sketch = ra.SketchConfig(hyperplanes=P_, tables=L_, beta=BETA, seed=0, causal=causal)
+    t0 = time.perf_counter()
+    for h, (inp, g) in enumerate(per_head):
+        cfg = dataclasses.replace(sketch, seed=sketch.seed + h)
+        ra.race_attention(inp, cfg)
+        ra.race_attention_vjp(inp, cfg, g)
+    return time.perf_counter() - t0
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -107,22 +180,35 @@ def run_reference(args, world, rank):
         pass
     causal = not args.noncausal
     n_sample = 4096 if causal else 16384
+    ra = _reference_package()
+    if ra is not None:
+        kind, what = "reference", "the unmodified reference package (baseline/_ref, race_attention 0.1.0) public API"
+        fn = lambda i: reference_step(ra, n_sample, causal, seed=i)  # noqa: E731
+    else:
+        kind, what = "port", "oracle/race_oracle.py (numpy restatement; baseline/_ref not installed)"
+        fn = lambda i: cpu_reference_step(n_sample, causal, seed=i)  # noqa: E731
     times = []
     for i in range(args.warmup + args.steps):
-        dt = cpu_reference_step(n_sample, causal, seed=i)
+        dt = fn(i)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
     value = n_sample * len(times) / tot
     cores = cpu_threads()
+    config = _config(args, world)
+    config["timed_sample_tokens"] = n_sample
+    config["sample_note"] = (f"each step times a {n_sample}-token sequence of the same layer (CPU RACE cost is "
+                             f"linear in N: the reference's own bench gives equal tokens/s at 4096 and 131072, "
+                             f"BASELINE.md section 2); the declared N would take minutes per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic N(0,1) Q,K,V,dO (ra/bench.py:161-169 order)", "config": _config(args, world),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+        "data": "synthetic N(0,1) Q,K,V,dO (ra/bench.py:161-169 order)", "config": config,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
                          "sample": f"{n_sample}-token {'causal' if causal else 'non-causal'} fwd+bwd, "
-                                   f"H={HEADS}, d={DIM}, f32, per step (oracle/race_oracle.py)"},
+                                   f"H={HEADS}, d={DIM}, f32, per step, through {what}"},
+        "host": _host_facts(),
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -358,18 +444,105 @@ def gpt_train_step(dev, steps=5, warmup=3):
 # ---------------------------------------------------------------------------
 # algorithmic bytes per token-head of each kernel (e = element bytes)
 def kernel_bytes(e, causal):
-    """Algorithmic bytes per token-head of each launched kernel (what it must read and write;
-    DESIGN.md section 4).  Causal: the forward also saves the 64-byte sketch row per token,
-    which lets each backward pass skip one of the four N x d operands."""
+    """(compulsory, intermediate) bytes per token-head of each launched kernel.
+
+    compulsory = the kernel's share of the layer's N x d tensors and den (Q, K, V, O, dO
+    read / O, dQ, dK, dV, den written); intermediate = what our decomposition adds: the 64-byte causal
+    sketch row per token (16 fp32: q and k projections + norms, which let each backward pass skip
+    one of the N x d operands) and the 1/D, -rho/D normaliser terms.  Re-reads of an input by a
+    second kernel (V in the causal forward) count as that kernel's compulsory input."""
     d = dv = DIM
-    rows = 64  # sketch row: 16 fp32 (q and k projections + norms)
+    rows = 64
     if causal:
-        return {"kside_partials": (d + dv) * e + rows // 2,                 # read K, V; write k half rows
-                "fwd_causal": (d + dv) * e + rows + dv * e + 4 + rows // 2,  # read Q, V, rows; write O, den, q half
-                "bwd_causal_q": (d + 2 * dv) * e + rows + d * e + 8,        # read Q, V, dO, rows; write dQ, rden, gden
-                "bwd_causal_k": (d + 2 * dv) * e + rows + 8 + (d + dv) * e}  # read K, V, dO, rows, rden, gden; write dK, dV
-    return {"kside_partials": (d + dv) * e, "fwd_readout": d * e + dv * e + 4,
-            "bwd_qside": (d + dv) * e + d * e, "bwd_kside": 2 * (d + dv) * e}
+        return {"kside_partials": ((d + dv) * e, rows // 2),                    # read K, V; write k half rows
+                "fwd_causal": ((d + dv) * e + dv * e + 4, rows + rows // 2),    # read Q, V, rows; write O, den, q half
+                "bwd_causal_q": ((d + 2 * dv) * e + d * e, rows + 8),           # read Q, V, dO, rows; write dQ, rden, gden
+                "bwd_causal_k": ((d + 2 * dv) * e + (d + dv) * e, rows + 8)}    # read K, V, dO, rows, rden, gden; write dK, dV
+    return {"kside_partials": ((d + dv) * e, 0), "fwd_readout": (d * e + dv * e + 4, 0),
+            "bwd_qside": ((d + dv) * e + d * e, 0), "bwd_kside": (2 * (d + dv) * e, 0)}
+
+
+def sharded_run(dev, world, n_total, dtype, causal=True, steps=3):
+    """BASELINE configs[3]: one causal fwd+bwd of a B=1, H=4, d=128 layer over an n_total-token
+    sequence sequence-sharded across the world (rank r owns tokens [r n/G, (r+1) n/G)), bucket
+    tables exchanged by all_gather + fixed-order exclusive prefix / suffix (sharded.py).  Device
+    time, max over ranks.  Every rank first reserves the step's memory and the ranks agree on it
+    (all_reduce of an OOM flag) before any collective, so an out-of-memory rank cannot strand
+    the others in a collective."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_04008_b200 as rb
+    from paper_2510_04008_b200.sharded import TorchDistComm, shard_bounds, sharded_backward, sharded_forward
+
+    rank = dist.get_rank()
+    lo, hi = shard_bounds(n_total, world, rank)
+    n = hi - lo
+    e = 2 if dtype == torch.bfloat16 else 4
+    cfg = rb.SketchConfig(hyperplanes=P_, tables=L_, beta=BETA, seed=0, causal=causal)
+    w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
+    p = cfg.params()
+    comm = TorchDistComm()
+    bad = torch.zeros(1, device=dev)
+    tensors = []
+    try:
+        gen = torch.Generator(device=dev).manual_seed(77 + rank)
+        tensors = [torch.randn((1, HEADS, n, DIM), generator=gen, device=dev, dtype=dtype) for _ in range(4)]
+        # the step's own allocations (O, dQ, dK, dV + den / state / workspace) reserved up front
+        reserve = torch.empty(int(n * HEADS * (4 * DIM * e + 160)), dtype=torch.uint8, device=dev)
+        del reserve
+    except torch.cuda.OutOfMemoryError:
+        bad.fill_(1)
+    dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    if bad.item():
+        del tensors
+        torch.cuda.empty_cache()
+        return {"tokens_total": n_total, "world": world, "tokens_per_gpu": n, "error": "out of memory on a rank"}
+    q, k, v, g = tensors
+
+    def step():
+        o, den, st = sharded_forward(q, k, v, w, p, comm=comm)
+        del o
+        return sharded_backward(q, k, v, w, g, p, st, comm=comm)
+
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(steps):
+        grads = step()
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([ev[0].elapsed_time(ev[1]) / steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    finite = torch.tensor([float(all(bool(torch.isfinite(t[0, :, -1].float()).all()) for t in grads))], device=dev)
+    dist.all_reduce(finite, op=dist.ReduceOp.MIN)
+    del q, k, v, g, tensors, grads
+    torch.cuda.empty_cache()
+    msf = float(ms.item())
+    return {"tokens_total": n_total, "world": world, "tokens_per_gpu": n, "causal": causal,
+            "ms_fwd_bwd": round(msf, 3), "tokens_per_s": n_total / (msf / 1e3), "finite": bool(finite.item()),
+            "exchange": "all_gather of H x F x (dv+1) fp32 totals + fixed-order exclusive prefix / suffix"}
+
+
+def sharded_max_context(dev, world, dtype):
+    """Largest total sequence (multiple of world x 1 Mi) whose sharded causal fwd+bwd runs, stepping
+    down 1 Mi tokens per rank from the free-memory estimate (the ranks agree on each attempt)."""
+    import torch
+    import torch.distributed as dist
+
+    e = 2 if dtype == torch.bfloat16 else 4
+    free, _ = torch.cuda.mem_get_info(dev)
+    per = torch.tensor([int(free * 0.95 / (HEADS * (8 * DIM * e + 160))) >> 20], device=dev)
+    dist.all_reduce(per, op=dist.ReduceOp.MIN)
+    m = int(per.item())
+    while m >= 1:
+        r = sharded_run(dev, world, (m << 20) * world, dtype, steps=1)
+        if "error" not in r:
+            return r
+        m -= 1
+    return {"tokens_total": 0, "error": "nothing fits"}
 
 
 def run_ours(args, world, rank, local_rank):
@@ -521,7 +694,6 @@ def run_ours(args, world, rank, local_rank):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    dom_bytes = kb[dom] * HEADS * n
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     # (tools/ncu_summary.py traffic; same workload: N=131072 per GPU, H=4, bf16)
     ncu_names = {"kside_partials": "k_aggregate2", "fwd_causal": "k_causal_fwd8", "bwd_causal_q": "k_bwd_causal_q8",
@@ -534,12 +706,23 @@ def run_ours(args, world, rank, local_rank):
             traffic = tr[ncu_names[dom]]["dram_bytes"]
     except Exception:
         pass
+    kernels = {}
+    for nm, ms_k in per.items():
+        io, inter = kb.get(nm, (0, 0))
+        io_b, inter_b = io * HEADS * n, inter * HEADS * n
+        kernels[nm] = {"ms": round(ms_k, 4), "compulsory_bytes": io_b, "intermediate_bytes": inter_b,
+                       "frac": round(io_b / (ms_k / 1e3) / 1e9 / peak, 4) if io_b else None,
+                       "frac_with_intermediates": round((io_b + inter_b) / (ms_k / 1e3) / 1e9 / peak, 4) if io_b else None}
+    dom_bytes = kb[dom][0] * HEADS * n
     achieved = dom_bytes / (per[dom] / 1e3) / 1e9
     step_bytes = ((7 * DIM + 5 * DIM) * e + 8) * HEADS * n   # (7d+5dv)e+8 per token-head
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write per launch)", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dom_bytes,
+                "algorithmic_note": "compulsory bytes only (the kernel's N x d reads/writes + den); "
+                                    "kernels[].frac_with_intermediates adds sketch rows / normaliser terms",
+                "kernels": kernels,
                 "kernel_ms": {k2: round(v2, 4) for k2, v2 in per.items()},
                 "step_algorithmic_GBps": step_bytes / (ms_step / 1e3) / 1e9,
                 "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak}
@@ -586,15 +769,22 @@ def run_ours(args, world, rank, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = 8192 if causal else 32768
-        dt = cpu_reference_step(n_s, causal)
-        cpu = {"value": n_s / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+        ra = _reference_package()
+        if ra is not None:
+            dt = reference_step(ra, n_s, causal)
+            kind, what = "reference", "the unmodified reference package (baseline/_ref) public API"
+        else:
+            dt = cpu_reference_step(n_s, causal)
+            kind, what = "port", "oracle/race_oracle.py, the reference algorithm"
+        cpu = {"value": n_s / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
                "sample": f"{n_s}-token {'causal' if causal else 'non-causal'} fwd+bwd, H={HEADS}, d={DIM}, f32 "
-                         f"(oracle/race_oracle.py, the reference algorithm), {dt:.1f} s"}
+                         f"({what}), {dt:.1f} s", "host": _host_facts()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.n_total else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic N(0,1) Q,K,V,dO resident in HBM",
             "config": _config(args, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "cuda_graph": not args.no_graph and world == 1, "clocks": clocks,
@@ -604,14 +794,33 @@ def run_ours(args, world, rank, local_rank):
     return None
 
 
+def _relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-exec as N ranks (one per GPU) so the line
+    never reports one rank for N requested."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, world, rank)
+        run_reference(args, world if launched else args.gpus, rank)
         return
+    if not launched and args.gpus > 1:
+        sys.exit(_relaunch_under_torchrun(args))
+    if launched and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU", file=sys.stderr)
+        sys.exit(2)
     if os.environ.get("RACE_BENCH_ONE_GPU") == "1":  # test hook: every rank on cuda:0 over gloo
         local_rank = 0
     if world > 1:
@@ -625,6 +834,21 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         line = run_ours(args, world, rank, local_rank)
+        if world > 1 and not args.no_max_context:
+            import torch
+            import torch.distributed as dist
+
+            dev = torch.device("cuda", local_rank)
+            dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+            torch.cuda.empty_cache()
+            s64 = sharded_run(dev, world, args.sharded_64m_total, dt)
+            smax = sharded_max_context(dev, world, dt)
+            if line is not None:
+                line["sharded_configs3"] = s64
+                line["max_context_sharded"] = smax
+                line["comm"] = {"backend": dist.get_backend(), "world": world,
+                                "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                                if dist.get_backend() == "nccl" else None}
         if line is not None:
             if world == 1 and not args.no_max_context:
                 import torch

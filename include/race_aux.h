@@ -24,6 +24,13 @@ extern "C" {
 
 #define RACE_F64 2 /* extra element type accepted by the race_aux_* entries */
 
+/* row_normalize (ra/core.py:114-123) when g is NULL: out = x / ||x|| per
+ * row, rows with ||x|| < 1e-12 unchanged.  With g (same dtype and shape
+ * as x): row_normalize_vjp (ra/core.py:126-139), out = (g - (g.x^)x^) /
+ * ||x||, zero-guarded rows pass g through.  out is float64 [n, d].       */
+int race_aux_row_normalize(int32_t dtype, int64_t n, int32_t d, const void* x,
+                           const void* g, double* out, void* stream);
+
 /* soft_features of every table (ra/sketch.py:87-129): phi [n, T * 2^P],
  * column tau * 2^P + r = softmax mass of row x on corner r of table tau.
  * normalize = 1 applies row_normalize first (ra/core.py:114-123), as

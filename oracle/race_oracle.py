@@ -143,13 +143,29 @@ def _prep(q, k, normalize):
     return (unit_rows(q), unit_rows(k)) if normalize else (q, k)
 
 
-def num_den(q, k, v, w_stack, beta, causal, block=4096):
+def key_state(k, v, w_stack, beta, normalize=True, block=65536):
+    """(A [F], B [F, dv]) = sum over the rows of phi(k)^T [1 | v] in float64: the causal block
+    carry of ra/forward.py:105-120 after these rows.  Seeding num_den / vjp with it (``carry=``)
+    checks the tail of a long sequence without re-running its head on the CPU."""
+    w_c = w_stack.astype(np.float64)
+    f = w_stack.shape[0] << w_stack.shape[1]
+    ca, cb = np.zeros(f), np.zeros((f, v.shape[1]))
+    for lo in range(0, k.shape[0], block):
+        kb = k[lo:lo + block].astype(np.float64)
+        pk = features(unit_rows(kb) if normalize else kb, w_c, beta)
+        ca += pk.sum(axis=0)
+        cb += pk.T @ v[lo:lo + block].astype(np.float64)
+    return ca, cb
+
+
+def num_den(q, k, v, w_stack, beta, causal, block=4096, carry=None):
     """Averaged numerator (n, dv) and denominator (n,) in float64 (ra/forward.py:124-144).
 
     q, k are already prepared (normalised).  Non-causal: S = phi(K)^T[V|1]
     accumulated over row blocks (ra/forward.py:84-87), then phi(Q) S
     (ra/forward.py:93-96).  Causal: running block carry with an inclusive
-    cumulative sum inside the block (ra/forward.py:100-121).
+    cumulative sum inside the block (ra/forward.py:100-121), starting from
+    ``carry`` = (A, B) of the rows before q (key_state; default zero).
     """
     n, dv = q.shape[0], v.shape[1]
     t_tot = w_stack.shape[0]
@@ -171,8 +187,7 @@ def num_den(q, k, v, w_stack, beta, causal, block=4096):
             den[lo:lo + block] = pq @ a_c
     else:
         f = t_tot << w_stack.shape[1]
-        carry_a = np.zeros(f)
-        carry_b = np.zeros((f, dv))
+        carry_a, carry_b = (np.zeros(f), np.zeros((f, dv))) if carry is None else carry
         for lo in range(0, n, block):
             hi = min(lo + block, n)
             pk = features(k[lo:hi], w_c, beta).astype(np.float64)
@@ -186,10 +201,10 @@ def num_den(q, k, v, w_stack, beta, causal, block=4096):
     return num / t_tot, den / t_tot
 
 
-def forward(q, k, v, w_stack, beta, causal=False, normalize=True, block=4096):
+def forward(q, k, v, w_stack, beta, causal=False, normalize=True, block=4096, carry=None):
     """(o, den, degenerate_rows) as race_attention returns them (ra/forward.py:147-164)."""
     qp, kp = _prep(q, k, normalize)
-    num, den = num_den(qp, kp, v, w_stack, beta, causal, block)
+    num, den = num_den(qp, kp, v, w_stack, beta, causal, block, carry)
     deg = den <= DEGENERATE_DEN_EPS
     o = np.zeros_like(num)
     np.divide(num, den[:, None], out=o, where=~deg[:, None])
@@ -211,10 +226,13 @@ def _feature_grad(x, w_stack, beta, dphi):
     return out
 
 
-def vjp(q, k, v, w_stack, beta, d_out, causal=False, normalize=True, block=4096):
-    """(dq, dk, dv) as race_attention_vjp returns them (ra/backward.py:184-235)."""
+def vjp(q, k, v, w_stack, beta, d_out, causal=False, normalize=True, block=4096, carry=None):
+    """(dq, dk, dv) as race_attention_vjp returns them (ra/backward.py:184-235).
+
+    Causal ``carry`` = key_state of earlier rows: the rows given are then the TAIL of a longer
+    sequence (nothing follows them, so the reverse scan's suffix carry starts at zero)."""
     qp, kp = _prep(q, k, normalize)
-    num, den = num_den(qp, kp, v, w_stack, beta, causal, block)
+    num, den = num_den(qp, kp, v, w_stack, beta, causal, block, carry)
     t_tot = w_stack.shape[0]
     live = den > DEGENERATE_DEN_EPS
     sden = np.where(live, den, 1.0)
@@ -257,8 +275,7 @@ def vjp(q, k, v, w_stack, beta, d_out, causal=False, normalize=True, block=4096)
         # ra/backward.py:132-181: forward carries, then a reverse suffix scan
         bounds = [(lo, min(lo + block, n)) for lo in range(0, n, block)]
         carries = []
-        ca = np.zeros(f)
-        cb = np.zeros((f, dv))
+        ca, cb = (np.zeros(f), np.zeros((f, dv))) if carry is None else (carry[0].copy(), carry[1].copy())
         for lo, hi in bounds:
             carries.append((ca.copy(), cb.copy()))
             pk = features(kp[lo:hi], w_c, beta).astype(np.float64)

@@ -3,8 +3,10 @@ non-causal, as hand-written sm_100a CUDA behind the reference package's API.
 
 Drop-in names (same meaning as ``race_attention`` in the reference):
 ``SketchConfig, AttnInputs, RaceOutput, RaceGradients, race_attention,
-race_attention_vjp, accumulate_num_den, table_hyperplanes, derive_table_rng,
-gaussian_matrix``.  Device-level: ``race_forward``, ``race_backward``,
+race_attention_vjp, accumulate_num_den, row_normalize, table_hyperplanes,
+derive_table_rng, gaussian_matrix`` plus the validation-side names of
+``ra/__init__.py:58-98`` (soft/hard hashing, theory sweeps, exact attention,
+``bench_scaling``).  Device-level: ``race_forward``, ``race_backward``,
 ``RaceAttentionFunction``, ``RaceAttention`` (nn.Module), and the
 sequence-sharded ``sharded_forward`` / ``sharded_backward``.
 """
@@ -13,6 +15,7 @@ from .attention import (
     DEGENERATE_DEN_EPS,
     ZERO_ROW_EPS,
     AttnInputs,
+    PrecisionWarning,
     RaceGradients,
     RaceOutput,
     SketchConfig,
@@ -22,6 +25,8 @@ from .attention import (
     gaussian_matrix,
     race_attention,
     race_attention_vjp,
+    row_normalize,
+    row_normalize_vjp,
     table_hyperplanes,
 )
 from .functional import (
@@ -52,7 +57,11 @@ from .exact import (
     softmax_attention,
     softmax_attention_vjp,
 )
+from .benchmark import BenchMethod, BenchRecord, bench_scaling, demo_kernel_heatmap
 from .theory import (
+    CollisionReport,
+    RowSumReport,
+    ScalingExperiment,
     bias_sweep,
     collision_identity_check,
     hard_race_attention,
@@ -77,4 +86,7 @@ __all__ = [
     "corner_vector", "dominant_corner_mass", "hard_hash", "hard_race_attention", "kernel_deviation",
     "make_hash_table", "output_rms_error", "race_kernel", "row_sum_stability", "soft_features",
     "softmax_attention", "softmax_attention_vjp", "variance_sweep",
+    # the rest of the reference's top-level names (ra/__init__.py:58-98)
+    "BenchMethod", "BenchRecord", "CollisionReport", "RowSumReport", "ScalingExperiment", "bench_scaling",
+    "demo_kernel_heatmap", "row_normalize", "row_normalize_vjp", "PrecisionWarning",
 ]

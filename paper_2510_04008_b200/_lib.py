@@ -89,6 +89,7 @@ _I32, _I64, _F64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 # include/race_aux.h (validation-side GPU functions; float64 compute)
 RACE_F64 = 2
 AUX_SIGS = {
+    "race_aux_row_normalize": ([_I32, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
     "race_aux_soft_features": ([_I32, _I64, _I32, _P, _P, _I32, _I32, _F64, _I32, _P, _P], ctypes.c_int),
     "race_aux_hard_hash": ([_I32, _I64, _I32, _P, _P, _I32, _I32, _I32, _P, _P], ctypes.c_int),
     "race_aux_feature_gram": ([_I64, _I64, _I32, _P, _P, _F64, _P, _P], ctypes.c_int),

@@ -13,6 +13,8 @@ Same names, dataclasses, argument meaning and error behaviour as
 * ``race_attention``              ra/forward.py:147-164
 * ``race_attention_vjp``          ra/backward.py:184-235
 * ``accumulate_num_den``          ra/forward.py:124-144
+* ``row_normalize``               ra/core.py:114-123
+* ``row_normalize_vjp``           ra/core.py:126-139
 
 The compute runs on the GPU through the C-ABI (``functional.py``); there is no
 CPU path.  Additions (keyword-only, optional): ``w=`` passes the random
@@ -23,13 +25,17 @@ compatibility; the result is identical for any value (the reference's
 worker-invariance contract, ra/acceptance.py:419-450).
 
 numpy inputs give numpy outputs (o in the input dtype, den float64, as the
-reference); float64 inputs are computed in float32 on the device.  torch
+reference).  float64 inputs are computed in float32 on the device (the B200
+path is fp32-accumulate, rel err ~1e-6 against the reference's float64, inside
+the 1e-3 fp32 tolerance but not the reference's own 1e-10 self-consistency
+bound); each such call emits a ``PrecisionWarning``.  torch
 inputs (float32 / bfloat16) give torch outputs on the input's device.
 """
 
 from __future__ import annotations
 
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -176,6 +182,47 @@ class RaceGradients:
     dv: object
 
 
+def row_normalize(x):
+    """Rows scaled to unit norm; rows with norm < 1e-12 unchanged (ra/core.py:114-123).
+
+    Runs on the GPU in float64 (race_aux_row_normalize); the result has x's container and dtype.
+    On the hot path this step is fused into the kernels (proj(x^) = x W^T / ||x||)."""
+    from . import _aux
+
+    x = _as_matrix(x, "x")
+    xd = _aux.to_dev(x)
+    out = torch.empty(xd.shape, dtype=torch.float64, device=xd.device)
+    _aux.check(_aux.lib().race_aux_row_normalize(_aux.code(xd), xd.shape[0], xd.shape[1], _aux._vp(xd), None,
+                                                 _aux._vp(out), _aux._stream()), "row_normalize")
+    return _aux.back(out, x)
+
+
+def row_normalize_vjp(x_raw, grad_normalized):
+    """Cotangent on row_normalize(x_raw) pulled back to x_raw (ra/core.py:126-139), float64."""
+    from . import _aux
+
+    x = _as_matrix(x_raw, "x_raw")
+    g = _as_matrix(grad_normalized, "grad_normalized")
+    if tuple(g.shape) != tuple(x.shape):
+        raise ValueError(f"grad shape {tuple(g.shape)} does not match x {tuple(x.shape)}")
+    xd, gd = _aux.same_dtype(_aux.to_dev(x), _aux.to_dev(g))
+    out = torch.empty(xd.shape, dtype=torch.float64, device=xd.device)
+    _aux.check(_aux.lib().race_aux_row_normalize(_aux.code(xd), xd.shape[0], xd.shape[1], _aux._vp(xd),
+                                                 _aux._vp(gd), _aux._vp(out), _aux._stream()), "row_normalize_vjp")
+    return _aux.back(out, x, dtype=np.float64) if not isinstance(x, torch.Tensor) else out.to(x.device)
+
+
+class PrecisionWarning(UserWarning):
+    """float64 inputs were computed in float32 on the device."""
+
+
+def _warn_f64(*xs) -> None:
+    if any((isinstance(x, torch.Tensor) and x.dtype == torch.float64) or
+           (not isinstance(x, torch.Tensor) and np.asarray(x).dtype == np.float64) for x in xs):
+        warnings.warn("float64 inputs are computed in float32 on the B200 path (fp32 accumulate; "
+                      "rel err ~1e-6 vs the reference's float64)", PrecisionWarning, stacklevel=3)
+
+
 # ---------------------------------------------------------------------------
 def _device() -> torch.device:
     if not torch.cuda.is_available():
@@ -211,6 +258,7 @@ def race_attention(inp: AttnInputs, cfg: SketchConfig, workers: int = 1, *, w=No
     Rows whose averaged denominator is <= 1e-30 are zeroed and flagged.
     """
     dev = _device()
+    _warn_f64(inp.q, inp.k, inp.v)
     q, k, v = (_to_dev(x, dev) for x in (inp.q, inp.k, inp.v))
     if not (q.dtype == k.dtype == v.dtype):
         q, k, v = q.float(), k.float(), v.float()
@@ -229,6 +277,7 @@ def race_attention_vjp(inp: AttnInputs, cfg: SketchConfig, d_out, workers: int =
     if tuple(d_out.shape) != (inp.n, inp.dim_v):
         raise ValueError(f"d_out shape {tuple(d_out.shape)} does not match output shape {(inp.n, inp.dim_v)}")
     dev = _device()
+    _warn_f64(inp.q, inp.k, inp.v, d_out)
     q, k, v, g = (_to_dev(x, dev) for x in (inp.q, inp.k, inp.v, d_out))
     if not (q.dtype == k.dtype == v.dtype == g.dtype):
         q, k, v, g = q.float(), k.float(), v.float(), g.float()
@@ -237,11 +286,22 @@ def race_attention_vjp(inp: AttnInputs, cfg: SketchConfig, d_out, workers: int =
 
 
 def accumulate_num_den(q, k, v, cfg: SketchConfig, workers: int = 1, *, w=None):
-    """Averaged (num [N, dv], den [N]) float64 on already-prepared q, k (ra/forward.py:124-144)."""
+    """Averaged (num [N, dv], den [N]) float64 on already-prepared q, k (ra/forward.py:124-144).
+
+    One device pass (no row normalisation, as the reference's caller has prepared q, k) gives
+    O = num / den and den; num is recovered as O * den in float64 from the fp32 O, so it is the
+    numerator to fp32 rounding.  Rows whose den is <= 1e-30 have |num| <= max|v| * den (phi >= 0),
+    i.e. |num| <= 1e-30 max|v|, and are returned as 0."""
     inp = AttnInputs(q, k, v)
     dev = _device()
+    _warn_f64(inp.q, inp.k, inp.v)
     qd, kd, vd = (_to_dev(x, dev) for x in (inp.q, inp.k, inp.v))
+    if not (qd.dtype == kd.dtype == vd.dtype):
+        qd, kd, vd = qd.float(), kd.float(), vd.float()
     o, den, _ = race_forward(qd, kd, vd, _w_tensor(cfg, inp.dim, w, dev), cfg.params(normalize=False),
                              want_state=False)
-    num = (o.double() * den.double()[:, None])
-    return num.cpu().numpy(), den.double().cpu().numpy()
+    den64 = den.double()
+    num = o.double() * den64[:, None]
+    if isinstance(inp.q, torch.Tensor):
+        return num.to(inp.q.device), den64.to(inp.q.device)
+    return num.cpu().numpy(), den64.cpu().numpy()

@@ -152,6 +152,10 @@ int group_plan(const race_desc_t* d, race::Geo* g, int* tg) {
 
 int64_t table_elems(const race::Geo& g) { return (int64_t(g.T) << g.P) * (g.dv + 1); }
 
+// causal state = carries [BH, nseg, F, dv+1] then the sketch rows [BH, N, 16]; the rows start on a
+// 256-byte boundary (the kernels write them with 16-byte vector stores / TMA) whatever F, dv, BH, nseg
+int64_t carry_elems(const race::Geo& g) { return (g.BH * g.nseg * table_elems(g) + 63) & ~int64_t(63); }
+
 struct WsLayout {
   float* part;
   float* tables;   // [BH, nseg, E] (enough for carries too)
@@ -363,7 +367,7 @@ int race_state_elems(const race_desc_t* desc, int64_t* elems) {
     *elems = 0;
     return RACE_OK;
   }
-  *elems = g.BH * (g.causal ? g.nseg : 1) * table_elems(g) + (g.causal ? 16 * g.BH * g.N : 0);
+  *elems = g.causal ? carry_elems(g) + 16 * g.BH * g.N : g.BH * table_elems(g);
   return RACE_OK;
 }
 
@@ -515,7 +519,7 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   float* tabs = state ? state : ws.tables;
   if (g.causal) {
     // the aggregation also writes the k halves of the sketch rows, so the scan reads Q, V and those rows
-    float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : ws.rows;
+    float* nrm = state ? state + carry_elems(g) : ws.rows;
     if (int rc = race_kside_partials_rows(desc, k, v, w, ws.part, nrm, workspace, stream)) return rc;
     if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
     return race_fwd_causal_krows(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
@@ -550,7 +554,7 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     if (int rc = race_combine(desc, RACE_COMBINE_TOTAL, ws.dpart, nullptr, ws.dtables, stream)) return rc;
     return race_bwd_kside(desc, k, v, w, ws.dtables, dk, dv, workspace, stream);
   }
-  const float* nrm = state ? state + g.BH * g.nseg * table_elems(g) : nullptr;
+  const float* nrm = state ? state + carry_elems(g) : nullptr;
   if (!nrm && race::tc_supported(g)) {  // once for both passes
     if (int rc = cuda_status(race::tc_project(g, q, k, w, ws.rows, S(stream)), "tc_project")) return rc;
     nrm = ws.rows;

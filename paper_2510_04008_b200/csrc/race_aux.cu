@@ -559,6 +559,36 @@ size_t bwd_smem(int d, int dv) {
   return sizeof(double) * (size_t(TB) * (2 * (d + 1) + 2 * (dv + 1) + 2 * (TB + 1)) + 6 * TB);
 }
 
+// row_normalize (ra/core.py:114-123) and row_normalize_vjp (ra/core.py:126-139): one warp per
+// row, fp64.  Rows with norm < ZERO_ROW_EPS pass through (forward) / pass the cotangent through (VJP).
+template <typename Tin>
+__global__ void k_row_normalize(const Tin* __restrict__ x, const Tin* __restrict__ g, int64_t n, int d,
+                                double* __restrict__ out) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 8 + wid;
+  if (row >= n) return;
+  const Tin* xr = x + row * d;
+  double ss = 0;
+  for (int e = lane; e < d; e += 32) {
+    const double xe = ld(xr, e);
+    ss += xe * xe;
+  }
+  const double nrm = sqrt(warp_sum(ss));
+  const bool small = nrm < kZeroRow;
+  const double scl = small ? 1.0 : nrm;
+  double* orow = out + row * d;
+  if (!g) {
+    for (int e = lane; e < d; e += 32) orow[e] = ld(xr, e) / scl;
+    return;
+  }
+  const Tin* gr = g + row * d;
+  double radial = 0;
+  for (int e = lane; e < d; e += 32) radial += ld(gr, e) * (ld(xr, e) / scl);
+  radial = warp_sum(radial);
+  for (int e = lane; e < d; e += 32)
+    orow[e] = small ? ld(gr, e) : (ld(gr, e) - radial * (ld(xr, e) / scl)) / scl;
+}
+
 // tile height for (d, dv): 32 rows while every accumulator fits kMaxCols columns per thread, else 16
 int pick_tb(int d, int dv) {
   const int mx = d > dv ? d : dv;
@@ -570,6 +600,18 @@ int pick_tb(int d, int dv) {
 }  // namespace
 
 extern "C" {
+
+int race_aux_row_normalize(int32_t dtype, int64_t n, int32_t d, const void* x, const void* g, double* out,
+                           void* stream) {
+  if (n < 0 || d < 1) return bad("row_normalize: bad shape");
+  if (n == 0) return RACE_OK;
+  return dispatch(dtype, [&](auto tag) {
+    using T = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+    k_row_normalize<T><<<unsigned((n + 7) / 8), 256, 0, S(stream)>>>(static_cast<const T*>(x),
+                                                                      static_cast<const T*>(g), n, d, out);
+    return launched("row_normalize");
+  });
+}
 
 int race_aux_soft_features(int32_t dtype, int64_t n, int32_t d, const void* x, const double* w, int32_t hyperplanes,
                            int32_t tables, double beta, int32_t normalize, double* phi, void* stream) {

@@ -1095,11 +1095,7 @@ unsigned* debug_progress_device() {
 bool tc_supported(const Geo& g) {
   const char* off = getenv("RACE_DISABLE_FAST_PATH");  // read per call: tests flip it
   if (off && off[0] == '1') return false;
-  int dev = 0, major = 0, minor = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-  if (major != 10 || minor != 0) return false;
+  if (!tcfast::device_is_sm100()) return false;
   const int F = g.T << g.P;
   return g.dtype == 1 && g.d == 128 && g.dv == 128 && F <= tcfast::FP && g.T * g.P <= 5 && g.P <= 3 && g.N > 0 &&
          g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 && tcfast::encode_fn() != nullptr;

@@ -7,7 +7,9 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <unordered_map>
 
 #include "race_common.cuh"
 #include "race_internal.h"
@@ -981,15 +983,55 @@ inline Args make_args(const Geo& g) {
   return a;
 }
 
-inline int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+// per-device facts queried once (the per-call path only reads them): bit 0 = queried,
+// bit 1 = sm_100, bits 8.. = SM count
+inline unsigned device_facts() {
+  static std::atomic<unsigned> facts[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 0;
+  if (dev >= 64) dev = 63;
+  unsigned f = facts[dev].load(std::memory_order_relaxed);
+  if (!f) {
+    int major = 0, minor = 0, n = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    f = 1u | ((major == 10 && minor == 0) ? 2u : 0u) | (unsigned(n) << 8);
+    facts[dev].store(f, std::memory_order_relaxed);
   }
-  return n;
+  return f;
+}
+inline bool device_is_sm100() { return (device_facts() & 2u) != 0; }
+inline int num_sms() {
+  const int n = int(device_facts() >> 8);
+  return n > 0 ? n : 148;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): it is a driver call
+// of a few microseconds, and an eager fwd+bwd makes six launches
+inline cudaError_t ensure_smem_attr(const void* kernel, int smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;  // kernel -> mask of devices set at >= smem
+  static std::unordered_map<const void*, int> done_smem;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(kernel);
+    if (it != done.end() && (it->second & bit) && done_smem[kernel] >= smem) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& s = done_smem[kernel];
+  if (s != smem) {  // a new size applies to every device again
+    done[kernel] = 0;
+    s = smem;
+  }
+  done[kernel] |= bit;
+  return cudaSuccess;
 }
 
 inline unsigned grid_for(const Geo& g) {
@@ -999,7 +1041,7 @@ inline unsigned grid_for(const Geo& g) {
 
 template <typename K, typename... Ts>
 cudaError_t launch_nt(K kernel, int nthreads, int smem, unsigned grid, cudaStream_t st, Ts... args) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, nthreads, smem, st>>>(args...);
   note_launch();
@@ -1007,7 +1049,7 @@ cudaError_t launch_nt(K kernel, int nthreads, int smem, unsigned grid, cudaStrea
 }
 template <typename K, typename... Ts>
 cudaError_t launch(K kernel, int smem, unsigned grid, cudaStream_t st, Ts... args) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, NTHREADS, smem, st>>>(args...);
   note_launch();

@@ -15,6 +15,8 @@ reference's (m, l) task order (``ra/forward.py:128``).
 from __future__ import annotations
 
 import ctypes
+import functools
+import os
 from dataclasses import dataclass
 
 import torch
@@ -56,8 +58,8 @@ def _vp(t: torch.Tensor | None) -> ctypes.c_void_p | None:
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream() -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device: torch.device | None = None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 def prepare_w(w: torch.Tensor, p: SketchParams, d: int, device) -> tuple[torch.Tensor, bool, int]:
@@ -78,6 +80,39 @@ def prepare_w(w: torch.Tensor, p: SketchParams, d: int, device) -> tuple[torch.T
     return w.contiguous(), per_head, heads
 
 
+class _Meta:
+    """Per-shape facts from the library (descriptor, segments, workspace and state sizes), queried
+    once per distinct problem: an eager layer call then makes no sizing calls across the C-ABI."""
+
+    __slots__ = ("desc", "dref", "nseg", "seg_tokens", "ws_bytes", "state_elems", "fast")
+
+    def __init__(self, desc):
+        self.desc = desc
+        self.dref = _lib.ref(desc)
+        self.nseg, self.seg_tokens = _lib.segments(desc)
+        self.ws_bytes = _lib.workspace_bytes(desc)
+        self.state_elems = _lib.state_elems(desc)
+        self.fast = _lib.fast_path(desc)
+
+
+_META: dict[tuple, _Meta] = {}
+
+
+def _meta(**kw) -> _Meta:
+    # the fast-path switch is part of the key: tests flip RACE_DISABLE_FAST_PATH at run time
+    key = (tuple(sorted(kw.items())), os.environ.get("RACE_DISABLE_FAST_PATH"), torch.cuda.current_device())
+    m = _META.get(key)
+    if m is None:
+        m = _META[key] = _Meta(_lib.make_desc(**kw))
+    return m
+
+
+def _check_device(dev: torch.device, **tensors) -> None:
+    for name, t in tensors.items():
+        if t is not None and t.device != dev:
+            raise ValueError(f"{name} is on {t.device} but q is on {dev}; all tensors must be on one device")
+
+
 class Problem:
     """Validated shapes + descriptor for one call."""
 
@@ -89,6 +124,7 @@ class Problem:
             raise ValueError(f"unsupported dtype {q.dtype}; use float32 or bfloat16")
         if k.dtype != q.dtype or v.dtype != q.dtype:
             raise ValueError("q, k, v must share one dtype")
+        _check_device(q.device, k=k, v=v)
         if q.shape != k.shape:
             raise ValueError(f"q and k shapes differ: {tuple(q.shape)} vs {tuple(k.shape)}")
         if q.dim() < 2 or v.dim() != q.dim() or v.shape[:-1] != q.shape[:-1]:
@@ -105,35 +141,41 @@ class Problem:
         self.w, per_head, heads = prepare_w(w, p, self.d, q.device)
         if per_head and (len(self.lead) == 0 or self.lead[-1] != heads):
             raise ValueError(f"per-head hyperplanes for {heads} heads but inputs have lead dims {self.lead}")
-        self.desc = _lib.make_desc(
-            dtype=_DTYPES[q.dtype], batch_heads=max(bh, 1), heads=heads, n=self.n, dim=self.d,
-            dim_v=self.dv, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
-            causal=p.causal, normalize=p.normalize, w_per_head=per_head)
-        self.dref = _lib.ref(self.desc)
-        self.nseg, self.seg_tokens = _lib.segments(self.desc)
+        m = _meta(dtype=_DTYPES[q.dtype], batch_heads=max(bh, 1), heads=heads, n=self.n, dim=self.d,
+                  dim_v=self.dv, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
+                  causal=p.causal, normalize=p.normalize, w_per_head=per_head)
+        self.desc, self.dref = m.desc, m.dref
+        self.nseg, self.seg_tokens = m.nseg, m.seg_tokens
+        self._ws_bytes, self._state_elems = m.ws_bytes, m.state_elems
         self.table_elems = (p.tables << p.hyperplanes) * (self.dv + 1)
 
     def ws(self) -> torch.Tensor:
-        return workspace(_lib.workspace_bytes(self.desc), self.device)
+        return workspace(self._ws_bytes, self.device)
+
+    def carry_elems(self) -> int:
+        """Floats of the causal carries [BH, nseg, F, dv+1], rounded up to 64 so the sketch rows that
+        follow them start on a 256-byte boundary (race_state_elems, include/race_b200.h)."""
+        return (self.bh * self.nseg * self.table_elems + 63) & ~63
 
     def state_shape(self) -> tuple[int, ...] | None:
         """Non-causal: the global tables [BH, F, dv+1].  Causal: a flat buffer holding the
-        per-segment carries [BH, nseg, F, dv+1] then the q/k sketch rows [BH, N, 16]
-        (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h).
+        per-segment carries [BH, nseg, F, dv+1] (padded to 64 floats) then the q/k sketch rows
+        [BH, N, 16] (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h).
         None when the tables run in groups (F beyond one kernel pass): the backward
         then recomputes, as the reference does (ra/backward.py:200)."""
-        if _lib.state_elems(self.desc) == 0:
+        if self._state_elems == 0:
             return None
         f = self.p.tables << self.p.hyperplanes
         if self.p.causal:
-            return (self.bh * self.nseg * f * (self.dv + 1) + 16 * self.bh * self.n,)
+            return (self.carry_elems() + 16 * self.bh * self.n,)
         return (self.bh, f, self.dv + 1)
 
     def split_causal_state(self, state: torch.Tensor):
         """(carries [BH, nseg, F, dv+1], sketch rows [BH, N, 16]) views of a causal state buffer."""
         nc = self.bh * self.nseg * self.table_elems
+        off = self.carry_elems()
         return (state[:nc].view(self.bh, self.nseg, self.table_elems),
-                state[nc:].view(self.bh, max(self.n, 0), 16))
+                state[off:].view(self.bh, max(self.n, 0), 16))
 
 
 def _c(t: torch.Tensor) -> torch.Tensor:
@@ -164,6 +206,7 @@ def _race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: boo
         raise ValueError("inplace backward needs contiguous q, k, v")
     q, k, v, d_o = _c(q), _c(k), _c(v), _c(d_o)
     pr = Problem(q, k, v, w, p)
+    _check_device(pr.device, d_o=d_o, state=state)
     if d_o.shape != v.shape or d_o.dtype != v.dtype:
         raise ValueError(f"d_out shape {tuple(d_o.shape)} does not match output shape {tuple(v.shape)}")
     if inplace:
@@ -209,7 +252,22 @@ def _pad(t: torch.Tensor) -> torch.Tensor:
     return torch.nn.functional.pad(t, (0, FAST_DIM - t.shape[-1])).contiguous()
 
 
-def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
+def _on_q_device(fn):
+    """Run fn with q's GPU as the current device: the C library launches on the current device's
+    stream (cudaGetDevice), so a call on cuda:1 tensors while cuda:0 is current must switch."""
+
+    @functools.wraps(fn)
+    def wrapped(q, *args, **kw):
+        if isinstance(q, torch.Tensor) and q.is_cuda and q.device.index != torch.cuda.current_device():
+            with torch.cuda.device(q.device):
+                return fn(q, *args, **kw)
+        return fn(q, *args, **kw)
+
+    return wrapped
+
+
+@_on_q_device
+def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True, pad: bool = True):
     """O, den (float32, the reference's averaged den) and the backward state.
 
     One fwd pass = key-side aggregation -> fixed-order combine -> readout
@@ -224,13 +282,15 @@ def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
     return _race_forward(q, k, v, w, p, want_state=want_state)
 
 
-def race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: bool = False):
+@_on_q_device
+def race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: bool = False, pad: bool = True):
     """(dq, dk, dv).  ``state`` from race_forward avoids re-aggregating K/V.
 
     ``inplace=True`` writes the gradients over q, k, v (which must be contiguous) and returns
     those tensors: the inputs are dead after the backward, so the layer holds 4 instead of 7
-    N x d tensors (race_bwd allows dq, dk, dv to alias q, k, v)."""
-    if _padded_fast(q, v, w, p):
+    N x d tensors (race_bwd allows dq, dk, dv to alias q, k, v).  ``pad`` must match the
+    race_forward call whose state is passed."""
+    if pad and _padded_fast(q, v, w, p):
         d, dv = q.shape[-1], v.shape[-1]
         dq, dk, dvv = _race_backward(_pad(q), _pad(k), _pad(v), _pad(torch.as_tensor(w).to(q.device)), _pad(d_o), p,
                                      state=state, inplace=True)
@@ -247,10 +307,11 @@ class RaceAttentionFunction(torch.autograd.Function):
     """Autograd wrapper: saves the tiny bucket-table state instead of phi."""
 
     @staticmethod
-    def forward(ctx, q, k, v, w, hyperplanes, tables, beta, causal, normalize):
+    def forward(ctx, q, k, v, w, hyperplanes, tables, beta, causal, normalize, pad=True):
         p = SketchParams(hyperplanes, tables, beta, causal, normalize)
-        o, den, state = race_forward(q, k, v, w, p, want_state=True)
+        o, den, state = race_forward(q, k, v, w, p, want_state=True, pad=pad)
         ctx.p = p
+        ctx.pad = pad
         ctx.save_for_backward(q, k, v, w, state)
         ctx.mark_non_differentiable(den)
         return o, den
@@ -258,12 +319,12 @@ class RaceAttentionFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, d_o, d_den):
         q, k, v, w, state = ctx.saved_tensors
-        dq, dk, dv = race_backward(q, k, v, w, d_o, ctx.p, state=state)
-        return dq, dk, dv, None, None, None, None, None, None
+        dq, dk, dv = race_backward(q, k, v, w, d_o, ctx.p, state=state, pad=ctx.pad)
+        return dq, dk, dv, None, None, None, None, None, None, None
 
 
-def race_attention_torch(q, k, v, w, p: SketchParams):
+def race_attention_torch(q, k, v, w, p: SketchParams, pad: bool = True):
     """Differentiable RACE attention on ``[..., N, d]`` CUDA tensors; returns O."""
     o, _ = RaceAttentionFunction.apply(q, k, v, w, p.hyperplanes, p.tables, float(p.beta),
-                                       bool(p.causal), bool(p.normalize))
+                                       bool(p.causal), bool(p.normalize), bool(pad))
     return o

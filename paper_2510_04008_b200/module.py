@@ -43,6 +43,7 @@ class RaceAttention(torch.nn.Module):
         self.cfg = cfg
         self.heads = heads
         self.dim = dim
+        self.pad_head_dim = pad_head_dim
         self.pad = pad_head_dim and dim < FAST_DIM
         self.params_ = SketchParams(cfg.hyperplanes, cfg.total_tables, float(cfg.beta), cfg.causal,
                                     cfg.normalize_inputs)
@@ -56,4 +57,4 @@ class RaceAttention(torch.nn.Module):
             extra = (0, FAST_DIM - self.dim)
             qp, kp, vp = (torch.nn.functional.pad(t, extra) for t in (q, k, v))
             return race_attention_torch(qp, kp, vp, self.w_pad, self.params_)[..., : v.shape[-1]]
-        return race_attention_torch(q, k, v, self.w, self.params_)
+        return race_attention_torch(q, k, v, self.w, self.params_, pad=self.pad_head_dim)

@@ -4,10 +4,10 @@ Rank r owns the contiguous token slice r of every (b, h) sequence (rank order
 = sequence order).  Q/K/V/dO never move; only the bucket tables
 (BH x F x (dv+1) fp32, 16.5 KB at B=1 H=4 P=2 L=2) cross NVLink:
 
-* non-causal fwd: local S_r = phi(K_r)^T[V_r|1] -> all_reduce(sum) -> readout.
+* non-causal fwd: local S_r = phi(K_r)^T[V_r|1] -> all_gather + fixed-order sum -> readout.
 * causal fwd:     local totals -> all_gather -> carry_r = sum_{r'<r} S_r'
                   (fixed order) -> per-segment exclusive prefix -> chunked scan.
-* non-causal bwd: local dS_r -> all_reduce(sum) -> key side.
+* non-causal bwd: local dS_r -> all_gather + fixed-order sum -> key side.
 * causal bwd:     local dS totals -> all_gather -> carry_r = sum_{r'>r} dS_r'
                   -> per-segment exclusive suffix -> reverse scan.
 
@@ -24,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .functional import Problem, SketchParams, _c, _stream, _vp
+from .functional import Problem, SketchParams, _c, _check_device, _on_q_device, _stream, _vp
 
 
 # ---------------------------------------------------------------------------
@@ -44,10 +44,20 @@ class TorchDistComm:
 
 
 def allreduce_tables(local: torch.Tensor, group=None) -> torch.Tensor:
-    """Global S (or dS) = sum over ranks of the local tables (non-causal)."""
-    out = local.clone()
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    """Global S (or dS) = sum over ranks of the local tables (non-causal).
+
+    all_gather + a local sum in rank order 0..G-1 rather than all_reduce: NCCL's reduction order
+    depends on the algorithm it picks (ring / tree / NVLS), so the result could differ in the last
+    bits between runs or world sizes; this keeps the reference's bit-determinism
+    (ra/acceptance.py:419-450) for the price of G x 16.5 KB per call."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return local.clone()
+    world = dist.get_world_size(group)
+    gathered = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(gathered, local.contiguous(), group=group)
+    out = gathered[0].clone()
+    for r in range(1, world):
+        out += gathered[r]
     return out
 
 
@@ -75,6 +85,7 @@ def _combine(pr: Problem, mode: int, part, carry, out):
                "race_combine")
 
 
+@_on_q_device
 def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
     """(o, den, state) for this rank's sequence shard; state feeds sharded_backward."""
     comm = comm or TorchDistComm(group)
@@ -115,11 +126,13 @@ def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
     return o, den, state
 
 
+@_on_q_device
 def sharded_backward(q, k, v, w, d_o, p: SketchParams, state, group=None, comm=None):
     """(dq, dk, dv) for this rank's shard given sharded_forward's state."""
     comm = comm or TorchDistComm(group)
     q, k, v, d_o, state = _c(q), _c(k), _c(v), _c(d_o), _c(state)
     pr = Problem(q, k, v, w, p)
+    _check_device(pr.device, d_o=d_o, state=state)
     L = _lib.lib()
     dev = pr.device
     E = pr.table_elems

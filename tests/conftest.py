@@ -70,3 +70,38 @@ def grad_errs(got, ref, rel_floor: float):
                 for r in ref)
     floor = max(rel_floor * scale, 1e-30)
     return [rel_err(g, r, floor) for g, r in zip(got, ref)]
+
+
+GOLDEN_EXTRA = os.path.join(ROOT, "tests", "golden", "golden_extra.npz")
+
+
+def load_num_den_golden() -> list[dict]:
+    """accumulate_num_den cases of tests/golden/make_extra_golden.py (real reference outputs)."""
+    z = np.load(GOLDEN_EXTRA)
+    out = []
+    for i in range(int(z["nd_count"])):
+        pre = f"nd{i:02d}_"
+        c = {k[len(pre):]: z[k] for k in z.files if k.startswith(pre)}
+        c["index"] = i
+        c["cfg_kwargs"] = dict(hyperplanes=int(c["P"]), tables=int(c["L"]), ensembles=int(c["M"]),
+                               beta=float(c["beta"]), seed=int(c["seed"]), causal=bool(c["causal"]))
+        out.append(c)
+    return out
+
+
+def load_row_normalize_golden() -> dict:
+    z = np.load(GOLDEN_EXTRA)
+    return {k[3:]: z[k] for k in z.files if k.startswith("rn_")}
+
+
+def record_parity(test: str, **errs) -> None:
+    """Append the measured worst errors of a parity test as one JSON line to $RACE_PARITY_LOG
+    (set by the GPU runs whose logs are committed under profiles/); no-op otherwise."""
+    path = os.environ.get("RACE_PARITY_LOG")
+    if not path:
+        return
+    import json
+
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": test, **{k: (float(v) if isinstance(v, (int, float, np.floating)) else v)
+                                             for k, v in errs.items()}}) + "\n")
