@@ -92,7 +92,6 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   if (d->tables < 1) return fail(RACE_EBADSHAPE, "tables must be >= 1");
   if (!(std::isfinite(d->beta) && d->beta > 0.f)) return fail(RACE_EBADSHAPE, "beta must be positive and finite");
   if (d->batch_heads > 65535) return fail(RACE_EUNSUPPORTED, "batch*heads > 65535");
-  if (d->hyperplanes > 10) return fail(RACE_EUNSUPPORTED, "P=%d > 10 corner bits is not supported on the GPU path", d->hyperplanes);
   g->BH = d->batch_heads;
   g->H = d->heads;
   g->N = d->n;
@@ -116,9 +115,12 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   return RACE_OK;
 }
 
-// one pass of the kernels holds all F = T * 2^P buckets of a row in shared memory
+// one pass of the kernels holds all F = T * 2^cb buckets of a row in shared memory (cb = P unless
+// the pass is a corner group); the corner softmax of a pass covers at most kPMax bits
 bool fits(const race::Geo& g) {
-  const int64_t F = int64_t(g.T) << g.P;
+  const int cb = race::pass_corner_bits(g);
+  if (cb > race::kPMax) return false;
+  const int64_t F = int64_t(g.T) << cb;
   if (F > 4096 || F * (g.dv + 1) > (1 << 22)) return false;
   return race::tc_supported(g) || race::simt_max_smem(g) <= 227 * 1024;
 }
@@ -131,26 +133,69 @@ int resolve(const race_desc_t* d, race::Geo* g) {
   return RACE_OK;
 }
 
-// Table groups: the estimator is a sum over tables (ra/forward.py:124-144), so a
-// config whose F does not fit one pass runs as groups of *tg tables each.  tg == T
-// means no grouping.
-int group_plan(const race_desc_t* d, race::Geo* g, int* tg) {
+// Groups: the estimator is a sum over tables (ra/forward.py:124-144) and, within a table, over its
+// corners, so a config whose F does not fit one pass runs as
+//   table groups:  tg tables per pass (cb = 0), or, when even one table does not fit (or P > 10),
+//   corner groups: one table per pass and 2^cb of its corners (cb < P), T * 2^(P - cb) passes.
+// tg == T, cb == 0 means no grouping.
+struct GroupPlan {
+  int tg = 0;  // tables per group
+  int cb = 0;  // corner bits per group (0: whole tables)
+  int64_t count(const race::Geo& g) const {
+    return cb ? int64_t(g.T) << (g.P - cb) : (g.T + tg - 1) / tg;
+  }
+  bool grouped(const race::Geo& g) const { return cb || tg < g.T; }
+};
+
+int group_plan(const race_desc_t* d, race::Geo* g, GroupPlan* gp) {
   if (int rc = resolve_shape(d, g)) return rc;
+  *gp = GroupPlan{};
   if (fits(*g)) {
-    *tg = g->T;
+    gp->tg = g->T;
     return RACE_OK;
   }
   race::Geo s = *g;
-  for (s.T = g->T - 1; s.T >= 1 && !fits(s); --s.T) {
+  if (g->P <= race::kPMax) {
+    for (s.T = g->T - 1; s.T >= 1 && !fits(s); --s.T) {
+    }
+    if (s.T >= 1) {
+      gp->tg = s.T;
+      return RACE_OK;
+    }
   }
-  if (s.T < 1)
-    return fail(RACE_EUNSUPPORTED, "d=%d dv=%d P=%d: even one table exceeds one pass of the GPU kernels", g->d,
-                g->dv, g->P);
-  *tg = s.T;
+  s.T = 1;
+  for (s.cb = (g->P - 1 < race::kPMax ? g->P - 1 : race::kPMax); s.cb >= 1 && !fits(s); --s.cb) {
+  }
+  if (s.cb < 1)
+    return fail(RACE_EUNSUPPORTED, "d=%d dv=%d P=%d: even two corners of one table exceed one pass of the GPU kernels",
+                g->d, g->dv, g->P);
+  if ((int64_t(g->T) << (g->P - s.cb)) > (int64_t(1) << 24))
+    return fail(RACE_EUNSUPPORTED, "P=%d T=%d: more than 2^24 corner groups", g->P, g->T);
+  gp->tg = 1;
+  gp->cb = s.cb;
   return RACE_OK;
 }
 
-int64_t table_elems(const race::Geo& g) { return (int64_t(g.T) << g.P) * (g.dv + 1); }
+// Geo of group i of the plan (table group: tables [t0, t0+cnt); corner group: table t0, high bits chi)
+race::Geo group_geo(const race::Geo& g, const GroupPlan& gp, int64_t i, int* t0, int* cnt) {
+  race::Geo s = g;
+  s.ext_rden = s.ext_gden = nullptr;
+  if (gp.cb) {
+    const int hb = g.P - gp.cb;
+    *t0 = int(i >> hb);
+    *cnt = 1;
+    s.T = 1;
+    s.cb = gp.cb;
+    s.chi = i & ((int64_t(1) << hb) - 1);
+  } else {
+    *t0 = int(i * gp.tg);
+    *cnt = g.T - *t0 < gp.tg ? g.T - *t0 : gp.tg;
+    s.T = *cnt;
+  }
+  return s;
+}
+
+int64_t table_elems(const race::Geo& g) { return (int64_t(g.T) << race::pass_corner_bits(g)) * (g.dv + 1); }
 
 // causal state = carries [BH, nseg, F, dv+1] then the sketch rows [BH, N, 16]; the rows start on a
 // 256-byte boundary (the kernels write them with 16-byte vector stores / TMA) whatever F, dv, BH, nseg
@@ -216,9 +261,9 @@ struct GroupWs {
   size_t bytes;
 };
 
-GroupWs group_ws(const race::Geo& g, int tg, void* base) {
-  race::Geo s = g;
-  s.T = tg;
+GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
+  int t0, tg;
+  const race::Geo s = group_geo(g, gp, 0, &t0, &tg);
   const int64_t tok = g.BH * (g.N > 0 ? g.N : 1);
   const int64_t ptok = g.BH * (g.N > 0 ? (g.N + 3) & ~int64_t(3) : 4);
   const size_t e = g.dtype == RACE_BF16 ? 2 : 4;
@@ -323,10 +368,11 @@ const float* group_w(const race::Geo& g, const float* w, int t0, int cnt, const 
   return ws.w;
 }
 
-int fwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
-                const float* w, void* o, float* den, void* workspace, void* stream, bool final_out);
-int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
-                const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace, void* stream);
+int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
+                const void* v, const float* w, void* o, float* den, void* workspace, void* stream, bool final_out);
+int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
+                const void* v, const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace,
+                void* stream);
 
 }  // namespace
 
@@ -344,8 +390,8 @@ int race_fast_path(const race_desc_t* desc) {
 
 int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens) {
   race::Geo g;
-  int tg;
-  if (int rc = group_plan(desc, &g, &tg)) return rc;
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
   if (nseg) *nseg = g.nseg;
   if (seg_tokens) *seg_tokens = g.seg_tokens;
   return RACE_OK;
@@ -353,17 +399,17 @@ int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens) {
 
 int race_workspace_bytes(const race_desc_t* desc, size_t* bytes) {
   race::Geo g;
-  int tg;
-  if (int rc = group_plan(desc, &g, &tg)) return rc;
-  *bytes = tg == g.T ? ws_layout(g, nullptr).bytes : group_ws(g, tg, nullptr).bytes;
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
+  *bytes = gp.grouped(g) ? group_ws(g, gp, nullptr).bytes : ws_layout(g, nullptr).bytes;
   return RACE_OK;
 }
 
 int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   race::Geo g;
-  int tg;
-  if (int rc = group_plan(desc, &g, &tg)) return rc;
-  if (tg < g.T) {  // table groups: race_bwd recomputes, there is no saved state
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
+  if (gp.grouped(g)) {  // table / corner groups: race_bwd recomputes, there is no saved state
     *elems = 0;
     return RACE_OK;
   }
@@ -507,13 +553,13 @@ int race_bwd_causal_k(const race_desc_t* desc, const void* q, const void* k, con
 int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, void* o,
              float* den, float* state, void* workspace, void* stream) {
   race::Geo g;
-  int tg;
-  if (int rc = group_plan(desc, &g, &tg)) return rc;
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
-  if (tg < g.T) {
+  if (gp.grouped(g)) {
     if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
-    return fwd_grouped(desc, g, tg, q, k, v, w, o, den, workspace, stream, true);
+    return fwd_grouped(desc, g, gp, q, k, v, w, o, den, workspace, stream, true);
   }
   WsLayout ws = ws_layout(g, workspace);
   float* tabs = state ? state : ws.tables;
@@ -532,13 +578,13 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
 int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* v, const float* w, const void* d_o,
              const float* state, void* dq, void* dk, void* dv, void* workspace, void* stream) {
   race::Geo g;
-  int tg;
-  if (int rc = group_plan(desc, &g, &tg)) return rc;
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
-  if (tg < g.T) {
+  if (gp.grouped(g)) {
     if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
-    return bwd_grouped(desc, g, tg, q, k, v, w, d_o, dq, dk, dv, workspace, stream);
+    return bwd_grouped(desc, g, gp, q, k, v, w, d_o, dq, dk, dv, workspace, stream);
   }
   WsLayout ws = ws_layout(g, workspace);
   const float* tabs = state;
@@ -577,22 +623,36 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
 
 namespace {
 
-int fwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
-                const float* w, void* o, float* den, void* workspace, void* stream, bool final_out) {
-  const GroupWs ws = group_ws(g, tg, workspace);
+int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
+                const void* v, const float* w, void* o, float* den, void* workspace, void* stream, bool final_out) {
+  const GroupWs ws = group_ws(g, gp, workspace);
   const int64_t rows = g.BH * g.N;
-  for (int t0 = 0; t0 < g.T; t0 += tg) {
-    const int cnt = g.T - t0 < tg ? g.T - t0 : tg;
-    race_desc_t sd = *desc;
-    sd.tables = cnt;
+  const int64_t ngroups = gp.count(g);
+  const cudaStream_t st = S(stream);
+  for (int64_t i = 0; i < ngroups; ++i) {
+    int t0, cnt;
+    const race::Geo gs = group_geo(g, gp, i, &t0, &cnt);
     cudaError_t e = cudaSuccess;
-    const float* wg = group_w(g, w, t0, cnt, ws, S(stream), &e);
+    const float* wg = group_w(g, w, t0, cnt, ws, st, &e);
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
-    if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, nullptr, ws.sub, stream)) return rc;
+    if (!gp.cb) {  // table group: a plain sub-problem (may run on the tcgen05 path)
+      race_desc_t sd = *desc;
+      sd.tables = cnt;
+      if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, nullptr, ws.sub, stream)) return rc;
+    } else {  // corner group: the generic kernels restricted to the group's corners
+      const WsLayout sub = ws_layout(gs, ws.sub);
+      e = race::simt_aggregate(gs, k, v, wg, sub.part, st);
+      if (e == cudaSuccess)
+        e = race::combine(gs, g.causal ? RACE_COMBINE_PREFIX : RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
+      if (e == cudaSuccess)
+        e = g.causal ? race::simt_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, nullptr, st)
+                     : race::simt_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
+      if (int rc = cuda_status(e, "corner group forward")) return rc;
+    }
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
-      k_group_fwd_acc<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(
-          rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), t0 == 0, ws.num_acc, ws.d_acc);
+      k_group_fwd_acc<T><<<blocks_for(rows * g.dv), 256, 0, st>>>(
+          rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       race::note_launch();
       return cudaGetLastError();
     });
@@ -612,11 +672,12 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void*
 // Backward with table groups: the per-token normalisers 1/D and -(dO.O)/D of the whole
 // estimator come from a grouped forward; each group then runs the generic backward kernels
 // with those normalisers (Geo::ext_rden/ext_gden) and the groups' gradients are summed.
-int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void* q, const void* k, const void* v,
-                const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace, void* stream) {
-  const GroupWs ws = group_ws(g, tg, workspace);
+int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
+                const void* v, const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace,
+                void* stream) {
+  const GroupWs ws = group_ws(g, gp, workspace);
   const int64_t rows = g.BH * g.N;
-  if (int rc = fwd_grouped(desc, g, tg, q, k, v, w, nullptr, nullptr, workspace, stream, false)) return rc;
+  if (int rc = fwd_grouped(desc, g, gp, q, k, v, w, nullptr, nullptr, workspace, stream, false)) return rc;
   cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
     k_group_rg<T><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
@@ -626,12 +687,10 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void*
     return cudaGetLastError();
   });
   if (int rc = cuda_status(e, "table group normalisers")) return rc;
-  for (int t0 = 0; t0 < g.T; t0 += tg) {
-    const int cnt = g.T - t0 < tg ? g.T - t0 : tg;
-    race_desc_t sd = *desc;
-    sd.tables = cnt;
-    race::Geo gs;
-    if (int rc = resolve(&sd, &gs)) return rc;
+  const int64_t ngroups = gp.count(g);
+  for (int64_t i = 0; i < ngroups; ++i) {
+    int t0, cnt;
+    race::Geo gs = group_geo(g, gp, i, &t0, &cnt);
     gs.ext_rden = ws.rden;
     gs.ext_gden = ws.gden;
     const float* wg = group_w(g, w, t0, cnt, ws, S(stream), &e);
@@ -655,7 +714,7 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, int tg, const void*
     if (int rc = cuda_status(e, "table group backward")) return rc;
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
-      const int first = t0 == 0;
+      const int first = i == 0;
       k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dq), first,
                                                                   ws.dq_acc);
       k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dk), first,

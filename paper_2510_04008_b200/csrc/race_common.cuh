@@ -64,4 +64,19 @@ __device__ __forceinline__ void corner_softmax(const float* u, int P, float beta
   }
 }
 
+// numerically stable logistic sigma(z) (ra/sketch.py:77-84)
+__device__ __forceinline__ float sigmoid_pos(float z) {
+  const float e = expf(-fabsf(z));
+  return z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+}
+
+// one bit's factor of the factored corner probability (ra/sketch.py:120-129):
+// sigma(2 beta c u) with c = -1 if neg_corner else +1, written as match ? 1/(1+e) : e/(1+e),
+// e = exp(-2 beta |u|) (the same form corner_softmax uses, so grouped and ungrouped agree)
+__device__ __forceinline__ float corner_factor(float u, int64_t neg_corner, float beta) {
+  const float e = expf(-2.f * beta * fabsf(u));
+  const bool match = (neg_corner != 0) == (u < 0.f);
+  return (match ? 1.f : e) / (1.f + e);
+}
+
 }  // namespace race

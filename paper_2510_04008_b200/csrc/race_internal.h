@@ -18,7 +18,16 @@ struct Geo {
   // when set, the generic backward kernels use them instead of their own group's D and O
   const float* ext_rden = nullptr;
   const float* ext_gden = nullptr;
+  // corner groups (race_abi.cu, P > 10 or one table beyond one pass): a sub-problem of ONE table
+  // whose kernels see only the 2^cb corners r = (chi << cb) | lo, lo < 2^cb.  phi_r is the factored
+  // product over all P bits (ra/sketch.py:120-129): the low cb bits vary per corner, the high bits
+  // are fixed to chi and contribute one per-row factor.  cb = 0: ungrouped (all P bits).
+  int cb = 0;
+  int64_t chi = 0;
 };
+
+// corners per table a kernel pass sees
+__host__ __device__ inline int pass_corner_bits(const Geo& g) { return g.cb ? g.cb : g.P; }
 
 // every kernel launch in the library bumps this (race_launch_count)
 void note_launch(int n = 1);

@@ -41,6 +41,8 @@ enum Need : unsigned {
 
 struct Plan {
   int d, dv, P, T, R, F, TP;
+  int cb;        // corner bits of this pass (< P for a corner group, Geo::cb), else P
+  int64_t chi;   // fixed high corner bits of a corner group
   int ldx, ldv, ldf, ldS, ldu, ldp;
   // float offsets (all buffers are float)
   int oW, oS, oAcc, oXq, oXk, oDx, oV, oG, oPhq, oPhk, oDph, oY, oU, oDproj, oPm, oEm;
@@ -49,7 +51,8 @@ struct Plan {
   int total;     // floats
 
   __host__ __device__ Plan(const Geo& g, unsigned need) {
-    d = g.d; dv = g.dv; P = g.P; T = g.T; R = 1 << g.P; F = g.T * R; TP = g.T * g.P;
+    d = g.d; dv = g.dv; P = g.P; T = g.T; cb = pass_corner_bits(g); chi = g.chi;
+    R = 1 << cb; F = g.T * R; TP = g.T * g.P;
     ldx = odd_ld(d + 1); ldv = odd_ld(dv + 1); ldf = odd_ld(F); ldS = odd_ld(dv + 1);
     ldu = odd_ld(TP); ldp = TILE + 1;
     int o = 0;
@@ -211,24 +214,37 @@ __device__ void tile_features(const Plan& pl, const float* xs, const float* scal
     const float inv = sc > 0.f ? 1.f / sc : 1.f;
     float u[kPMax];
     const float* x = xs + r * pl.ldx;
+    auto proj = [&](int p) {
+      const float* w = ws + (tau * pl.P + p) * pl.d;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent chains (fixed order)
+      int c = 0;
+      for (; c + 4 <= pl.d; c += 4) {
+        a0 = fmaf(x[c], w[c], a0);
+        a1 = fmaf(x[c + 1], w[c + 1], a1);
+        a2 = fmaf(x[c + 2], w[c + 2], a2);
+        a3 = fmaf(x[c + 3], w[c + 3], a3);
+      }
+      for (; c < pl.d; ++c) a0 = fmaf(x[c], w[c], a0);
+      return tanhf(((a0 + a1) + (a2 + a3)) * inv);
+    };
 #pragma unroll
     for (int p = 0; p < kPMax; ++p) {
-      if (p < pl.P) {
-        const float* w = ws + (tau * pl.P + p) * pl.d;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent chains (fixed order)
-        int c = 0;
-        for (; c + 4 <= pl.d; c += 4) {
-          a0 = fmaf(x[c], w[c], a0);
-          a1 = fmaf(x[c + 1], w[c + 1], a1);
-          a2 = fmaf(x[c + 2], w[c + 2], a2);
-          a3 = fmaf(x[c + 3], w[c + 3], a3);
-        }
-        for (; c < pl.d; ++c) a0 = fmaf(x[c], w[c], a0);
-        u[p] = tanhf(((a0 + a1) + (a2 + a3)) * inv);
+      if (p < pl.cb) {
+        u[p] = proj(p);
         if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = u[p];
       }
     }
-    corner_softmax(u, pl.P, beta, phi + r * pl.ldf + tau * pl.R);
+    float* out = phi + r * pl.ldf + tau * pl.R;
+    corner_softmax(u, pl.cb, beta, out);
+    if (pl.cb < pl.P) {  // corner group: the fixed high bits scale every corner of the pass
+      float m = 1.f;
+      for (int p = pl.cb; p < pl.P; ++p) {
+        const float up = proj(p);
+        if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = up;
+        m *= corner_factor(up, (pl.chi >> (p - pl.cb)) & 1, beta);
+      }
+      for (int rr = 0; rr < pl.R; ++rr) out[rr] *= m;
+    }
   }
 }
 
@@ -262,14 +278,56 @@ __device__ void tile_features_n(const Plan& pl, int n, const float* xs0, const f
     float u[kPMax];
 #pragma unroll
     for (int p = 0; p < kPMax; ++p) {
-      if (p < pl.P) {
+      if (p < pl.cb) {
         u[p] = tanhf(pj[(t * TILE + r) * pl.ldu + tau * pl.P + p] * inv);
         if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = u[p];
       }
     }
-    corner_softmax(u, pl.P, beta, (t ? phi1 : phi0) + r * pl.ldf + tau * pl.R);
+    float* out = (t ? phi1 : phi0) + r * pl.ldf + tau * pl.R;
+    corner_softmax(u, pl.cb, beta, out);
+    if (pl.cb < pl.P) {  // corner group (see tile_features)
+      float m = 1.f;
+      for (int p = pl.cb; p < pl.P; ++p) {
+        const float up = tanhf(pj[(t * TILE + r) * pl.ldu + tau * pl.P + p] * inv);
+        if (u_out) u_out[r * pl.ldu + tau * pl.P + p] = up;
+        m *= corner_factor(up, (pl.chi >> (p - pl.cb)) & 1, beta);
+      }
+      for (int rr = 0; rr < pl.R; ++rr) out[rr] *= m;
+    }
   }
   __syncthreads();  // pj is reused by the next call
+}
+
+// Factored feature VJP of one (row, table) over the corners of a corner group (ra/backward.py:65-88):
+// phi_r = prod_t sigma(2 beta c_rt u_t)  =>  du_t = 2 beta sum_r dphi_r phi_r c_rt (1 - sigma(2 beta c_rt u_t)).
+// Low bits t < cb: split the sum by c_rt = +-1 (S+ and s - S+); high bits: c_t is fixed by chi, so
+// du_t = 2 beta c_t (1 - sigma_t) s.  Sums over groups give the full VJP (it is linear in the corners).
+// Writes dproj_t = du_t (1 - u_t^2) for the table's P projections.
+__device__ __forceinline__ void group_feature_vjp(const Plan& pl, const float* ph, const float* dp, float s,
+                                                  const float* u, float beta, float* dproj) {
+  float splus[kPMax];
+#pragma unroll
+  for (int p = 0; p < kPMax; ++p) splus[p] = 0.f;
+  for (int rr = 0; rr < pl.R; ++rr) {
+    const float x = dp[rr] * ph[rr];
+#pragma unroll
+    for (int p = 0; p < kPMax; ++p)
+      if (p < pl.cb && !((rr >> p) & 1)) splus[p] += x;
+  }
+#pragma unroll
+  for (int p = 0; p < kPMax; ++p) {
+    if (p < pl.cb) {
+      const float sp = sigmoid_pos(2.f * beta * u[p]);  // sigma(2 beta u): c = +1 corners
+      const float du = 2.f * beta * ((1.f - sp) * splus[p] - sp * (s - splus[p]));
+      dproj[p] = du * (1.f - u[p] * u[p]);
+    }
+  }
+  for (int p = pl.cb; p < pl.P; ++p) {
+    const bool neg = (pl.chi >> (p - pl.cb)) & 1;  // c_t = -1
+    const float sp = sigmoid_pos(2.f * beta * u[p]);
+    const float du = 2.f * beta * (neg ? -sp : (1.f - sp)) * s;
+    dproj[p] = du * (1.f - u[p] * u[p]);
+  }
 }
 
 // Feature VJP for the TILE rows: given dphi (smem [TILE][ldf]) produce dx
@@ -288,6 +346,10 @@ __device__ void tile_feature_vjp(const Plan& pl, const float* xs, const float* s
     const float* dp = dphi + r * pl.ldf + tau * pl.R;
     float s = 0.f;
     for (int rr = 0; rr < pl.R; ++rr) s = fmaf(dp[rr], ph[rr], s);
+    if (pl.cb < pl.P) {  // corner group: factored VJP, exact per corner subset (ra/backward.py:65-88)
+      group_feature_vjp(pl, ph, dp, s, u + r * pl.ldu + tau * pl.P, beta, dproj + r * pl.ldu + tau * pl.P);
+      continue;
+    }
     float du[kPMax];
 #pragma unroll
     for (int p = 0; p < kPMax; ++p) du[p] = 0.f;
@@ -1064,7 +1126,7 @@ cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const 
   return RACE_DISPATCH(bwd_causal_k, g, q, k, v, d_o, w, rden, gden, dcar, dk, dv, st);
 }
 cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st) {
-  const int64_t E = int64_t(g.T << g.P) * (g.dv + 1);
+  const int64_t E = (int64_t(g.T) << pass_corner_bits(g)) * (g.dv + 1);
   dim3 grid(unsigned((E + 31) / 32), unsigned(g.BH));
   simt::k_combine<<<grid, 32 * simt::CG, 0, st>>>(g.BH, g.nseg, E, mode, part, carry, out);
   note_launch();

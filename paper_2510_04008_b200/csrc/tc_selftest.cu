@@ -121,6 +121,106 @@ __global__ void __launch_bounds__(128) k_selftest(int M, int N, int K, int a_mn,
   if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
+
+// M = 64 MMAs on the half-subpartition TMEM layout (row 16q + i of the accumulator in DP 32q + i):
+// chain 0 writes D at DP offset 0 and chain 1 at DP offset 16 of the SAME columns, each with its own
+// A ([64 x K] K-major SW128 in smem, or in TMEM for ts = 1 at the chain's DP offset) and a shared B
+// ([N x K] K-major SW128).  D rows 0..63 = chain 0, 64..127 = chain 1.  This is the layout two
+// independent 64-token chains per CTA would use.
+__global__ void __launch_bounds__(128) k_selftest_m64(int N, int K, int ts, const __nv_bfloat16* __restrict__ A,
+                                                      const __nv_bfloat16* __restrict__ B, float* __restrict__ D) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sa0 = smem;            // 16 KB each
+  uint8_t* sa1 = smem + 16384;
+  uint8_t* sb = smem + 32768;     // up to 32 KB
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  for (int i = tid; i < 128 * K; i += 128) {
+    const int m = i / K, k = i % K;
+    uint8_t* base = m < 64 ? sa0 : sa1;
+    *reinterpret_cast<__nv_bfloat16*>(base + canon_off(m & 63, k, 64, K, 0, 128)) = A[i];
+  }
+  for (int i = tid; i < N * K; i += 128) {
+    const int n = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sb + canon_off(n, k, N, K, 0, 128)) = B[i];
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tslot);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  // the accumulator row of this thread's DP: chain (lane >= 16), row 16 * warp + lane % 16
+  const int chain = lane >> 4, row = chain * 64 + warp * 16 + (lane & 15);
+  if (ts) {  // A in TMEM columns 128.. at the same DP as its accumulator row
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t u[16];
+      for (int j = 0; j < 16; ++j) {
+        const int k = 2 * (c0 + j);
+        const __nv_bfloat16 lo = k < K ? A[row * K + k] : __float2bfloat16(0.f);
+        const __nv_bfloat16 hi = k + 1 < K ? A[row * K + k + 1] : __float2bfloat16(0.f);
+        u[j] = uint32_t(*reinterpret_cast<const unsigned short*>(&lo)) |
+               (uint32_t(*reinterpret_cast<const unsigned short*>(&hi)) << 16);
+      }
+      tmem_st16u(tmem + (uint32_t(warp * 32) << 16) + 128 + c0, u);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16(64, N, 0, 0);
+    for (int ch = 0; ch < 2; ++ch) {
+      const uint32_t doff = uint32_t(16 * ch) << 16;
+      for (int kk = 0; kk < K / 16; ++kk) {
+        if (ts)
+          umma_bf16_ts(tmem + doff, tmem + doff + 128 + kk * 8, operand_desc(smem_u32(sb), kk, N, K, 0, 128), idesc,
+                       kk > 0);
+        else
+          umma_bf16(tmem + doff, operand_desc(smem_u32(ch ? sa1 : sa0), kk, 64, K, 0, 128),
+                    operand_desc(smem_u32(sb), kk, N, K, 0, 128), idesc, kk > 0);
+      }
+    }
+    umma_commit(bar);
+  }
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+}  // namespace
+
+extern "C" int tc_selftest_m64(int N, int K, int ts, const void* A, const void* B, float* D, void* stream) {
+  if (N % 16 || N < 16 || N > 128 || K % 64 || K > 128) return 1;
+  const size_t smem = 65536 + 128;
+  cudaFuncSetAttribute(k_selftest_m64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_selftest_m64<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(N, K, ts, static_cast<const __nv_bfloat16*>(A),
+                                                                     static_cast<const __nv_bfloat16*>(B), D);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "tc_selftest_m64 launch: %s\n", cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
+namespace {
 }  // namespace
 
 extern "C" int tc_selftest_gemm(int M, int N, int K, int a_mn, int b_mn, int a_sw, int b_sw, const void* A,

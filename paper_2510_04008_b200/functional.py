@@ -273,8 +273,9 @@ def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True, pad: b
     One fwd pass = key-side aggregation -> fixed-order combine -> readout
     (non-causal) or chunked scan (causal); see race_fwd in race_b200.h.  bf16
     heads narrower than 128 run zero-padded on the tcgen05 kernels (the state
-    then describes the padded problem; race_backward pads the same way)."""
-    if _padded_fast(q, v, w, p):
+    then describes the padded problem; race_backward pads the same way).  ``pad=False`` keeps the
+    native width (generic CUDA-core kernels)."""
+    if pad and _padded_fast(q, v, w, p):
         dv = v.shape[-1]
         o, den, st = _race_forward(_pad(q), _pad(k), _pad(v), _pad(torch.as_tensor(w).to(q.device)), p,
                                    want_state=want_state)

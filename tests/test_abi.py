@@ -56,7 +56,8 @@ def test_segmentation_and_sizes():
     d = _desc()
     nseg, seg = _lib.segments(d)
     assert seg % 128 == 0 and nseg * seg >= 131072 > (nseg - 1) * seg
-    assert _lib.state_elems(d) == 4 * nseg * 8 * 129 + 16 * 4 * 131072  # carries + sketch rows
+    # carries (padded to 64 floats: the sketch rows start 256-byte aligned) + sketch rows
+    assert _lib.state_elems(d) == ((4 * nseg * 8 * 129 + 63) // 64) * 64 + 16 * 4 * 131072
     assert _lib.state_elems(_desc(causal=False)) == 4 * 8 * 129
     assert _lib.workspace_bytes(d) >= 4 * 4 * nseg * 8 * 129
     assert _lib.segments(_desc(n=1)) == (1, 128)
@@ -71,12 +72,29 @@ def test_segmentation_and_sizes():
     (dict(beta=float("inf")), ValueError),
     (dict(dim=0), ValueError),
     (dict(batch_heads=6, heads=4), ValueError),
-    (dict(hyperplanes=11), _lib.RaceUnsupported),
     (dict(dim=4096), _lib.RaceUnsupported),
 ])
 def test_validation(kw, exc):
     with pytest.raises(exc):
         _lib.segments(_desc(**kw))
+
+
+@pytest.mark.parametrize("P", [8, 10, 11, 16, 20])
+def test_wide_sketches_plan_corner_groups(P):
+    """P beyond one kernel pass (and every P in [11, 20], which the reference accepts, ra/core.py:71)
+    runs as table / corner groups: valid sizes, no saved state (the backward recomputes)."""
+    d = _desc(hyperplanes=P, tables=2)
+    assert _lib.segments(d)[0] >= 1
+    assert _lib.workspace_bytes(d) > 0
+    assert _lib.state_elems(d) == 0
+
+
+def test_state_rows_offset_is_aligned():
+    for P, L, n, bh in ((1, 1, 128, 1), (1, 3, 300, 1), (2, 2, 4099, 3)):
+        d = _desc(hyperplanes=P, tables=L, n=n, batch_heads=bh, heads=bh)
+        nseg, _ = _lib.segments(d)
+        carries = bh * nseg * (L << P) * 129
+        assert _lib.state_elems(d) - 16 * bh * n == ((carries + 63) // 64) * 64
 
 
 def test_bad_abi_version():

@@ -52,11 +52,7 @@ def test_golden_fp32(case):
     _cuda()
     cfg = rb.SketchConfig(**case.cfg_kwargs)
     inp = rb.AttnInputs(case["q"], case["k"], case["v"])
-    if cfg.hyperplanes > 10:
-        with pytest.raises(_lib.RaceUnsupported):
-            rb.race_attention(inp, cfg)
-        return
-    out = rb.race_attention(inp, cfg)
+    out = rb.race_attention(inp, cfg)  # P = 11 cases run as corner groups (factored form)
     assert out.o.dtype == np.float64 and out.den.dtype == np.float64
     assert rel_err(out.o, case["o"]) <= TOL_F32
     assert rel_err(out.den, case["den"]) <= TOL_F32
@@ -68,8 +64,7 @@ def test_golden_fp32(case):
     assert max(errs) <= TOL_F32, errs
 
 
-BF16_CASES = [c for c in CASES if all(_is_bf16_valued(c[x]) for x in ("q", "k", "v", "d_out"))
-              and int(c["P"]) <= 10]
+BF16_CASES = [c for c in CASES if all(_is_bf16_valued(c[x]) for x in ("q", "k", "v", "d_out"))]
 
 
 @pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"{c['index']:03d}-{c['tag']}")
@@ -420,7 +415,8 @@ def test_causal_forward_from_kside_rows(n, pl):
         _lib.check(fn(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(car), _vp(o), _vp(den), _vp(rows), _vp(ws), S),
                    "fwd")
         torch.cuda.synchronize()
-        outs.append((o.float().cpu(), den.cpu(), state.cpu()))
+        # carries + sketch rows (not the alignment gap between them, race_state_elems)
+        outs.append((o.float().cpu(), den.cpu(), torch.cat([car.flatten(), rows.flatten()]).cpu()))
     (o0, d0, s0), (o1, d1, s1) = outs
     assert torch.isfinite(s1).all()
     assert rel_err(s1, s0) <= 1e-6

@@ -241,3 +241,47 @@ def test_tensors_on_another_device_raise():
     w = rb.head_hyperplanes(cfg, 1, 128).to(dev)
     with pytest.raises(ValueError):
         rb.race_forward(q, q.cpu(), q, w, cfg.params())
+
+
+# ---------------------------------------------------------------------------
+# 5. sketches beyond one kernel pass: table groups and corner groups (P up to 20)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("shape", [
+    # n, d, dv, P, L, M, beta, dtype
+    (200, 128, 128, 8, 1, 1, 8.0, "f32"),      # one table beyond one pass at d=128: corner groups
+    (150, 128, 128, 10, 2, 1, 4.0, "bf16"),
+    (60, 16, 16, 11, 1, 1, 2.0, "f32"),         # the reference's factored path (ra/sketch.py:120-129)
+    (40, 32, 24, 13, 2, 1, 8.0, "f32"),
+    (24, 8, 8, 16, 1, 2, 1.0, "f32"),
+    (12, 8, 4, 20, 1, 1, 0.5, "f32"),           # SketchConfig's maximum P (ra/core.py:71)
+], ids=lambda s: "n%d_d%d_P%dL%dM%d_%s" % (s[0], s[1], s[3], s[4], s[5], s[7]))
+def test_wide_sketches_vs_oracle(shape, causal):
+    """Forward and VJP of sketches whose F = T 2^P does not fit one kernel pass, against the oracle
+    (explicit softmax for P <= 10, factored per-bit logistic for P > 10: ra/sketch.py:111-129,
+    ra/backward.py:53-90).  fp32 inputs: 1e-3; bf16: 1e-2."""
+    n, d, dv, P, L, M, beta, dt = shape
+    dev = _cuda()
+    rng = np.random.default_rng(P * 100 + n)
+    q, k = (rng.standard_normal((1, 1, n, d)).astype(np.float32) for _ in range(2))
+    v, g = (rng.standard_normal((1, 1, n, dv)).astype(np.float32) for _ in range(2))
+    q[0, 0, 2] = 0.0  # a zero row (pass-through, ra/core.py:120-122)
+    dtype = torch.float32 if dt == "f32" else torch.bfloat16
+    tq, tk, tv, tg = (torch.from_numpy(a).to(dev, dtype) for a in (q, k, v, g))
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, ensembles=M, beta=beta, seed=P, causal=causal)
+    w = rb.head_hyperplanes(cfg, 1, d).to(dev)
+    p = cfg.params()
+    o, den, st = rb.race_forward(tq, tk, tv, w, p)
+    assert st is None  # grouped: the backward recomputes (ra/backward.py:200)
+    dq, dk, dvv = rb.race_backward(tq, tk, tv, w, tg, p)
+    qh, kh, vh, gh = (t[0, 0].double().cpu().numpy() for t in (tq, tk, tv, tg))
+    wh = w[0].double().cpu().numpy()
+    o_r, den_r, _ = ro.forward(qh, kh, vh, wh, beta, causal)
+    ref = ro.vjp(qh, kh, vh, wh, beta, gh, causal)
+    tol = TOL_F32 if dt == "f32" else TOL_BF16
+    e_o, e_den = rel_err(o[0, 0].float().cpu(), o_r), rel_err(den[0, 0].cpu(), den_r)
+    errs = grad_errs([t[0, 0].float().cpu().numpy() for t in (dq, dk, dvv)], ref, GRAD_FLOOR)
+    record_parity(f"wide_P{P}L{L}M{M}_{dt}_{'c' if causal else 'nc'}", o=e_o, den=e_den, dq=errs[0], dk=errs[1],
+                  dv=errs[2])
+    assert e_den <= TOL_F32 and e_o <= tol, (e_o, e_den)
+    assert max(errs) <= tol, errs

@@ -53,3 +53,26 @@ def test_umma_layouts(combo):
     ref = a.double() @ b.double().T
     err = (d.double() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("ts", [0, 1], ids=["smemA", "tmemA"])
+@pytest.mark.parametrize("nk", [(128, 128), (32, 64), (16, 128)], ids=lambda x: "N%dK%d" % x)
+def test_umma_m64_two_chains_share_columns(nk, ts):
+    """Two M=64 accumulators in the same TMEM columns at DP offsets 0 and 16 (half-subpartition
+    layout, CUTLASS TmemAllocMode::Interleaved), A from smem or from TMEM at the chain's offset."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    n, k = nk
+    lib = ctypes.CDLL(LIB)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(n * 7 + k + ts)
+    a = torch.randn(128, k, generator=g, device=dev).to(torch.bfloat16)
+    b = torch.randn(n, k, generator=g, device=dev).to(torch.bfloat16)
+    d = torch.full((128, n), float("nan"), device=dev)
+    rc = lib.tc_selftest_m64(n, k, ts, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                             ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = a.double() @ b.double().T
+    err = (d.double() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
