@@ -9,8 +9,8 @@
  *   accumulate_num_den(q, k, v, cfg, workers)    ra/forward.py:124
  *
  * Each function below replaces one step of those (cited per entry).  The
- * Python drop-in (paper_2510_04008_b200/api.py) binds them through ctypes;
- * INTEGRATION.md shows the binding.
+ * Python drop-in (paper_2510_04008_b200/attention.py over functional.py and
+ * the ctypes table in _lib.py) binds them; INTEGRATION.md shows the binding.
  *
  * Conventions
  *   - All tensor pointers are DEVICE pointers, contiguous, row-major:
@@ -89,12 +89,22 @@ int race_fast_path(const race_desc_t* desc);
  * causal carries and all per-segment partial tables use this split.       */
 int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens);
 
-/* Scratch bytes needed by any entry point below for this desc.           */
+/* Scratch bytes needed by any entry point below for this desc.
+ *
+ * Sketches whose F = T * 2^P buckets do not fit one kernel pass (and every
+ * P in [11, 20], which SketchConfig accepts, ra/core.py:71) run race_fwd /
+ * race_bwd as groups: whole tables per pass, or, when one table does not
+ * fit, 2^cb of its corners per pass with the factored per-bit features
+ * (ra/sketch.py:120-129, ra/backward.py:65-88); the groups' numerators,
+ * denominators and gradients are summed.  Such descs have no saved state
+ * (race_state_elems = 0: race_bwd recomputes, as ra/backward.py:200 does)
+ * and the split-phase entries below return RACE_EUNSUPPORTED for them.    */
 int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
 
 /* Elements (float32) of the state race_fwd saves for race_bwd:
  * non-causal: tables [BH, F, dv+1];
- * causal: carries [BH, nseg, F, dv+1] followed by the sketch rows
+ * causal: carries [BH, nseg, F, dv+1], padded to a multiple of 64 floats
+ *         (so what follows starts 256-byte aligned), then the sketch rows
  *         [BH, N, 16]: per token, floats 0..7 describe q and 8..15 k; slot j
  *         (j < T*P) holds x^.w_j = (x.w_j)/||x|| and slot 7 holds ||x||^2.
  *         The backward rebuilds phi from them instead of re-reading the

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     k_aggregate2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   using namespace agg2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* full = bars;               // [STAGES]
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     k_readout8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
   using namespace rdo8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* full = bars;                    // [STAGES]
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
                   const __grid_constant__ CUtensorMap tmROWS, Args a) {
   using namespace cfw8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* fullqk = bars;       // [2]  Q, K bytes landed
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_project(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, Args a) {
   using namespace prj;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* full = bars;          // [2]

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
                     float* __restrict__ rden, float* __restrict__ gden) {
   using namespace cq8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* fullQ = bars + 0;      // [2]
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
                     const __grid_constant__ CUtensorMap tmDV, Args a) {
   using namespace ck8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t sb = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* fullK = bars + 0;     // K landed (one buffer)

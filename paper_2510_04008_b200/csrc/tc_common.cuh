@@ -89,29 +89,36 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps after ~10 s instead of hanging the GPU.
+// Bounded wait: a protocol bug traps after ~10 s instead of hanging the GPU.  The trap carries no
+// message by default: a printf in this inlined hot loop makes every kernel keep a stack frame and
+// spill live registers around the call (LDL/STL on the compute warps' critical path);
+// -DRACE_MBAR_VERBOSE restores the diagnostic print.
+static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity)
+#ifdef RACE_MBAR_VERBOSE
+{
+  printf("race: mbarrier wait timeout (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
+         smem_u32(bar), parity);
+  __trap();
+}
+#else
+{
+  (void)bar;
+  (void)parity;
+  __trap();
+}
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef RACE_SPIN_WAIT
   if (mbar_test_wait(bar, parity)) return;
   const long long t0s = clock64();
-  while (!mbar_test_wait(bar, parity)) {
-    if (clock64() - t0s > (1ll << 34)) {
-      printf("race: mbarrier wait timeout (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
-             smem_u32(bar), parity);
-      __trap();
-    }
-  }
+  while (!mbar_test_wait(bar, parity))
+    if (clock64() - t0s > (1ll << 34)) mbar_timeout(bar, parity);
   return;
 #endif
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (1ll << 34)) {
-      printf("race: mbarrier wait timeout (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
-             smem_u32(bar), parity);
-      __trap();
-    }
-  }
+  while (!mbar_try_wait(bar, parity))
+    if (clock64() - t0 > (1ll << 34)) mbar_timeout(bar, parity);
 }
 
 // ---------------------------------------------------------------------------

@@ -82,6 +82,13 @@ __device__ __forceinline__ unsigned gtimer_lo() {
       *(volatile unsigned*)&(a_).dbg[148 * 256 - 2 * 148 + 2 * blockIdx.x + (which_)] = gtimer_lo(); \
   } while (0)
 
+// 1024-byte aligned base of the dynamic shared memory, derived by pointer arithmetic on the
+// __shared__ array itself (not through an integer round trip) so that every pointer taken from it
+// stays in the shared address space: the compiler then emits LDS / STS instead of generic LD / ST
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* smem_raw) {
+  return smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+}
+
 // ---------------------------------------------------------------------------
 // role helpers
 // ---------------------------------------------------------------------------

@@ -221,6 +221,65 @@ extern "C" int tc_selftest_m64(int N, int K, int ts, const void* A, const void* 
 }
 
 namespace {
+
+// Layout probe of the 16-lane TMEM load shapes: TMEM cell (dp, col) is filled with dp * 1024 + col
+// by 32x32b stores, then every warp reads its quarter's first 16 DPs (lane offset 0) or second 16
+// (offset 16) with tcgen05.ld.16x64b.x8 / 16x128b.x4 / 16x256b.x2 (8 registers per thread each)
+// and records what each thread's register holds: out[warp][thread][reg].
+template <int SHAPE>
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t* r) {
+  if constexpr (SHAPE == 64)
+    asm volatile("tcgen05.ld.sync.aligned.16x64b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+  else if constexpr (SHAPE == 128)
+    asm volatile("tcgen05.ld.sync.aligned.16x128b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+  else
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(128) k_ld16_probe(int shape, int lane_off, uint32_t* out) {
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc<64>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t dp = warp * 32 + lane;
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    uint32_t u[16];
+    for (int j = 0; j < 16; ++j) u[j] = dp * 1024 + c0 + j;
+    tmem_st16u(tmem + (uint32_t(warp * 32) << 16) + c0, u);
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t r[8];
+  const uint32_t addr = tmem + (uint32_t(warp * 32 + lane_off) << 16);
+  if (shape == 64) ld16<64>(addr, r);
+  else if (shape == 128) ld16<128>(addr, r);
+  else ld16<256>(addr, r);
+  tmem_ld_wait();
+  for (int j = 0; j < 8; ++j) out[(warp * 32 + lane) * 8 + j] = r[j];
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<64>(tmem);
+}
+
+}  // namespace
+
+extern "C" int tc_ld16_probe(int shape, int lane_off, uint32_t* out, void* stream) {
+  k_ld16_probe<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(shape, lane_off, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+namespace {
 }  // namespace
 
 extern "C" int tc_selftest_gemm(int M, int N, int K, int a_mn, int b_mn, int a_sw, int b_sw, const void* A,

@@ -76,3 +76,32 @@ def test_umma_m64_two_chains_share_columns(nk, ts):
     ref = a.double() @ b.double().T
     err = (d.double() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("lane_off", [0, 16])
+@pytest.mark.parametrize("shape", [64, 128, 256])
+def test_tmem_ld16_layout_probe(shape, lane_off, tmp_path):
+    """Record (and check self-consistency of) what tcgen05.ld.16x{64,128,256}b returns per thread:
+    every value is a (dp, col) of the warp's quarter at DP offset lane_off..lane_off+15, every cell
+    of those 16 DPs x 64 columns... read exactly once.  The mapping is logged for the kernels."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    lib = ctypes.CDLL(LIB)
+    out = torch.zeros(128 * 8, dtype=torch.int32, device="cuda")
+    assert lib.tc_ld16_probe(shape, lane_off, ctypes.c_void_p(out.data_ptr()),
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    torch.cuda.synchronize()
+    v = out.view(4, 32, 8).cpu()
+    dp, col = v // 1024, v % 1024
+    lines = []
+    for w in range(4):
+        base = 32 * w + lane_off
+        assert bool(((dp[w] >= base) & (dp[w] < base + 16)).all()), (w, dp[w])
+        cells = {(int(a), int(b)) for a, b in zip(dp[w].flatten(), col[w].flatten())}
+        assert len(cells) == 32 * 8  # no cell twice
+    for t in range(32):
+        lines.append(f"t{t}: " + " ".join(f"({int(dp[0, t, j]) - lane_off},{int(col[0, t, j])})" for j in range(8)))
+    path = os.environ.get("RACE_PARITY_LOG")
+    if path:
+        with open(path.replace(".jsonl", f"_ld16x{shape}b_off{lane_off}.txt"), "w") as f:
+            f.write("\n".join(lines) + "\n")
