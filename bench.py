@@ -376,8 +376,9 @@ def scale_sweep(dev, dtype, sizes=(1 << 20, 1 << 21, 1 << 22, 1 << 23, 12 << 20,
 
 
 def sketch_sweep(dev, dtype, n=131072):
-    """SURVEY 8(d)'s optional sketch sweep: the headline layer with larger sketches (the
-    tcgen05 kernels cover F <= 8; larger F runs on the generic CUDA-core kernels)."""
+    """SURVEY 8(d)'s optional sketch sweep: the headline layer with larger sketches.  One tcgen05
+    pass covers F <= 8 buckets; larger bf16 sketches run as several tcgen05 passes (table groups for
+    P <= 3, corner groups for P = 4, 5; race_group_plan), the rest on the CUDA-core kernels."""
     import torch
 
     import paper_2510_04008_b200 as rb
@@ -387,11 +388,12 @@ def sketch_sweep(dev, dtype, n=131072):
     out = []
     gen = torch.Generator(device=dev).manual_seed(9)
     q, k, v, g = (torch.randn((1, HEADS, n, DIM), generator=gen, device=dev, dtype=dtype) for _ in range(4))
-    for P, L in ((2, 2), (3, 1), (1, 4), (4, 4)):
+    for P, L in ((2, 2), (3, 1), (1, 4), (2, 4), (2, 8), (3, 4), (4, 4), (5, 2)):
         cfg = rb.SketchConfig(hyperplanes=P, tables=L, beta=BETA, seed=0, causal=True)
         w = rb.head_hyperplanes(cfg, HEADS, DIM).to(dev)
         p = cfg.params()
-        fast = _lib.fast_path(Problem(q, k, v, w, p).desc)
+        plan = _lib.group_plan(Problem(q, k, v, w, p).desc)
+        fast = plan["fast"]
         o, den, st = rb.race_forward(q, k, v, w, p)
         rb.race_backward(q, k, v, w, g, p, state=st)
         torch.cuda.synchronize()
@@ -404,6 +406,7 @@ def sketch_sweep(dev, dtype, n=131072):
         torch.cuda.synchronize()
         ms = ev[0].elapsed_time(ev[1]) / 3
         out.append({"P": P, "L": L, "F": L << P, "causal": True, "tokens": n, "fast_path": bool(fast),
+                    "passes": plan["passes"],
                     "ms_fwd_bwd": round(ms, 3), "tokens_per_s": n / (ms / 1e3)})
     return out
 

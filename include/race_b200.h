@@ -84,6 +84,16 @@ int64_t race_launch_count(void);
 /* 0 = generic SIMT kernels, 1 = sm_100a tcgen05/TMA fast path for this desc. */
 int race_fast_path(const race_desc_t* desc);
 
+/* How race_fwd / race_bwd run this desc: `passes` kernel passes (1 = the
+ * whole sketch at once; more = table or corner groups, see
+ * race_workspace_bytes), each over `tables_per_pass` tables and 2^corner_bits
+ * corners per table; fast = 1 when every pass runs on the sm_100a tcgen05
+ * kernels (bf16, d = dv = 128: any P <= 3 via table groups and P = 4, 5 via
+ * corner groups of 8 corners), 0 for the CUDA-core kernels.              */
+int race_group_plan(const race_desc_t* desc, int64_t* passes,
+                    int32_t* tables_per_pass, int32_t* corner_bits,
+                    int32_t* fast);
+
 /* Sequence segmentation shared by every kernel: tokens are cut into nseg
  * contiguous segments of seg_tokens (a multiple of 128) per (b, h).  The
  * causal carries and all per-segment partial tables use this split.       */
@@ -96,9 +106,9 @@ int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens);
  * race_bwd as groups: whole tables per pass, or, when one table does not
  * fit, 2^cb of its corners per pass with the factored per-bit features
  * (ra/sketch.py:120-129, ra/backward.py:65-88); the groups' numerators,
- * denominators and gradients are summed.  Such descs have no saved state
- * (race_state_elems = 0: race_bwd recomputes, as ra/backward.py:200 does)
- * and the split-phase entries below return RACE_EUNSUPPORTED for them.    */
+ * denominators and gradients are summed.  Their state is the summed
+ * numerators and denominators (race_state_elems); the split-phase entries
+ * below return RACE_EUNSUPPORTED for them.                                */
 int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
 
 /* Elements (float32) of the state race_fwd saves for race_bwd:
@@ -108,7 +118,11 @@ int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
  *         [BH, N, 16]: per token, floats 0..7 describe q and 8..15 k; slot j
  *         (j < T*P) holds x^.w_j = (x.w_j)/||x|| and slot 7 holds ||x||^2.
  *         The backward rebuilds phi from them instead of re-reading the
- *         other operand (the generic path fills only the norms).          */
+ *         other operand (the generic path fills only the norms).
+ * grouped descs (race_group_plan passes > 1): the summed (unaveraged)
+ *         numerators [BH, N, dv] then denominators [BH, N] of the whole
+ *         estimator, from which race_bwd takes 1/D and -(dO.O)/D without
+ *         re-running the grouped forward.                                 */
 int race_state_elems(const race_desc_t* desc, int64_t* elems);
 
 /* ---- monolithic single-device entry points ---------------------------- */

@@ -27,7 +27,7 @@ EXPORTS = (
     "race_workspace_bytes", "race_state_elems", "race_fwd", "race_bwd",
     "race_kside_partials", "race_combine", "race_fwd_readout", "race_fwd_causal",
     "race_bwd_qside", "race_bwd_kside", "race_bwd_causal_q", "race_bwd_causal_k",
-    "race_kside_partials_rows", "race_fwd_causal_krows",
+    "race_kside_partials_rows", "race_fwd_causal_krows", "race_group_plan",
 )
 
 
@@ -70,6 +70,7 @@ _SIGS = {
     "race_launch_count": ([], ctypes.c_int64),
     "race_fast_path": ([_P], ctypes.c_int),
     "race_segments": ([_P, _P, _P], ctypes.c_int),
+    "race_group_plan": ([_P, _P, _P, _P, _P], ctypes.c_int),
     "race_workspace_bytes": ([_P, _P], ctypes.c_int),
     "race_state_elems": ([_P, _P], ctypes.c_int),
     "race_fwd": ([_P] * 10, ctypes.c_int),
@@ -182,3 +183,11 @@ def state_elems(desc: RaceDesc) -> int:
 
 def fast_path(desc: RaceDesc) -> bool:
     return bool(lib().race_fast_path(ref(desc)))
+
+
+def group_plan(desc: RaceDesc) -> dict:
+    """{passes, tables_per_pass, corner_bits, fast}: how race_fwd / race_bwd split this sketch."""
+    n, t, c, f = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    check(lib().race_group_plan(ref(desc), ctypes.byref(n), ctypes.byref(t), ctypes.byref(c), ctypes.byref(f)),
+          "race_group_plan")
+    return {"passes": n.value, "tables_per_pass": t.value, "corner_bits": c.value, "fast": bool(f.value)}

@@ -147,9 +147,35 @@ struct GroupPlan {
   bool grouped(const race::Geo& g) const { return cb || tg < g.T; }
 };
 
+// bf16 heads of width 128 whose sketch is beyond one tcgen05 pass still run on the tcgen05 kernels
+// when it splits into passes that each are one (table groups for P <= 3, corner groups of 8 corners
+// for P = 4, 5): several fast passes beat one pass of the CUDA-core kernels by far at these widths
+bool fast_grouping(const race::Geo& g, GroupPlan* gp) {
+  if (g.dtype != RACE_BF16 || g.d != 128 || g.dv != 128 || race::tc_supported(g)) return false;
+  race::Geo s = g;
+  if (g.P <= 3) {
+    int tg = 1;
+    while ((tg + 1) * g.P <= 5 && ((tg + 1) << g.P) <= 8) ++tg;
+    if (tg >= g.T) return false;
+    s.T = tg;
+    if (!race::tc_supported(s)) return false;
+    gp->tg = tg;
+    gp->cb = 0;
+    return true;
+  }
+  if (g.P > 5) return false;
+  s.T = 1;
+  s.cb = 3;
+  if (!race::tc_supported(s)) return false;
+  gp->tg = 1;
+  gp->cb = 3;
+  return true;
+}
+
 int group_plan(const race_desc_t* d, race::Geo* g, GroupPlan* gp) {
   if (int rc = resolve_shape(d, g)) return rc;
   *gp = GroupPlan{};
+  if (fast_grouping(*g, gp)) return RACE_OK;
   if (fits(*g)) {
     gp->tg = g->T;
     return RACE_OK;
@@ -292,30 +318,67 @@ GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
 using race::from_f32;
 using race::to_f32;
 
-// num_acc (+)= o_g * D_g, d_acc (+)= D_g with D_g = den_g * tg (den_g is the group's averaged den)
-template <typename T>
+// 4-wide element access (16-byte fp32 / 8-byte bf16 vectors); callers check the alignment
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xffff0000u));
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+}
+
+// num_acc (+)= o_g * D_g, d_acc (+)= D_g with D_g = den_g * tg (den_g is the group's averaged den);
+// one warp per row (no index division per element), 4 columns per lane step when VEC
+template <typename T, bool VEC>
 __global__ void k_group_fwd_acc(int64_t rows, int dv, const T* __restrict__ o, const float* __restrict__ den, float tg,
                                 int first, float* __restrict__ num_acc, float* __restrict__ d_acc) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows * dv) return;
-  const int64_t r = i / dv;
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
   const float D = den[r] * tg;
-  const float x = to_f32(o[i]) * D;
-  num_acc[i] = first ? x : num_acc[i] + x;
-  if (i % dv == 0) d_acc[r] = first ? D : d_acc[r] + D;
+  const T* orow = o + r * dv;
+  float* nrow = num_acc + r * dv;
+  if (VEC) {
+    for (int c = 4 * lane; c < dv; c += 128) {
+      const float4 x = ld4(orow + c);
+      float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(nrow + c);
+      a.x = fmaf(x.x, D, a.x);
+      a.y = fmaf(x.y, D, a.y);
+      a.z = fmaf(x.z, D, a.z);
+      a.w = fmaf(x.w, D, a.w);
+      st4(nrow + c, a);
+    }
+  } else {
+    for (int c = lane; c < dv; c += 32) nrow[c] = fmaf(to_f32(orow[c]), D, first ? 0.f : nrow[c]);
+  }
+  if (lane == 0) d_acc[r] = first ? D : d_acc[r] + D;
 }
 
 // o = num / D (zero when the averaged den is degenerate, ra/forward.py:157-163), den = D / T
-template <typename T>
+template <typename T, bool VEC>
 __global__ void k_group_fwd_out(int64_t rows, int dv, const float* __restrict__ num_acc,
                                 const float* __restrict__ d_acc, float T_, T* __restrict__ o, float* __restrict__ den) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows * dv) return;
-  const int64_t r = i / dv;
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
   const float D = d_acc[r];
   const bool live = D / T_ > race::kDegenerateDenEps;
-  o[i] = from_f32<T>(live ? num_acc[i] / D : 0.f);
-  if (i % dv == 0) den[r] = D / T_;
+  const float rD = live ? 1.f / D : 0.f;
+  const float* nrow = num_acc + r * dv;
+  T* orow = o + r * dv;
+  if (VEC) {
+    for (int c = 4 * lane; c < dv; c += 128) {
+      const float4 a = ld4(nrow + c);
+      st4(orow + c, make_float4(a.x * rD, a.y * rD, a.z * rD, a.w * rD));
+    }
+  } else {
+    for (int c = lane; c < dv; c += 32) orow[c] = from_f32<T>(live ? nrow[c] / D : 0.f);
+  }
+  if (lane == 0) den[r] = D / T_;
 }
 
 // rden = 1 / D, gden = -(dO . O) / D of the whole estimator; one warp per row
@@ -339,16 +402,28 @@ __global__ void k_group_rg(int64_t BH, int64_t N, int dv, const float* __restric
   }
 }
 
-template <typename T>
-__global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int first, float* __restrict__ acc) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) acc[i] = first ? to_f32(x[i]) : acc[i] + to_f32(x[i]);
-}
-
-template <typename T>
-__global__ void k_group_cast(int64_t n, const float* __restrict__ acc, T* __restrict__ x) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = from_f32<T>(acc[i]);
+// gradient sum over groups: mode 0 acc = x, 1 acc += x, 2 out = (acc + x) in the output dtype
+// (the last group's add fused with the cast); 4 elements per thread when VEC
+template <typename T, bool VEC>
+__global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int mode, float* __restrict__ acc,
+                                 T* __restrict__ out) {
+  const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * (VEC ? 4 : 1);
+  if (i0 >= n) return;
+  if (VEC && i0 + 4 <= n) {
+    float4 v = ld4(x + i0);
+    if (mode) {
+      const float4 a = ld4(acc + i0);
+      v = make_float4(v.x + a.x, v.y + a.y, v.z + a.z, v.w + a.w);
+    }
+    if (mode == 2) st4(out + i0, v);
+    else st4(acc + i0, v);
+    return;
+  }
+  for (int64_t i = i0; i < n && i < i0 + (VEC ? 4 : 1); ++i) {
+    const float v = to_f32(x[i]) + (mode ? acc[i] : 0.f);
+    if (mode == 2) out[i] = from_f32<T>(v);
+    else acc[i] = v;
+  }
 }
 
 unsigned blocks_for(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
@@ -369,10 +444,11 @@ const float* group_w(const race::Geo& g, const float* w, int t0, int cnt, const 
 }
 
 int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
-                const void* v, const float* w, void* o, float* den, void* workspace, void* stream, bool final_out);
+                const void* v, const float* w, void* o, float* den, float* state, void* workspace, void* stream,
+                bool final_out);
 int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
-                const void* v, const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace,
-                void* stream);
+                const void* v, const float* w, const void* d_o, const float* state, void* dq, void* dk, void* dv,
+                void* workspace, void* stream);
 
 }  // namespace
 
@@ -386,6 +462,20 @@ int race_fast_path(const race_desc_t* desc) {
   race::Geo g;
   if (resolve(desc, &g) != RACE_OK) return 0;
   return race::tc_supported(g) ? 1 : 0;
+}
+
+int race_group_plan(const race_desc_t* desc, int64_t* passes, int32_t* tables_per_pass, int32_t* corner_bits,
+                    int32_t* fast) {
+  race::Geo g;
+  GroupPlan gp;
+  if (int rc = group_plan(desc, &g, &gp)) return rc;
+  int t0, cnt;
+  const race::Geo s = gp.grouped(g) ? group_geo(g, gp, 0, &t0, &cnt) : g;
+  if (passes) *passes = gp.grouped(g) ? gp.count(g) : 1;
+  if (tables_per_pass) *tables_per_pass = gp.grouped(g) ? gp.tg : g.T;
+  if (corner_bits) *corner_bits = race::pass_corner_bits(s);
+  if (fast) *fast = race::tc_supported(s) ? 1 : 0;
+  return RACE_OK;
 }
 
 int race_segments(const race_desc_t* desc, int64_t* nseg, int64_t* seg_tokens) {
@@ -409,8 +499,8 @@ int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   race::Geo g;
   GroupPlan gp;
   if (int rc = group_plan(desc, &g, &gp)) return rc;
-  if (gp.grouped(g)) {  // table / corner groups: race_bwd recomputes, there is no saved state
-    *elems = 0;
+  if (gp.grouped(g)) {  // table / corner groups: the summed numerators [BH, N, dv] and denominators [BH, N]
+    *elems = g.BH * g.N * (g.dv + 1);
     return RACE_OK;
   }
   *elems = g.causal ? carry_elems(g) + 16 * g.BH * g.N : g.BH * table_elems(g);
@@ -558,8 +648,7 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
   if (gp.grouped(g)) {
-    if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
-    return fwd_grouped(desc, g, gp, q, k, v, w, o, den, workspace, stream, true);
+    return fwd_grouped(desc, g, gp, q, k, v, w, o, den, state, workspace, stream, true);
   }
   WsLayout ws = ws_layout(g, workspace);
   float* tabs = state ? state : ws.tables;
@@ -583,8 +672,7 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   if (g.N == 0) return RACE_OK;
   if (!workspace) return fail(RACE_EBADSHAPE, "workspace is required");
   if (gp.grouped(g)) {
-    if (state) return fail(RACE_EBADSHAPE, "no state with table groups (race_state_elems is 0)");
-    return bwd_grouped(desc, g, gp, q, k, v, w, d_o, dq, dk, dv, workspace, stream);
+    return bwd_grouped(desc, g, gp, q, k, v, w, d_o, state, dq, dk, dv, workspace, stream);
   }
   WsLayout ws = ws_layout(g, workspace);
   const float* tabs = state;
@@ -623,9 +711,16 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
 
 namespace {
 
+// Forward over the groups: num_acc / d_acc (the workspace's, or the caller's state: [BH, N, dv] then
+// [BH, N]) sum the groups' numerators and denominators; final_out writes o and den from them.
 int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
-                const void* v, const float* w, void* o, float* den, void* workspace, void* stream, bool final_out) {
-  const GroupWs ws = group_ws(g, gp, workspace);
+                const void* v, const float* w, void* o, float* den, float* state, void* workspace, void* stream,
+                bool final_out) {
+  GroupWs ws = group_ws(g, gp, workspace);
+  if (state) {
+    ws.num_acc = state;
+    ws.d_acc = state + g.BH * g.N * g.dv;
+  }
   const int64_t rows = g.BH * g.N;
   const int64_t ngroups = gp.count(g);
   const cudaStream_t st = S(stream);
@@ -639,20 +734,30 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
       race_desc_t sd = *desc;
       sd.tables = cnt;
       if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, nullptr, ws.sub, stream)) return rc;
-    } else {  // corner group: the generic kernels restricted to the group's corners
+    } else {  // corner group: the kernels restricted to the group's corners
       const WsLayout sub = ws_layout(gs, ws.sub);
-      e = race::simt_aggregate(gs, k, v, wg, sub.part, st);
+      const bool fast = race::tc_supported(gs);
+      e = fast ? race::tc_aggregate(gs, k, v, wg, sub.part, nullptr, st) : race::simt_aggregate(gs, k, v, wg, sub.part, st);
       if (e == cudaSuccess)
         e = race::combine(gs, g.causal ? RACE_COMBINE_PREFIX : RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
-      if (e == cudaSuccess)
-        e = g.causal ? race::simt_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, nullptr, st)
-                     : race::simt_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
+      if (e == cudaSuccess) {
+        if (fast)
+          e = g.causal ? race::tc_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, sub.rows, false, st)
+                       : race::tc_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
+        else
+          e = g.causal ? race::simt_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, nullptr, st)
+                       : race::simt_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
+      }
       if (int rc = cuda_status(e, "corner group forward")) return rc;
     }
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
-      k_group_fwd_acc<T><<<blocks_for(rows * g.dv), 256, 0, st>>>(
-          rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
+      if (g.dv % 4 == 0)
+        k_group_fwd_acc<T, true><<<blocks_for(rows * 32), 256, 0, st>>>(
+            rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
+      else
+        k_group_fwd_acc<T, false><<<blocks_for(rows * 32), 256, 0, st>>>(
+            rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       race::note_launch();
       return cudaGetLastError();
     });
@@ -661,8 +766,13 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
   if (!final_out) return RACE_OK;
   cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
-    k_group_fwd_out<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc, float(g.T),
-                                                                       static_cast<T*>(o), den);
+    const bool vec = g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(T))) == 0;
+    if (vec)
+      k_group_fwd_out<T, true><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+                                                                            float(g.T), static_cast<T*>(o), den);
+    else
+      k_group_fwd_out<T, false><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+                                                                             float(g.T), static_cast<T*>(o), den);
     race::note_launch();
     return cudaGetLastError();
   });
@@ -672,12 +782,19 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
 // Backward with table groups: the per-token normalisers 1/D and -(dO.O)/D of the whole
 // estimator come from a grouped forward; each group then runs the generic backward kernels
 // with those normalisers (Geo::ext_rden/ext_gden) and the groups' gradients are summed.
+// Backward over the groups: the whole estimator's 1/D and -(dO.O)/D from the saved sums (state) or a
+// recomputed grouped forward, then each group's backward with those normalisers; gradients summed.
 int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
-                const void* v, const float* w, const void* d_o, void* dq, void* dk, void* dv, void* workspace,
-                void* stream) {
-  const GroupWs ws = group_ws(g, gp, workspace);
+                const void* v, const float* w, const void* d_o, const float* state, void* dq, void* dk, void* dv,
+                void* workspace, void* stream) {
+  GroupWs ws = group_ws(g, gp, workspace);
   const int64_t rows = g.BH * g.N;
-  if (int rc = fwd_grouped(desc, g, gp, q, k, v, w, nullptr, nullptr, workspace, stream, false)) return rc;
+  if (state) {
+    ws.num_acc = const_cast<float*>(state);
+    ws.d_acc = const_cast<float*>(state) + rows * g.dv;
+  } else if (int rc = fwd_grouped(desc, g, gp, q, k, v, w, nullptr, nullptr, nullptr, workspace, stream, false)) {
+    return rc;
+  }
   cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
     k_group_rg<T><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
@@ -697,6 +814,24 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
     const WsLayout sub = ws_layout(gs, ws.sub);
     const cudaStream_t st = S(stream);
+    if (race::tc_supported(gs)) {  // tcgen05 kernels, query side on the whole estimator's 1/D, -rho/D
+      e = race::tc_aggregate(gs, k, v, wg, sub.part, nullptr, st);
+      if (!g.causal) {
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
+        if (e == cudaSuccess) e = race::tc_bwd_q(gs, q, d_o, wg, sub.tables, ws.dq, sub.dpart, st);
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.dpart, nullptr, sub.dtables, st);
+        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, ws.dv, st);
+      } else {
+        if (e == cudaSuccess) e = race::tc_project(gs, q, k, wg, sub.rows, st);
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_PREFIX, sub.part, nullptr, sub.tables, st);
+        if (e == cudaSuccess)
+          e = race::tc_bwd_causal_q(gs, q, k, v, d_o, wg, sub.tables, sub.rows, ws.dq, sub.rden, sub.gden, sub.dpart,
+                                    st);
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_SUFFIX, sub.dpart, nullptr, sub.dtables, st);
+        if (e == cudaSuccess)
+          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, sub.rows, ws.dk, ws.dv, st);
+      }
+    } else {
     e = race::simt_aggregate(gs, k, v, wg, sub.part, st);
     if (!g.causal) {
       if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
@@ -711,30 +846,29 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
       if (e == cudaSuccess)
         e = race::simt_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, ws.dk, ws.dv, st);
     }
+    }
     if (int rc = cuda_status(e, "table group backward")) return rc;
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
-      const int first = i == 0;
-      k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dq), first,
-                                                                  ws.dq_acc);
-      k_group_grad_acc<T><<<blocks_for(rows * g.d), 256, 0, st>>>(rows * g.d, static_cast<const T*>(ws.dk), first,
-                                                                  ws.dk_acc);
-      k_group_grad_acc<T><<<blocks_for(rows * g.dv), 256, 0, st>>>(rows * g.dv, static_cast<const T*>(ws.dv), first,
-                                                                   ws.dv_acc);
+      const int mode = i == 0 ? 0 : (i + 1 == ngroups ? 2 : 1);
+      auto acc = [&](int64_t n, const void* x, float* a, void* out) {
+        const bool vec = (reinterpret_cast<uintptr_t>(out) % (4 * sizeof(T))) == 0;
+        if (vec)
+          k_group_grad_acc<T, true><<<blocks_for((n + 3) / 4), 256, 0, st>>>(n, static_cast<const T*>(x), mode, a,
+                                                                             static_cast<T*>(out));
+        else
+          k_group_grad_acc<T, false><<<blocks_for(n), 256, 0, st>>>(n, static_cast<const T*>(x), mode, a,
+                                                                    static_cast<T*>(out));
+      };
+      acc(rows * g.d, ws.dq, ws.dq_acc, dq);
+      acc(rows * g.d, ws.dk, ws.dk_acc, dk);
+      acc(rows * g.dv, ws.dv, ws.dv_acc, dv);
       race::note_launch(3);
       return cudaGetLastError();
     });
     if (int rc = cuda_status(e, "table group gradient sum")) return rc;
   }
-  e = by_dtype(g.dtype, [&](auto* tag) {
-    using T = std::remove_pointer_t<decltype(tag)>;
-    k_group_cast<T><<<blocks_for(rows * g.d), 256, 0, S(stream)>>>(rows * g.d, ws.dq_acc, static_cast<T*>(dq));
-    k_group_cast<T><<<blocks_for(rows * g.d), 256, 0, S(stream)>>>(rows * g.d, ws.dk_acc, static_cast<T*>(dk));
-    k_group_cast<T><<<blocks_for(rows * g.dv), 256, 0, S(stream)>>>(rows * g.dv, ws.dv_acc, static_cast<T*>(dv));
-    race::note_launch(3);
-    return cudaGetLastError();
-  });
-  return cuda_status(e, "table group gradients");
+  return RACE_OK;  // the last group's accumulation wrote dq, dk, dv
 }
 
 }  // namespace

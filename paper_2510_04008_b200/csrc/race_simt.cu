@@ -24,7 +24,10 @@
 namespace race {
 namespace simt {
 
-constexpr int TILE = 32;   // tokens per tile
+#ifndef RACE_SIMT_TILE
+#define RACE_SIMT_TILE 32
+#endif
+constexpr int TILE = RACE_SIMT_TILE;  // tokens per tile
 constexpr int NT = 256;    // threads per CTA
 
 __host__ __device__ inline int odd_ld(int n) { return n | 1; }

@@ -1096,9 +1096,13 @@ bool tc_supported(const Geo& g) {
   const char* off = getenv("RACE_DISABLE_FAST_PATH");  // read per call: tests flip it
   if (off && off[0] == '1') return false;
   if (!tcfast::device_is_sm100()) return false;
-  const int F = g.T << g.P;
-  return g.dtype == 1 && g.d == 128 && g.dv == 128 && F <= tcfast::FP && g.T * g.P <= 5 && g.P <= 3 && g.N > 0 &&
-         g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 && tcfast::encode_fn() != nullptr;
+  // one pass: F = T * 2^cb <= 8 buckets, T * P <= 5 projections (W' holds three bf16 pieces of each in 16
+  // rows), at most 3 corner bits per table; a corner group (cb < P) is one table of up to 5 hyperplanes
+  const int cb = pass_corner_bits(g);
+  const int F = g.T << cb;
+  return g.dtype == 1 && g.d == 128 && g.dv == 128 && F <= tcfast::FP && g.T * g.P <= 5 && cb <= 3 &&
+         (g.cb == 0 || g.T == 1) && g.N > 0 && g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 &&
+         tcfast::encode_fn() != nullptr;
 }
 
 cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float* w, float* part, float* rows,
@@ -1110,7 +1114,7 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
   a.w = w;
   a.tout = part;
   a.rows_out = rows;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
     case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
     default: return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
@@ -1126,7 +1130,7 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
   a.w = w;
   a.tin = tab;
   a.den = den;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
     case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
     default: return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
@@ -1141,7 +1145,7 @@ cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* 
   Args a = make_args(g);
   a.w = w;
   a.rows_out = rows;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch(k_project<1>, prj::SMEM, grid_for(g), st, mq, mk, a);
     case 2: return launch(k_project<2>, prj::SMEM, grid_for(g), st, mq, mk, a);
     default: return launch(k_project<3>, prj::SMEM, grid_for(g), st, mq, mk, a);
@@ -1163,7 +1167,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.den = den;
   a.rows_out = nrm;
   a.dbg = trace_for("fwd");
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
 #define RACE_FWD8(PP)                                                                                     \
   return krows ? launch_nt(k_causal_fwd8<PP, true>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
                : launch_nt(k_causal_fwd8<PP, false>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)

@@ -254,8 +254,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           num = fmaf(phi[f], y[f], num);
         }
         const bool live = valid && D * invT > kDegenerateDenEps;
-        const float rD = live ? 1.f / D : 0.f;
-        const float rho = num * rD;
+        float rD = live ? 1.f / D : 0.f;
+        float rho = num * rD;
+        if (a.ext_rd) {  // table / corner group: normalisers of the whole estimator
+          const int64_t i = m.bh * a.Np + t + r;
+          rD = valid ? a.ext_rd[i] : 0.f;
+          rho = (valid && rD != 0.f) ? -a.ext_gd[i] / rD : 0.f;
+        }
         float dphi[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
@@ -536,7 +541,7 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   a.w = w;
   a.tin = tab;
   a.tout = dpart;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
     case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
     default: return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
@@ -552,7 +557,7 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
   Args a = make_args(g);
   a.w = w;
   a.tin = dtab;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
     case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
     default: return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);

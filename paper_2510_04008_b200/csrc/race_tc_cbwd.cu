@@ -431,8 +431,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const float D = Dint + (xpar[r] + xpar[128 + r]);
         const float ndt = xpar[256 + r] + xpar[384 + r];
         const bool live = valid && D * invT > kDegenerateDenEps;
-        const float rD = live ? 1.f / D : 0.f;
-        const float rho = (ydot + ndt) * rD;
+        float rD = live ? 1.f / D : 0.f;
+        float rho = (ydot + ndt) * rD;
+        if (a.ext_rd) {  // table / corner group: normalisers of the whole estimator
+          const int64_t i = m.bh * a.Np + t + r;
+          rD = valid ? a.ext_rd[i] : 0.f;
+          rho = (valid && rD != 0.f) ? -a.ext_gd[i] / rD : 0.f;
+        }
         // E~ = tril(E - rho) -> bf16 pairs into TMEM (A of Z)
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(et_ready);
-        if (h == 0 && valid) {
+        if (h == 0 && valid && !a.ext_rd) {
           rden[m.bh * a.Np + t + r] = rD;  // row pitch Np (multiple of 4: 16-byte TMA tiles)
           gden[m.bh * a.Np + t + r] = -rho * rD;
         }
@@ -1070,7 +1075,7 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   if (!nrm) return cudaErrorInvalidValue;  // race_abi.cu always supplies the forward's rows
   CUtensorMap mrows;
   if (!make_map_rows(&mrows, nrm, g.BH * g.N)) return cudaErrorInvalidValue;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
     case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
     default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
@@ -1097,7 +1102,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   if (!make_map_f32_1d(&mrd, rden, g.BH * np, 128) || !make_map_f32_1d(&mgd, gden, g.BH * np, 128) ||
       !make_map_rows(&mrows, nrm, g.BH * g.N))
     return cudaErrorInvalidValue;
-  switch (g.P) {
+  switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
     case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
     default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);

@@ -56,6 +56,13 @@ struct Args {
   float* rows_out;
   int pf;               // chunks of L2 prefetch (cp.async.bulk.prefetch) ahead of the TMA loads
   int ttid;             // compute thread that records the per-chunk trace (RACE_TRACE_TID, default 64)
+  // corner group (Geo::cb, race_abi.cu): one table of P + hb hyperplanes, of whose 2^(P+hb) corners
+  // this pass sees the 2^P with high bits chi; hb = 0 otherwise
+  int hb, chi;
+  // table / corner groups: 1/D and -(dO.O)/D of the WHOLE estimator per token ([BH, Np]); the
+  // query-side backward kernels use them instead of their own group's D and rho
+  const float* ext_rd;
+  const float* ext_gd;
 };
 
 #define RACE_DBG(a_, slot_, val_)                                                        \
@@ -252,6 +259,21 @@ __device__ __forceinline__ float fast_exp_neg(float y) {  // exp(-y)
   return ex2_approx(-1.4426950408889634f * y);
 }
 
+// Corner group (a.hb > 0, one table): the fixed high bits chi of the pass's corners contribute
+// prod_b sigma(2 beta c_b u_{P+b}) to every phi_r (factored form, ra/sketch.py:120-129), with
+// u_j = tanh_of(j) for the projections j = P .. P + hb - 1.
+template <typename U>
+__device__ __forceinline__ float group_weight(const Args& a, U tanh_of) {
+  float m = 1.f;
+  for (int b = 0; b < a.hb; ++b) {
+    const float u = tanh_of(a.P + b);
+    const float e = fast_exp_neg(2.f * a.beta * fabsf(u));
+    const bool match = (((a.chi >> b) & 1) != 0) == (u < 0.f);
+    m *= (match ? 1.f : e) / (1.f + e);
+  }
+  return m;
+}
+
 // features of one row from its 16 projection columns (P compile-time, T <= 8 >> P)
 template <int P>
 __device__ __forceinline__ void row_features(const Args& a, const float* proj, float inv, bool valid, float* phi) {
@@ -272,7 +294,8 @@ __device__ __forceinline__ void row_features(const Args& a, const float* proj, f
         neg[p] = u < 0.f;
         z *= 1.f + e[p];
       }
-      const float rz = 1.f / z;
+      float rz = 1.f / z;
+      if (a.hb) rz *= group_weight(a, [&](int j) { return fast_tanh((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv); });
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         float prod = rz;
@@ -317,7 +340,13 @@ __device__ __forceinline__ void row_features_hat(const Args& a, const float* hat
         neg[p] = uu < 0.f;
         z *= 1.f + e[p];
       }
-      const float rz = 1.f / z;
+      float rz = 1.f / z;
+      if (a.hb)
+        rz *= group_weight(a, [&](int j) {
+          const float uu = fast_tanh(hat[j]);
+          u[j] = uu;
+          return uu;
+        });
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         float prod = rz;
@@ -477,7 +506,15 @@ __device__ __forceinline__ void row_features_u(const Args& a, const float* proj,
         neg[p] = uu < 0.f;
         z *= 1.f + e[p];
       }
-      const float rz = 1.f / z;
+      float rz = 1.f / z;
+      if (a.hb)
+        rz *= group_weight(a, [&](int j) {
+          const float ph = (proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv;
+          const float uu = fast_tanh(ph);
+          phat[j] = ph;
+          u[j] = uu;
+          return uu;
+        });
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         float prod = rz;
@@ -497,6 +534,33 @@ __device__ __forceinline__ void row_feature_vjp(const Args& a, const float* u, c
   constexpr int TMAX = FP / R;
 #pragma unroll
   for (int j = 0; j < 8; ++j) dproj[j] = 0.f;
+  if (a.hb) {  // corner group (one table): factored VJP, exact per corner subset (ra/backward.py:65-88)
+    // phi_r = prod_t sigma(2 beta c_rt u_t) => du_t = 2 beta sum_r dphi_r phi_r c_rt (1 - sigma(2 beta c_rt u_t))
+    float s = 0.f, sp[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) sp[p] = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const float x = dphi[rr] * phi[rr];
+      s += x;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (!((rr >> p) & 1)) sp[p] += x;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {  // low bits: split by c_rt = +1 (sum sp) / -1 (s - sp)
+      const float sg = 1.f / (1.f + fast_exp_neg(2.f * a.beta * u[p]));  // sigma(2 beta u)
+      dproj[p] = 2.f * a.beta * ((1.f - sg) * sp[p] - sg * (s - sp[p])) * (1.f - u[p] * u[p]);
+    }
+    for (int b = 0; b < a.hb; ++b) {  // high bits: c fixed by chi
+      const int j = P + b;
+      const float uj = u[j < 5 ? j : 0];
+      const float sg = 1.f / (1.f + fast_exp_neg(2.f * a.beta * uj));
+      const float d = ((a.chi >> b) & 1) ? -sg : (1.f - sg);
+      dproj[j < 8 ? j : 0] = 2.f * a.beta * d * s * (1.f - uj * uj);
+    }
+    return;
+  }
 #pragma unroll
   for (int tau = 0; tau < TMAX; ++tau) {
     if (tau < a.T) {
@@ -977,9 +1041,13 @@ inline Args make_args(const Geo& g) {
   a.Np = (g.N + 3) & ~int64_t(3);
   a.nseg = g.nseg;
   a.seg_tokens = g.seg_tokens;
-  a.P = g.P;
+  a.P = pass_corner_bits(g);  // corner bits of this pass (the kernels' template P)
   a.T = g.T;
-  a.TP = g.T * g.P;
+  a.TP = g.T * g.P;           // projections (all hyperplanes of the pass's tables)
+  a.hb = g.P - a.P;
+  a.chi = int(g.chi);
+  a.ext_rd = g.ext_rden;
+  a.ext_gd = g.ext_gden;
   a.beta = g.beta;
   a.normalize = g.normalize;
   a.w_per_head = g.w_per_head;

@@ -84,7 +84,7 @@ class _Meta:
     """Per-shape facts from the library (descriptor, segments, workspace and state sizes), queried
     once per distinct problem: an eager layer call then makes no sizing calls across the C-ABI."""
 
-    __slots__ = ("desc", "dref", "nseg", "seg_tokens", "ws_bytes", "state_elems", "fast")
+    __slots__ = ("desc", "dref", "nseg", "seg_tokens", "ws_bytes", "state_elems", "fast", "grouped", "fast_plan")
 
     def __init__(self, desc):
         self.desc = desc
@@ -93,6 +93,9 @@ class _Meta:
         self.ws_bytes = _lib.workspace_bytes(desc)
         self.state_elems = _lib.state_elems(desc)
         self.fast = _lib.fast_path(desc)
+        plan = _lib.group_plan(desc)
+        self.grouped = plan["passes"] > 1
+        self.fast_plan = plan["fast"]
 
 
 _META: dict[tuple, _Meta] = {}
@@ -147,6 +150,7 @@ class Problem:
         self.desc, self.dref = m.desc, m.dref
         self.nseg, self.seg_tokens = m.nseg, m.seg_tokens
         self._ws_bytes, self._state_elems = m.ws_bytes, m.state_elems
+        self.grouped = m.grouped
         self.table_elems = (p.tables << p.hyperplanes) * (self.dv + 1)
 
     def ws(self) -> torch.Tensor:
@@ -161,10 +165,12 @@ class Problem:
         """Non-causal: the global tables [BH, F, dv+1].  Causal: a flat buffer holding the
         per-segment carries [BH, nseg, F, dv+1] (padded to 64 floats) then the q/k sketch rows
         [BH, N, 16] (projections x^.w_j and ||x||^2 of every q and k row, include/race_b200.h).
-        None when the tables run in groups (F beyond one kernel pass): the backward
-        then recomputes, as the reference does (ra/backward.py:200)."""
+        Sketches run as table / corner groups (F beyond one kernel pass): a flat buffer of the
+        summed numerators [BH, N, dv] then denominators [BH, N] (race_state_elems)."""
         if self._state_elems == 0:
             return None
+        if self.grouped:
+            return (self._state_elems,)
         f = self.p.tables << self.p.hyperplanes
         if self.p.causal:
             return (self.carry_elems() + 16 * self.bh * self.n,)
@@ -242,10 +248,10 @@ def _padded_fast(q: torch.Tensor, v: torch.Tensor, w, p: SketchParams) -> bool:
     bh = 1
     for x in q.shape[:-2]:
         bh *= x
-    desc = _lib.make_desc(dtype=_lib.RACE_BF16, batch_heads=max(bh, 1), heads=heads, n=q.shape[-2], dim=FAST_DIM,
-                          dim_v=FAST_DIM, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
-                          causal=p.causal, normalize=p.normalize, w_per_head=per_head)
-    return _lib.fast_path(desc)
+    m = _meta(dtype=_lib.RACE_BF16, batch_heads=max(bh, 1), heads=heads, n=q.shape[-2], dim=FAST_DIM,
+              dim_v=FAST_DIM, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
+              causal=p.causal, normalize=p.normalize, w_per_head=per_head)
+    return m.fast_plan  # one tcgen05 pass, or tcgen05 table / corner groups
 
 
 def _pad(t: torch.Tensor) -> torch.Tensor:

@@ -99,7 +99,7 @@ def sharded_forward(q, k, v, w, p: SketchParams, group=None, comm=None):
     ws = pr.ws()
     part = torch.empty((pr.bh, pr.nseg, E), dtype=torch.float32, device=dev)
     local = torch.zeros((pr.bh, E), dtype=torch.float32, device=dev)
-    if pr.state_shape() is None:
+    if pr.grouped or pr.state_shape() is None:
         raise _lib.RaceUnsupported("sequence sharding needs all F buckets in one kernel pass (no table groups)")
     if p.causal:
         state = torch.empty(pr.state_shape(), dtype=torch.float32, device=dev)

@@ -82,11 +82,14 @@ def test_validation(kw, exc):
 @pytest.mark.parametrize("P", [8, 10, 11, 16, 20])
 def test_wide_sketches_plan_corner_groups(P):
     """P beyond one kernel pass (and every P in [11, 20], which the reference accepts, ra/core.py:71)
-    runs as table / corner groups: valid sizes, no saved state (the backward recomputes)."""
+    runs as table / corner groups: valid sizes; the state is the summed numerators [BH, N, dv] and
+    denominators [BH, N] the backward takes its normalisers from."""
     d = _desc(hyperplanes=P, tables=2)
     assert _lib.segments(d)[0] >= 1
     assert _lib.workspace_bytes(d) > 0
-    assert _lib.state_elems(d) == 0
+    assert _lib.state_elems(d) == 4 * 131072 * 129
+    plan = _lib.group_plan(d)
+    assert plan["passes"] > 1 and plan["corner_bits"] <= 10
 
 
 def test_state_rows_offset_is_aligned():

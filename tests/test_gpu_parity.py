@@ -438,10 +438,13 @@ def test_table_groups_match_oracle(causal, shape):
 
     t = [torch.tensor(x, dtype=torch.float32, device=dev)[None] for x in (q, k, v, g)]
     w = torch.tensor(rb.all_hyperplanes(cfg, d), dtype=torch.float32, device=dev)
-    assert Problem(t[0], t[1], t[2], w, cfg.params()).state_shape() is None  # grouped: no saved state
+    pr = Problem(t[0], t[1], t[2], w, cfg.params())
+    assert pr.grouped and pr.state_shape() == (n * (dv + 1),)  # grouped: the summed num / den are the state
     o, den, st = rb.race_forward(t[0], t[1], t[2], w, cfg.params())
-    assert st is None
-    dq, dk, dvv = rb.race_backward(t[0], t[1], t[2], w, t[3], cfg.params())
+    dq, dk, dvv = rb.race_backward(t[0], t[1], t[2], w, t[3], cfg.params(), state=st)
+    # the saved sums give exactly the recomputing backward's gradients (ra/backward.py:200 recomputes)
+    for a, b in zip((dq, dk, dvv), rb.race_backward(t[0], t[1], t[2], w, t[3], cfg.params())):
+        assert torch.equal(a, b)
     wr = rb.all_hyperplanes(cfg, d)
     o_r, den_r, _ = ro.forward(q, k, v, wr, cfg.beta, causal)
     assert rel_err(o[0].cpu(), o_r) <= TOL_F32

@@ -272,8 +272,10 @@ def test_wide_sketches_vs_oracle(shape, causal):
     w = rb.head_hyperplanes(cfg, 1, d).to(dev)
     p = cfg.params()
     o, den, st = rb.race_forward(tq, tk, tv, w, p)
-    assert st is None  # grouped: the backward recomputes (ra/backward.py:200)
-    dq, dk, dvv = rb.race_backward(tq, tk, tv, w, tg, p)
+    assert st is not None and st.numel() == n * (dv + 1)  # grouped: the summed numerators / denominators
+    dq, dk, dvv = rb.race_backward(tq, tk, tv, w, tg, p, state=st)
+    for a, b in zip((dq, dk, dvv), rb.race_backward(tq, tk, tv, w, tg, p)):  # == recomputing backward
+        assert torch.equal(a, b)
     qh, kh, vh, gh = (t[0, 0].double().cpu().numpy() for t in (tq, tk, tv, tg))
     wh = w[0].double().cpu().numpy()
     o_r, den_r, _ = ro.forward(qh, kh, vh, wh, beta, causal)
@@ -285,3 +287,22 @@ def test_wide_sketches_vs_oracle(shape, causal):
                   dv=errs[2])
     assert e_den <= TOL_F32 and e_o <= tol, (e_o, e_den)
     assert max(errs) <= tol, errs
+
+
+# ---------------------------------------------------------------------------
+# 6. bf16 sketches beyond one tcgen05 pass: table / corner groups of tcgen05 passes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+@pytest.mark.parametrize("sk", [(2, 4, 1), (2, 8, 1), (2, 4, 2), (1, 8, 1), (3, 3, 1), (4, 2, 1), (5, 1, 1), (4, 4, 1)],
+                         ids=lambda s: "P%dL%dM%d" % s)
+def test_fast_groups_vs_oracle(sk, causal):
+    """bf16, d = 128: sketches of up to F = 64 buckets run as several tcgen05 passes (table groups of
+    F <= 8 for P <= 3; corner groups of 8 corners with the factored features / VJP for P = 4, 5),
+    the query side of each pass using the whole estimator's 1/D and -rho/D.  All heads vs the oracle."""
+    P, L, M = sk
+    q, k, v, g = _host_inputs(4099, 128, 2, seed=P * 10 + L, zero_rows=2)
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, ensembles=M, beta=8.0, seed=21, causal=causal)
+    w = rb.head_hyperplanes(cfg, 2, 128).to(q.device)
+    plan = _lib.group_plan(Problem(q, k, v, w, cfg.params()).desc)
+    assert plan["fast"] and plan["passes"] > 1, plan
+    _check_layer(q, k, v, g, w, cfg.params(), range(2), f"fast_groups_P{P}L{L}M{M}_{'c' if causal else 'nc'}")

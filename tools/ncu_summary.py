@@ -90,12 +90,15 @@ def traffic(path: str, out: str) -> None:
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    res = {}
+    import os
+
+    res, seen = (json.load(open(out)) if os.path.exists(out) else {}), set()  # merge into the existing file
     for r in data:
         name = re.sub(r"<.*", "", short(r[col["Kernel Name"]])).split("::")[-1]
-        if name in res:
+        if name in seen:
             continue
         b = sum(float(r[col[m]]) * scale[units[col[m]]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        seen.add(name)
         res[name] = {"dram_bytes": b, "us": float(r[col["gpu__time_duration.sum"]]), "capture": path.split("/")[-1]}
     json.dump(res, open(out, "w"), indent=1, sort_keys=True)
     print(json.dumps(res, indent=1, sort_keys=True))
