@@ -61,7 +61,7 @@ static_assert(SMEM <= 232448, "k_aggregate2 shared memory");
 constexpr uint32_t TM_PK = 0, TM_ACC = 32;  // accumulators at 32 and 64
 }  // namespace agg2
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_aggregate2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   using namespace agg2;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(&pk_empty[gc & 1]);
         float phi[FP];
-        row_features<P>(a, proj, inv, t + r < m.t1, phi);
+        row_features<P, HB>(a, proj, inv, t + r < m.t1, phi);
 #pragma unroll
         for (int f = 0; f < FP; ++f) asum[f] += phi[f];
         if (gc >= 2) mbar_wait(&phi_empty[gc & 1], ((gc >> 1) - 1) & 1);
@@ -288,7 +288,7 @@ static_assert(SMEM <= 232448, "k_readout8 shared memory");
 constexpr uint32_t TM_NUM_R = 128;
 }  // namespace rdo8
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_readout8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
   using namespace rdo8;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_ld_wait();
       const bool valid = c.t + r < m.t1;
       float phi[FP];
-      row_features<P>(a, proj, inv, valid, phi);
+      row_features<P, HB>(a, proj, inv, valid, phi);
       float D = 0.f;
 #pragma unroll
       for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
@@ -549,7 +549,7 @@ static_assert(SMEM <= 232448, "k_causal_fwd8 shared memory");
 
 // KR: the k halves of the sketch rows were written by the key-side aggregation (k_aggregate2),
 // so this pass reads Q, V and those rows instead of K (no K tile, no K projection).
-template <int P, bool KR>
+template <int P, bool KR, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_causal_fwd8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         float pq[16];
         tmem_ld16(tmem + lb + TM_PROJQ, pq);
         tmem_ld_wait();
-        row_features<P>(a, pq, invq, valid, phq);
+        row_features<P, HB>(a, pq, invq, valid, phq);
         write_phi_q(sb + OFF_PHIQ, r, phq);
         if (a.rows_out && valid) {  // sketch row, q half
           float hat[5];
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         float pq[16], phk[FP];
         if (KR) {
           float u[5];
-          row_features_hat<P>(a, hk, valid, phk, u);
+          row_features_hat<P, HB>(a, hk, valid, phk, u);
           tmem_ld16(tmem + lb + TM_PROJQ, pq);
           write_phi_k(sb + OFF_PHIK, r, phk);
           tmem_ld_wait();
@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           tmem_ld16(tmem + lb + TM_PROJK, pk);
           tmem_ld16(tmem + lb + TM_PROJQ, pq);
           tmem_ld_wait();
-          row_features<P>(a, pk, invk, valid, phk);
+          row_features<P, HB>(a, pk, invk, valid, phk);
           write_phi_k(sb + OFF_PHIK, r, phk);
           if (a.rows_out && valid) {  // sketch row, k half
             float hat[5];
@@ -847,7 +847,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
         }
-        row_features<P>(a, pq, invq, valid, phq);
+        row_features<P, HB>(a, pq, invq, valid, phq);
       }
       float D = 0.f;
 #pragma unroll
@@ -950,7 +950,7 @@ constexpr int OFF_BAR = OFF_W + WOP;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace prj
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_project(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, Args a) {
   using namespace prj;
@@ -1117,7 +1117,9 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
     case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
-    default: return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+    default:
+      if (g.cb) return launch_nt(k_aggregate2<3, 2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      return launch_nt(k_aggregate2<3>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
   }
 }
 
@@ -1133,7 +1135,9 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
     case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
-    default: return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+    default:
+      if (g.cb) return launch_nt(k_readout8<3, 2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+      return launch_nt(k_readout8<3>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
   }
 }
 
@@ -1148,7 +1152,9 @@ cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* 
   switch (pass_corner_bits(g)) {
     case 1: return launch(k_project<1>, prj::SMEM, grid_for(g), st, mq, mk, a);
     case 2: return launch(k_project<2>, prj::SMEM, grid_for(g), st, mq, mk, a);
-    default: return launch(k_project<3>, prj::SMEM, grid_for(g), st, mq, mk, a);
+    default:
+      if (g.cb) return launch(k_project<3, 2>, prj::SMEM, grid_for(g), st, mq, mk, a);
+      return launch(k_project<3>, prj::SMEM, grid_for(g), st, mq, mk, a);
   }
 }
 
@@ -1168,12 +1174,14 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.rows_out = nrm;
   a.dbg = trace_for("fwd");
   switch (pass_corner_bits(g)) {
-#define RACE_FWD8(PP)                                                                                     \
-  return krows ? launch_nt(k_causal_fwd8<PP, true>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
-               : launch_nt(k_causal_fwd8<PP, false>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)
-    case 1: RACE_FWD8(1);
-    case 2: RACE_FWD8(2);
-    default: RACE_FWD8(3);
+#define RACE_FWD8(PP, HB)                                                                                     \
+  return krows ? launch_nt(k_causal_fwd8<PP, true, HB>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
+               : launch_nt(k_causal_fwd8<PP, false, HB>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)
+    case 1: RACE_FWD8(1, 0);
+    case 2: RACE_FWD8(2, 0);
+    default:
+      if (g.cb) RACE_FWD8(3, 2);
+      RACE_FWD8(3, 0);
 #undef RACE_FWD8
   }
 }

@@ -75,7 +75,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;  // DS: two accumulators at 32 and 64
 }  // namespace bq8n
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
              const __grid_constant__ CUtensorMap tmDQ, Args a) {
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tmem_ld16(tmem + lb + TM_Y, yv);
         tmem_ld_wait();
         float phi[FP], u[5], ph[5];
-        row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
+        row_features_u<P, HB>(a, proj, sc.inv, valid, phi, u, ph);
         float y[FP], D = 0.f, num = 0.f;
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
         float dproj[8];
-        row_feature_vjp<P>(a, u, phi, dphi, dproj);
+        row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
         if (h == 0) {
           float phit[FP];
 #pragma unroll
@@ -339,7 +339,7 @@ using bk::TM_DV;
 using bk::TM_DX;
 }  // namespace bk8n
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_k8(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
              const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a) {
@@ -498,11 +498,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_ld16(tmem + lb + TM_Z, zv);
       tmem_ld_wait();
       float phi[FP], u[5], ph[5], dphi[FP];
-      row_features_u<P>(a, proj, sc.inv, valid, phi, u, ph);
+      row_features_u<P, HB>(a, proj, sc.inv, valid, phi, u, ph);
 #pragma unroll
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
       float dproj[8];
-      row_feature_vjp<P>(a, u, phi, dphi, dproj);
+      row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
       if (h == 0) write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
       else write_dproj(sb + OFF_DPROJ, r, dproj);
       fence_proxy_async();
@@ -544,7 +544,9 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
     case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-    default: return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    default:
+      if (g.cb) return launch_nt(k_bwd_q8<3, 2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+      return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
   }
 }
 
@@ -560,7 +562,9 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
     case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-    default: return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    default:
+      if (g.cb) return launch_nt(k_bwd_k8<3, 2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+      return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
   }
 }
 

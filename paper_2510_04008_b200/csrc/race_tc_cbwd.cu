@@ -91,7 +91,7 @@ __device__ __forceinline__ void write_dproj_w(uint32_t buf, int r, const float* 
 }
 }  // namespace cq8
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -366,14 +366,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 9, gc);
         float phq[FP], uq[5];
         if (h == 0) {
-          row_features_hat<P>(a, hq, valid, phq, uq);
+          row_features_hat<P, HB>(a, hq, valid, phq, uq);
           write_phi_q(sb + OFF_PHIQ, r, phq);
           fence_proxy_async();
           tc_fence_before();
           mbar_arrive(phi_ready);
         } else {
           float phk[FP], uk[5];
-          row_features_hat<P>(a, hatk, valid, phk, uk);
+          row_features_hat<P, HB>(a, hatk, valid, phk, uk);
           write_phi_k(sb + OFF_PHIK, r, phk);
           fence_proxy_async();
           tc_fence_before();
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
           }
-          row_features_hat<P>(a, hq, valid, phq, uq);
+          row_features_hat<P, HB>(a, hq, valid, phq, uq);
         }
         float yv[16];
         mbar_wait(c1, par);
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
         float dproj[8];
-        row_feature_vjp<P>(a, uq, phq, dphi, dproj);
+        row_feature_vjp<P, HB>(a, uq, phq, dphi, dproj);
         const float dotq = dot_from_proj(dproj, hq);
         if (h == 0) write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z (c3)
 #pragma unroll
@@ -601,7 +601,7 @@ struct RCursor {
   }
 };
 
-template <int P>
+template <int P, int HB = 0>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -899,10 +899,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       float phq[FP], uq[5], phk[FP], uk[5];
       {
         if (h == 0) {
-          row_features_hat<P>(a, hatq, valid, phq, uq);
+          row_features_hat<P, HB>(a, hatq, valid, phq, uq);
           write_phi_k(sb + OFF_PHIQ, r, phq);  // [hi|hi|lo|0]
         } else {
-          row_features_hat<P>(a, hk, valid, phk, uk);
+          row_features_hat<P, HB>(a, hk, valid, phk, uk);
           write_phi_q(sb + OFF_PHIK, r, phk);  // [hi|lo|hi|0]
         }
         fence_proxy_async();
@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xpar[256 + qw * FP + f] = dac[f];
           }
-          row_features_hat<P>(a, hk, valid, phk, uk);  // for dk (off the MMA path)
+          row_features_hat<P, HB>(a, hk, valid, phk, uk);  // for dk (off the MMA path)
         }
       }
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 24, gc);
@@ -1001,7 +1001,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
       float dproj[8];
-      row_feature_vjp<P>(a, uk, phk, dphi, dproj);
+      row_feature_vjp<P, HB>(a, uk, phk, dphi, dproj);
       const float dotk = dot_from_proj(dproj, hk);
       if (h == 1) cq8::write_dproj_w(sb + OFF_PHIQ, r, dproj, a.TP);  // Phi_q is dead after Pm, Z (c3)
       fence_proxy_async();
@@ -1078,7 +1078,11 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
     case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
-    default: return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
+    default:
+      if (g.cb)
+        return launch_nt(k_bwd_causal_q8<3, 2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a,
+                         rden, gden);
+      return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
   }
 }
 
@@ -1105,7 +1109,11 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
     case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
-    default: return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
+    default:
+      if (g.cb)
+        return launch_nt(k_bwd_causal_k8<3, 2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows,
+                         mdv2, a);
+      return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
   }
 }
 

@@ -262,20 +262,28 @@ __device__ __forceinline__ float fast_exp_neg(float y) {  // exp(-y)
 // Corner group (a.hb > 0, one table): the fixed high bits chi of the pass's corners contribute
 // prod_b sigma(2 beta c_b u_{P+b}) to every phi_r (factored form, ra/sketch.py:120-129), with
 // u_j = tanh_of(j) for the projections j = P .. P + hb - 1.
-template <typename U>
+// Compiled only into the corner-group instantiations (HB > 0, the kernels' second template
+// argument): fully unrolled with compile-time indices j = P + b < 5 (hb <= HB = 2 since a pass has
+// T*P <= 5 projections), so no register array is demoted to local memory and the ordinary
+// instantiations carry none of this code.
+template <int P, int HB, typename U>
 __device__ __forceinline__ float group_weight(const Args& a, U tanh_of) {
   float m = 1.f;
-  for (int b = 0; b < a.hb; ++b) {
-    const float u = tanh_of(a.P + b);
-    const float e = fast_exp_neg(2.f * a.beta * fabsf(u));
-    const bool match = (((a.chi >> b) & 1) != 0) == (u < 0.f);
-    m *= (match ? 1.f : e) / (1.f + e);
+#pragma unroll
+  for (int b = 0; b < HB; ++b) {
+    constexpr int kMax = 5;
+    if (b < a.hb && P + b < kMax) {
+      const float u = tanh_of(P + b < kMax ? P + b : 0);
+      const float e = fast_exp_neg(2.f * a.beta * fabsf(u));
+      const bool match = (((a.chi >> b) & 1) != 0) == (u < 0.f);
+      m *= (match ? 1.f : e) / (1.f + e);
+    }
   }
   return m;
 }
 
 // features of one row from its 16 projection columns (P compile-time, T <= 8 >> P)
-template <int P>
+template <int P, int HB = 0>
 __device__ __forceinline__ void row_features(const Args& a, const float* proj, float inv, bool valid, float* phi) {
   constexpr int R = 1 << P;
   constexpr int TMAX = FP / R;
@@ -295,7 +303,7 @@ __device__ __forceinline__ void row_features(const Args& a, const float* proj, f
         z *= 1.f + e[p];
       }
       float rz = 1.f / z;
-      if (a.hb) rz *= group_weight(a, [&](int j) { return fast_tanh((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv); });
+      if constexpr (HB > 0) rz *= group_weight<P, HB>(a, [&](int j) { return fast_tanh((proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv); });
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         float prod = rz;
@@ -318,7 +326,7 @@ __device__ __forceinline__ void store_row_half(float* dst, const float* hat, flo
   reinterpret_cast<float4*>(dst)[1] = make_float4(hat[4], 0.f, 0.f, sumsq);
 }
 // features from stored projections hat (same arithmetic as row_features[_u])
-template <int P>
+template <int P, int HB = 0>
 __device__ __forceinline__ void row_features_hat(const Args& a, const float* hat, bool valid, float* phi, float* u) {
   constexpr int R = 1 << P;
   constexpr int TMAX = FP / R;
@@ -341,8 +349,8 @@ __device__ __forceinline__ void row_features_hat(const Args& a, const float* hat
         z *= 1.f + e[p];
       }
       float rz = 1.f / z;
-      if (a.hb)
-        rz *= group_weight(a, [&](int j) {
+      if constexpr (HB > 0)
+        rz *= group_weight<P, HB>(a, [&](int j) {
           const float uu = fast_tanh(hat[j]);
           u[j] = uu;
           return uu;
@@ -481,7 +489,7 @@ __device__ __forceinline__ void write_sopT(uint32_t buf, int c, const float* s) 
 }
 
 // features + the tanh values u_j (j < TP) kept for the VJP
-template <int P>
+template <int P, int HB = 0>
 __device__ __forceinline__ void row_features_u(const Args& a, const float* proj, float inv, bool valid, float* phi,
                                                float* u, float* phat) {
   constexpr int R = 1 << P;
@@ -507,8 +515,8 @@ __device__ __forceinline__ void row_features_u(const Args& a, const float* proj,
         z *= 1.f + e[p];
       }
       float rz = 1.f / z;
-      if (a.hb)
-        rz *= group_weight(a, [&](int j) {
+      if constexpr (HB > 0)
+        rz *= group_weight<P, HB>(a, [&](int j) {
           const float ph = (proj[3 * j] + proj[3 * j + 1] + proj[3 * j + 2]) * inv;
           const float uu = fast_tanh(ph);
           phat[j] = ph;
@@ -527,14 +535,14 @@ __device__ __forceinline__ void row_features_u(const Args& a, const float* proj,
 }
 
 // softmax-over-corners + tanh VJP (ra/backward.py:53-90): dphi -> dproj_j, j < TP
-template <int P>
+template <int P, int HB = 0>
 __device__ __forceinline__ void row_feature_vjp(const Args& a, const float* u, const float* phi, const float* dphi,
                                                 float* dproj) {
   constexpr int R = 1 << P;
   constexpr int TMAX = FP / R;
 #pragma unroll
   for (int j = 0; j < 8; ++j) dproj[j] = 0.f;
-  if (a.hb) {  // corner group (one table): factored VJP, exact per corner subset (ra/backward.py:65-88)
+  if constexpr (HB > 0) {  // corner group (one table): factored VJP, exact per corner subset (ra/backward.py:65-88)
     // phi_r = prod_t sigma(2 beta c_rt u_t) => du_t = 2 beta sum_r dphi_r phi_r c_rt (1 - sigma(2 beta c_rt u_t))
     float s = 0.f, sp[P];
 #pragma unroll
@@ -552,31 +560,35 @@ __device__ __forceinline__ void row_feature_vjp(const Args& a, const float* u, c
       const float sg = 1.f / (1.f + fast_exp_neg(2.f * a.beta * u[p]));  // sigma(2 beta u)
       dproj[p] = 2.f * a.beta * ((1.f - sg) * sp[p] - sg * (s - sp[p])) * (1.f - u[p] * u[p]);
     }
-    for (int b = 0; b < a.hb; ++b) {  // high bits: c fixed by chi
-      const int j = P + b;
-      const float uj = u[j < 5 ? j : 0];
-      const float sg = 1.f / (1.f + fast_exp_neg(2.f * a.beta * uj));
-      const float d = ((a.chi >> b) & 1) ? -sg : (1.f - sg);
-      dproj[j < 8 ? j : 0] = 2.f * a.beta * d * s * (1.f - uj * uj);
+#pragma unroll
+    for (int b = 0; b < HB; ++b) {  // high bits: c fixed by chi (compile-time indices, see group_weight)
+      constexpr int kMax = 5;
+      if (b < a.hb && P + b < kMax) {
+        const int j = P + b < kMax ? P + b : 0;
+        const float uj = u[j];
+        const float sg = 1.f / (1.f + fast_exp_neg(2.f * a.beta * uj));
+        const float d = ((a.chi >> b) & 1) ? -sg : (1.f - sg);
+        dproj[j] = 2.f * a.beta * d * s * (1.f - uj * uj);
+      }
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int tau = 0; tau < TMAX; ++tau) {
-    if (tau < a.T) {
-      float s = 0.f;
+    for (int tau = 0; tau < TMAX; ++tau) {
+      if (tau < a.T) {
+        float s = 0.f;
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) s = fmaf(dphi[tau * R + rr], phi[tau * R + rr], s);
+        for (int rr = 0; rr < R; ++rr) s = fmaf(dphi[tau * R + rr], phi[tau * R + rr], s);
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        float du = 0.f;
+        for (int p = 0; p < P; ++p) {
+          float du = 0.f;
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
-          const float dl = phi[tau * R + rr] * (dphi[tau * R + rr] - s);
-          du += ((rr >> p) & 1) ? -dl : dl;
+          for (int rr = 0; rr < R; ++rr) {
+            const float dl = phi[tau * R + rr] * (dphi[tau * R + rr] - s);
+            du += ((rr >> p) & 1) ? -dl : dl;
+          }
+          const float uu = u[tau * P + p];
+          dproj[tau * P + p] = a.beta * du * (1.f - uu * uu);
         }
-        const float uu = u[tau * P + p];
-        dproj[tau * P + p] = a.beta * du * (1.f - uu * uu);
       }
     }
   }
