@@ -76,7 +76,12 @@ int report_cuda(cudaError_t e, const char* where) { return cuda_status(e, where)
 
 namespace {
 
-constexpr int64_t kSegTarget = 148 * 8;  // CTAs to aim for across all (b, h)
+constexpr int64_t kSegTarget = 148 * 8;  // work items to aim for across all (b, h): tcgen05 kernels
+// CUDA-core kernels (one CTA per item, 2 per SM); RACE_SIMT_SEG_TARGET overrides (tuning)
+const int64_t kSegTargetSimt = [] {
+  const char* e = getenv("RACE_SIMT_SEG_TARGET");
+  return e && e[0] ? int64_t(atoll(e)) : int64_t(148) * 2 * 7;
+}();
 
 int resolve_shape(const race_desc_t* d, race::Geo* g) {
   if (!d) return fail(RACE_EBADSHAPE, "null descriptor");
@@ -104,7 +109,13 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   g->w_per_head = d->w_per_head ? 1 : 0;
   g->dtype = d->dtype;
   g->causal = d->causal ? 1 : 0;
-  int64_t target = (kSegTarget + g->BH - 1) / g->BH;
+  // Segments are the work items.  The tcgen05 kernels walk contiguous item ranges of a persistent
+  // grid (148 CTAs): ~8 items per SM.  The CUDA-core kernels launch one CTA per item, two resident
+  // per SM: aim for ~7 full waves of 2 x 148 so the last wave's tail is small (3.5 waves of 512-token
+  // segments left the last wave half empty at N = 131072, H = 4).
+  const bool fast_capable = g->dtype == RACE_BF16 && g->d == 128 && g->dv == 128;
+  const int64_t seg_target = fast_capable ? kSegTarget : kSegTargetSimt;
+  int64_t target = (seg_target + g->BH - 1) / g->BH;
   if (target < 1) target = 1;
   int64_t per = (g->N + target - 1) / target;
   per = ((per + 127) / 128) * 128;
