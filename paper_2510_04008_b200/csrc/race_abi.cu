@@ -6,6 +6,7 @@
 // returned status back to ValueError.  Every entry point is stream-ordered,
 // allocation-free and thread-safe (the only global is the thread-local error
 // string).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -295,6 +296,8 @@ struct GroupWs {
   float* dq_acc;    // fp32 sums
   float* dk_acc;
   float* dv_acc;
+  float* dproj_q;   // [BH*N, T*P] summed dproj of the query / key side (tcgen05 groups)
+  float* dproj_k;
   size_t bytes;
 };
 
@@ -322,6 +325,8 @@ GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
   w.dq_acc = static_cast<float*>(take(sizeof(float) * tok * g.d));
   w.dk_acc = static_cast<float*>(take(sizeof(float) * tok * g.d));
   w.dv_acc = static_cast<float*>(take(sizeof(float) * tok * g.dv));
+  w.dproj_q = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
+  w.dproj_k = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
   w.bytes = off;
   return w;
 }
@@ -434,6 +439,115 @@ __global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int mode, f
     const float v = to_f32(x[i]) + (mode ? acc[i] : 0.f);
     if (mode == 2) out[i] = from_f32<T>(v);
     else acc[i] = v;
+  }
+}
+
+// dx from the summed per-row dproj of all groups (grouped tcgen05 backward): dx^ = sum_j dproj_j w_j over
+// every hyperplane, then the sphere-tangent VJP dx = (dx^ - (dx^.x^) x^) / ||x|| of ra/core.py:126-139
+// (zero-norm rows and unnormalised inputs pass dx^ through).  One warp per row; the hyperplanes of every
+// head sit in shared memory, the row's dproj in lane registers (broadcast by shuffles), and a lane's
+// columns c = lane + 32 i in registers, so each operand is read once.
+constexpr int kDxRows = 4;  // rows per warp iteration (independent chains: latency hiding)
+// NCH = 4-column chunks per lane (d <= 128 * NCH); 32-bit shared-memory indexing throughout
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) k_dx_from_dproj(int64_t rows, int64_t N, int d, int tp,
+                                                       const T* __restrict__ x, const float* __restrict__ dproj,
+                                                       const float* __restrict__ w, int nheads_w, int H,
+                                                       int normalize, T* __restrict__ dx) {
+  extern __shared__ float4 wsm4[];  // [nheads_w, tp, d / 4] float4
+  const int d4 = d / 4;
+  const int hstride = tp * d4;
+  {
+    const float4* w4 = reinterpret_cast<const float4*>(w);
+    const int nw4 = nheads_w * hstride;
+    for (int i = threadIdx.x; i < nw4; i += blockDim.x) wsm4[i] = w4[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t nquads = (rows + kDxRows - 1) / kDxRows;
+  for (int64_t qd = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; qd < nquads; qd += nwarps) {
+    float4 xv[kDxRows][NCH], acc[kDxRows][NCH];
+    float mine[kDxRows];
+    int woff[kDxRows];
+    // head of the quad's first row: one division per quad; rows crossing into the next sequence step it
+    int64_t bh = (qd * kDxRows) / N, bh_end = (bh + 1) * N;
+    int head = nheads_w > 1 ? int(bh % H) : 0;
+#pragma unroll
+    for (int q = 0; q < kDxRows; ++q) {  // every load of the four rows first
+      const int64_t r = qd * kDxRows + q;
+      const bool ok = r < rows;
+      const int64_t rr = ok ? r : rows - 1;
+      while (rr >= bh_end) {
+        bh_end += N;
+        if (++head == H) head = 0;
+      }
+      woff[q] = (nheads_w > 1 ? head * hstride : 0) + lane;
+      mine[q] = (ok && lane < tp) ? dproj[rr * tp + lane] : 0.f;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c4 = lane + 32 * i;
+        xv[q][i] = (ok && c4 < d4) ? ld4(x + rr * d + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[q][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    for (int j = 0; j < tp; ++j) {  // tp <= 32 (checked by the caller)
+#pragma unroll
+      for (int q = 0; q < kDxRows; ++q) {
+        const float pj = __shfl_sync(0xffffffffu, mine[q], j);
+        const int base = woff[q] + j * d4;
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          if (lane + 32 * i < d4) {
+            const float4 wv = wsm4[base + 32 * i];
+            acc[q][i].x = fmaf(pj, wv.x, acc[q][i].x);
+            acc[q][i].y = fmaf(pj, wv.y, acc[q][i].y);
+            acc[q][i].z = fmaf(pj, wv.z, acc[q][i].z);
+            acc[q][i].w = fmaf(pj, wv.w, acc[q][i].w);
+          }
+        }
+      }
+    }
+    float ss[kDxRows], dot[kDxRows];
+#pragma unroll
+    for (int q = 0; q < kDxRows; ++q) {
+      ss[q] = 0.f;
+      dot[q] = 0.f;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const float4 a = xv[q][i];
+        ss[q] = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss[q]))));
+        dot[q] += acc[q][i].x * a.x + acc[q][i].y * a.y + acc[q][i].z * a.z + acc[q][i].w * a.w;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < kDxRows; ++q) {
+        ss[q] += __shfl_xor_sync(0xffffffffu, ss[q], o);
+        dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
+      }
+#pragma unroll
+    for (int q = 0; q < kDxRows; ++q) {
+      const int64_t r = qd * kDxRows + q;
+      if (r < rows) {
+        const float nrm = sqrtf(ss[q]);
+        const bool tang = normalize && nrm >= race::kZeroRowEps;
+        const float inv = tang ? 1.f / nrm : 1.f;
+        const float dt = tang ? dot[q] * inv : 0.f;  // dx^ . x^
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const int c4 = lane + 32 * i;
+          if (c4 < d4) {
+            float4 o = acc[q][i];
+            if (tang)
+              o = make_float4((o.x - dt * xv[q][i].x * inv) * inv, (o.y - dt * xv[q][i].y * inv) * inv,
+                              (o.z - dt * xv[q][i].z * inv) * inv, (o.w - dt * xv[q][i].w * inv) * inv);
+            st4(dx + r * d + 4 * c4, o);
+          }
+        }
+      }
+    }
   }
 }
 
@@ -816,11 +930,32 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
   });
   if (int rc = cuda_status(e, "table group normalisers")) return rc;
   const int64_t ngroups = gp.count(g);
+  // tcgen05 groups: the query / key kernels emit each row's dproj (summed over corner groups) instead
+  // of dq / dk, and one pass at the end forms dq, dk from them (no per-group dq / dk accumulation)
+  int t0_, cnt_;
+  const int tp_all = g.T * g.P;
+  const bool dproj_mode = race::tc_supported(group_geo(g, gp, 0, &t0_, &cnt_)) &&
+                          size_t(g.w_per_head ? g.H : 1) * tp_all * g.d * sizeof(float) <= 160 * 1024 &&
+                          tp_all <= 32 && g.d % 4 == 0 && g.d <= 256 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(dq) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  if (dproj_mode && gp.cb) {  // corner groups add into their table's columns
+    e = cudaMemsetAsync(ws.dproj_q, 0, sizeof(float) * rows * tp_all, S(stream));
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws.dproj_k, 0, sizeof(float) * rows * tp_all, S(stream));
+    if (int rc = cuda_status(e, "dproj init")) return rc;
+  }
   for (int64_t i = 0; i < ngroups; ++i) {
     int t0, cnt;
     race::Geo gs = group_geo(g, gp, i, &t0, &cnt);
     gs.ext_rden = ws.rden;
     gs.ext_gden = ws.gden;
+    if (dproj_mode) {
+      gs.dproj_q = ws.dproj_q;
+      gs.dproj_k = ws.dproj_k;
+      gs.dproj_ld = tp_all;
+      gs.dproj_col = t0 * g.P;
+      gs.dproj_acc = gp.cb ? 1 : 0;
+    }
     const float* wg = group_w(g, w, t0, cnt, ws, S(stream), &e);
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
     const WsLayout sub = ws_layout(gs, ws.sub);
@@ -871,15 +1006,33 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
           k_group_grad_acc<T, false><<<blocks_for(n), 256, 0, st>>>(n, static_cast<const T*>(x), mode, a,
                                                                     static_cast<T*>(out));
       };
-      acc(rows * g.d, ws.dq, ws.dq_acc, dq);
-      acc(rows * g.d, ws.dk, ws.dk_acc, dk);
+      if (!dproj_mode) {
+        acc(rows * g.d, ws.dq, ws.dq_acc, dq);
+        acc(rows * g.d, ws.dk, ws.dk_acc, dk);
+      }
       acc(rows * g.dv, ws.dv, ws.dv_acc, dv);
-      race::note_launch(3);
+      race::note_launch(dproj_mode ? 1 : 3);
       return cudaGetLastError();
     });
     if (int rc = cuda_status(e, "table group gradient sum")) return rc;
   }
-  return RACE_OK;  // the last group's accumulation wrote dq, dk, dv
+  if (!dproj_mode) return RACE_OK;  // the last group's accumulation wrote dq, dk, dv
+  e = by_dtype(g.dtype, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    const int nheads_w = g.w_per_head ? int(g.H) : 1;
+    const size_t smem = sizeof(float) * size_t(nheads_w) * tp_all * g.d;
+    auto kern = g.d <= 128 ? k_dx_from_dproj<T, 1> : k_dx_from_dproj<T, 2>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return err;
+    const unsigned grid = unsigned(std::min<int64_t>(blocks_for((rows + kDxRows - 1) / kDxRows * 32), 148 * 8));
+    kern<<<grid, 256, smem, S(stream)>>>(rows, g.N, g.d, tp_all, static_cast<const T*>(q), ws.dproj_q, w, nheads_w,
+                                         int(g.H), g.normalize, static_cast<T*>(dq));
+    kern<<<grid, 256, smem, S(stream)>>>(rows, g.N, g.d, tp_all, static_cast<const T*>(k), ws.dproj_k, w, nheads_w,
+                                         int(g.H), g.normalize, static_cast<T*>(dk));
+    race::note_launch(2);
+    return cudaGetLastError();
+  });
+  return cuda_status(e, "dq, dk from dproj");
 }
 
 }  // namespace

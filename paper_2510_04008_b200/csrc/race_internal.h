@@ -24,6 +24,12 @@ struct Geo {
   // are fixed to chi and contribute one per-row factor.  cb = 0: ungrouped (all P bits).
   int cb = 0;
   int64_t chi = 0;
+  // grouped tcgen05 backward (race_abi.cu): the query / key backward kernels write (corner groups:
+  // add) each row's dproj_j, j < T*P, into [BH*N, dproj_ld] fp32 at column dproj_col instead of
+  // storing dq / dk; one pass at the end turns the summed dproj into dq, dk (dx^ = dproj . W)
+  float* dproj_q = nullptr;
+  float* dproj_k = nullptr;
+  int dproj_ld = 0, dproj_col = 0, dproj_acc = 0;
 };
 
 // corners per table a kernel pass sees

@@ -75,7 +75,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;  // DS: two accumulators at 32 and 64
 }  // namespace bq8n
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool GRP = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
              const __grid_constant__ CUtensorMap tmDQ, Args a) {
@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       auto store_dq = [&](uint32_t j) {
         const int s = j & 1;
         mbar_wait(&dqstaged[s], (j >> 1) & 1);
-        for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, qt[s], qb[s]);
+        if (!a.dproj_out)  // grouped backward: dq is formed from the summed dproj afterwards
+          for (int h = 0; h < 2; ++h)
+            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, qt[s], qb[s]);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         uint8_t* stage = smem + s * STAGE_BYTES;
         float* xp = xsq + (gc & 1) * 256;
         const bool valid = t + r < m.t1;
+        const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
         mbar_wait(&full[s], (gc >> 1) & 1);
         xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
         compute_bar256();
@@ -256,16 +258,16 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const bool live = valid && D * invT > kDegenerateDenEps;
         float rD = live ? 1.f / D : 0.f;
         float rho = num * rD;
-        if (a.ext_rd) {  // table / corner group: normalisers of the whole estimator
-          const int64_t i = m.bh * a.Np + t + r;
-          rD = valid ? a.ext_rd[i] : 0.f;
-          rho = (valid && rD != 0.f) ? -a.ext_gd[i] / rD : 0.f;
+        if (GRP && a.ext_rd) {  // table / corner group: normalisers of the whole estimator
+          rD = pre.rd;
+          rho = rD != 0.f ? -pre.gd / rD : 0.f;
         }
         float dphi[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
         float dproj[8];
         row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
+        if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
         if (h == 0) {
           float phit[FP];
 #pragma unroll
@@ -339,7 +341,7 @@ using bk::TM_DV;
 using bk::TM_DX;
 }  // namespace bk8n
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool GRP = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_k8(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
              const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a) {
@@ -390,7 +392,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const int s = j & 1;
         mbar_wait(&staged[s], (j >> 1) & 1);
         for (int h = 0; h < 2; ++h) {
-          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, kt[s], kb[s]);
+          if (!a.dproj_out)  // grouped backward: dk is formed from the summed dproj afterwards
+            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, kt[s], kb[s]);
           tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + s * STAGE_BYTES + TILE + h * SUB), h * 64, kt[s], kb[s]);
         }
         tma_store_commit();
@@ -487,6 +490,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       uint8_t* stage = smem + s * STAGE_BYTES;
       float* xp = xsq + (gc & 1) * 256;
       const bool valid = t + r < m.t1;
+      const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
       mbar_wait(&full[s], (gc >> 1) & 1);
       xp[h * 128 + r] = half_row_sumsq_p(stage, r, h);
       compute_bar256();
@@ -503,6 +507,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
       float dproj[8];
       row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
+      if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
       if (h == 0) write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
       else write_dproj(sb + OFF_DPROJ, r, dproj);
       fence_proxy_async();
@@ -541,13 +546,18 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   a.w = w;
   a.tin = tab;
   a.tout = dpart;
+  a.dproj_out = g.dproj_q;
+  const bool grp = g.ext_rden || g.dproj_q;  // a pass of a grouped backward (race_abi.cu)
+#define RACE_BQ8(...) return launch_nt(k_bwd_q8<__VA_ARGS__>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a)
   switch (pass_corner_bits(g)) {
-    case 1: return launch_nt(k_bwd_q8<1>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-    case 2: return launch_nt(k_bwd_q8<2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+    case 1: if (grp) RACE_BQ8(1, 0, true); RACE_BQ8(1);
+    case 2: if (grp) RACE_BQ8(2, 0, true); RACE_BQ8(2);
     default:
-      if (g.cb) return launch_nt(k_bwd_q8<3, 2>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
-      return launch_nt(k_bwd_q8<3>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a);
+      if (g.cb) RACE_BQ8(3, 2, true);
+      if (grp) RACE_BQ8(3, 0, true);
+      RACE_BQ8(3);
   }
+#undef RACE_BQ8
 }
 
 cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w, const float* dtab, void* dk,
@@ -559,13 +569,19 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
   Args a = make_args(g);
   a.w = w;
   a.tin = dtab;
+  a.dproj_out = g.dproj_k;
+  const bool grp = g.ext_rden || g.dproj_k;
+#define RACE_BK8(...) \
+  return launch_nt(k_bwd_k8<__VA_ARGS__>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a)
   switch (pass_corner_bits(g)) {
-    case 1: return launch_nt(k_bwd_k8<1>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-    case 2: return launch_nt(k_bwd_k8<2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+    case 1: if (grp) RACE_BK8(1, 0, true); RACE_BK8(1);
+    case 2: if (grp) RACE_BK8(2, 0, true); RACE_BK8(2);
     default:
-      if (g.cb) return launch_nt(k_bwd_k8<3, 2>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
-      return launch_nt(k_bwd_k8<3>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a);
+      if (g.cb) RACE_BK8(3, 2, true);
+      if (grp) RACE_BK8(3, 0, true);
+      RACE_BK8(3);
   }
+#undef RACE_BK8
 }
 
 }  // namespace race

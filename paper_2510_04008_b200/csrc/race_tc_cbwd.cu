@@ -91,7 +91,7 @@ __device__ __forceinline__ void write_dproj_w(uint32_t buf, int r, const float* 
 }
 }  // namespace cq8
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool GRP = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const int s = j & 1;
         mbar_wait(&dqstaged[s], (j >> 1) & 1);
         const int qt = int(s ? qt1 : qt0), qb = int(s ? qb1 : qb0);
-        for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + s * TILE + h * SUB), h * 64, qt, qb);
+        if (!a.dproj_out)  // grouped backward: dq is formed from the summed dproj afterwards
+          for (int h = 0; h < 2; ++h)
+            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + s * TILE + h * SUB), h * 64, qt, qb);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         uint8_t* qtile = smem + OFF_Q + s * TILE;
         float* xpar = xbase + par * XPAR;
         const bool valid = t + r < m.t1;
+        const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
         mbar_wait(&fullT[s], (gc >> 1) & 1);
         const float* trow = reinterpret_cast<const float*>(smem + OFF_TOK + s * TOK_BYTES) + r * ROWW;
         float hq[5], hatk[5];  // x^.w_j of this q row and of this k row (the forward's sketch row)
@@ -433,10 +435,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const bool live = valid && D * invT > kDegenerateDenEps;
         float rD = live ? 1.f / D : 0.f;
         float rho = (ydot + ndt) * rD;
-        if (a.ext_rd) {  // table / corner group: normalisers of the whole estimator
-          const int64_t i = m.bh * a.Np + t + r;
-          rD = valid ? a.ext_rd[i] : 0.f;
-          rho = (valid && rD != 0.f) ? -a.ext_gd[i] / rD : 0.f;
+        if (GRP && a.ext_rd) {  // table / corner group: normalisers of the whole estimator
+          rD = pre.rd;
+          rho = rD != 0.f ? -pre.gd / rD : 0.f;
         }
         // E~ = tril(E - rho) -> bf16 pairs into TMEM (A of Z)
 #pragma unroll
@@ -491,6 +492,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
         float dproj[8];
         row_feature_vjp<P, HB>(a, uq, phq, dphi, dproj);
+        if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
         const float dotq = dot_from_proj(dproj, hq);
         if (h == 0) write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z (c3)
 #pragma unroll
@@ -601,7 +603,7 @@ struct RCursor {
   }
 };
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool GRP = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -685,8 +687,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       };
       auto store_dk = [&](uint32_t j) {
         mbar_wait(dkstaged, j & 1);
-        for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, kt, kb);
+        if (!a.dproj_out)  // grouped backward: dk is formed from the summed dproj afterwards
+          for (int h = 0; h < 2; ++h)
+            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, kt, kb);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -857,6 +860,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const int s = gc & 1;
       float* xpar = xbase + par * XPAR;
       const bool valid = t + r < m.t1;
+      const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
       if (m.bh != prev_bh) {  // (re)load the suffix state dS_>seg, dA_>seg and W', W''
         prev_bh = m.bh;
         const float* dcar = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
@@ -1002,6 +1006,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
       float dproj[8];
       row_feature_vjp<P, HB>(a, uk, phk, dphi, dproj);
+      if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
       const float dotk = dot_from_proj(dproj, hk);
       if (h == 1) cq8::write_dproj_w(sb + OFF_PHIQ, r, dproj, a.TP);  // Phi_q is dead after Pm, Z (c3)
       fence_proxy_async();
@@ -1071,19 +1076,25 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   a.tin = car;
   a.tout = dpart;
   a.rows_in = nrm;
+  a.dproj_out = g.dproj_q;
   a.dbg = trace_for("bq");
   if (!nrm) return cudaErrorInvalidValue;  // race_abi.cu always supplies the forward's rows
   CUtensorMap mrows;
   if (!make_map_rows(&mrows, nrm, g.BH * g.N)) return cudaErrorInvalidValue;
+  const bool grp = g.ext_rden || g.dproj_q;  // a pass of a grouped backward (race_abi.cu)
+#define RACE_CQ8(...)                                                                                           \
+  return launch_nt(k_bwd_causal_q8<__VA_ARGS__>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, \
+                   mrows, a, rden, gden)
   switch (pass_corner_bits(g)) {
-    case 1: return launch_nt(k_bwd_causal_q8<1>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
-    case 2: return launch_nt(k_bwd_causal_q8<2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
+    case 1: if (grp) RACE_CQ8(1, 0, true); RACE_CQ8(1);
+    case 2: if (grp) RACE_CQ8(2, 0, true); RACE_CQ8(2);
     default:
-      if (g.cb)
-        return launch_nt(k_bwd_causal_q8<3, 2>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a,
-                         rden, gden);
-      return launch_nt(k_bwd_causal_q8<3>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, mrows, a, rden, gden);
+      if (g.cb) RACE_CQ8(3, 2, true);
+      if (grp) RACE_CQ8(3, 0, true);
+      RACE_CQ8(3);
   }
+#undef RACE_CQ8
+
 }
 
 cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
@@ -1098,6 +1109,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.w = w;
   a.tin = dcar;
   a.rows_in = nrm;
+  a.dproj_out = g.dproj_k;
   a.dbg = trace_for("bk");
   if (!nrm) return cudaErrorInvalidValue;
   CUtensorMap mrd, mgd, mrows, mdv2;
@@ -1106,15 +1118,20 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   if (!make_map_f32_1d(&mrd, rden, g.BH * np, 128) || !make_map_f32_1d(&mgd, gden, g.BH * np, 128) ||
       !make_map_rows(&mrows, nrm, g.BH * g.N))
     return cudaErrorInvalidValue;
+  const bool grp = g.ext_rden || g.dproj_k;
+#define RACE_CK8(...)                                                                                           \
+  return launch_nt(k_bwd_causal_k8<__VA_ARGS__>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, \
+                   mgd, mrows, mdv2, a)
   switch (pass_corner_bits(g)) {
-    case 1: return launch_nt(k_bwd_causal_k8<1>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
-    case 2: return launch_nt(k_bwd_causal_k8<2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
+    case 1: if (grp) RACE_CK8(1, 0, true); RACE_CK8(1);
+    case 2: if (grp) RACE_CK8(2, 0, true); RACE_CK8(2);
     default:
-      if (g.cb)
-        return launch_nt(k_bwd_causal_k8<3, 2>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows,
-                         mdv2, a);
-      return launch_nt(k_bwd_causal_k8<3>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, mgd, mrows, mdv2, a);
+      if (g.cb) RACE_CK8(3, 2, true);
+      if (grp) RACE_CK8(3, 0, true);
+      RACE_CK8(3);
   }
+#undef RACE_CK8
+
 }
 
 }  // namespace race

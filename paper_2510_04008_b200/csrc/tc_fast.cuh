@@ -63,7 +63,40 @@ struct Args {
   // query-side backward kernels use them instead of their own group's D and rho
   const float* ext_rd;
   const float* ext_gd;
+  // grouped backward: per-row dproj out (Geo::dproj_q / dproj_k) instead of the dq / dk store
+  float* dproj_out;
+  int dproj_ld, dproj_col, dproj_acc;
 };
+
+// Grouped backward extras, loaded at the start of a chunk so their global-memory latency stays off the
+// compute chain: the whole estimator's 1/D, -rho/D (ext) and, for corner groups, the dproj already
+// summed over the table's earlier corner groups.
+struct GroupPre {
+  float rd, gd, prev[5];
+};
+__device__ __forceinline__ GroupPre group_prefetch(const Args& a, int64_t bh, int64_t t, int r, bool valid) {
+  GroupPre g{0.f, 0.f, {0.f, 0.f, 0.f, 0.f, 0.f}};
+  if (a.ext_rd && valid) {
+    const int64_t i = bh * a.Np + t + r;
+    g.rd = a.ext_rd[i];
+    g.gd = a.ext_gd[i];
+  }
+  if (a.dproj_out && a.dproj_acc && valid) {
+    const float* src = a.dproj_out + (bh * a.N + t + r) * a.dproj_ld + a.dproj_col;
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      if (j < a.TP) g.prev[j] = src[j];
+  }
+  return g;
+}
+// write this row's dproj_j, j < TP (plus the prefetched sum of earlier corner groups) at column
+// dproj_col of the grouped-backward buffer
+__device__ __forceinline__ void emit_dproj(const Args& a, int64_t row, const float* dproj, const GroupPre& pre) {
+  float* dst = a.dproj_out + row * a.dproj_ld + a.dproj_col;
+#pragma unroll
+  for (int j = 0; j < 5; ++j)
+    if (j < a.TP) dst[j] = dproj[j] + pre.prev[j];
+}
 
 #define RACE_DBG(a_, slot_, val_)                                                        \
   do {                                                                                   \
@@ -1060,6 +1093,10 @@ inline Args make_args(const Geo& g) {
   a.chi = int(g.chi);
   a.ext_rd = g.ext_rden;
   a.ext_gd = g.ext_gden;
+  a.dproj_out = nullptr;  // set per kernel (query / key side) by the launchers
+  a.dproj_ld = g.dproj_ld;
+  a.dproj_col = g.dproj_col;
+  a.dproj_acc = g.dproj_acc;
   a.beta = g.beta;
   a.normalize = g.normalize;
   a.w_per_head = g.w_per_head;
