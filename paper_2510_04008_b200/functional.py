@@ -185,7 +185,11 @@ class Problem:
 
 
 def _c(t: torch.Tensor) -> torch.Tensor:
-    return t if t.is_contiguous() else t.contiguous()
+    """Contiguous and 16-byte aligned (TMA tensor maps and the vector loads need aligned bases; a view
+    starting mid-allocation gets copied)."""
+    if t.is_contiguous() and t.data_ptr() % 16 == 0:
+        return t
+    return t.clone(memory_format=torch.contiguous_format) if t.is_contiguous() else t.contiguous()
 
 
 def _race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):

@@ -306,3 +306,26 @@ def test_fast_groups_vs_oracle(sk, causal):
     plan = _lib.group_plan(Problem(q, k, v, w, cfg.params()).desc)
     assert plan["fast"] and plan["passes"] > 1, plan
     _check_layer(q, k, v, g, w, cfg.params(), range(2), f"fast_groups_P{P}L{L}M{M}_{'c' if causal else 'nc'}")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+@pytest.mark.parametrize("sk", [(2, 2), (2, 4)], ids=["P2L2", "P2L4"])
+def test_misaligned_views_match_aligned(sk, dtype):
+    """Inputs that are contiguous views starting mid-allocation (not 16-byte aligned) give the aligned
+    inputs' results: the host layer copies them (TMA tensor maps and vector loads need aligned bases)."""
+    dev = _cuda()
+    n, P, L = 1000, *sk
+    gen = torch.Generator(device=dev).manual_seed(4)
+    base = [torch.randn(4 * n * 128 + 1, generator=gen, device=dev).to(dtype) for _ in range(4)]
+    views = [b[1:].view(1, 4, n, 128) for b in base]
+    assert all(v.data_ptr() % 16 for v in views)
+    aligned = [v.clone() for v in views]
+    cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=3, causal=True)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(dev)
+    p = cfg.params()
+    outs = []
+    for q, k, v, g in (views, aligned):
+        o, den, st = rb.race_forward(q, k, v, w, p)
+        outs.append((o, den) + tuple(rb.race_backward(q, k, v, w, g, p, state=st)))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
