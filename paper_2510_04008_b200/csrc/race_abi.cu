@@ -114,7 +114,7 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   // grid (148 CTAs): ~8 items per SM.  The CUDA-core kernels launch one CTA per item, two resident
   // per SM: aim for ~7 full waves of 2 x 148 so the last wave's tail is small (3.5 waves of 512-token
   // segments left the last wave half empty at N = 131072, H = 4).
-  const bool fast_capable = g->dtype == RACE_BF16 && g->d == 128 && g->dv == 128;
+  const bool fast_capable = g->dtype == RACE_BF16 && g->d <= 128 && g->dv <= 128 && g->d % 8 == 0 && g->dv % 8 == 0;
   const int64_t seg_target = fast_capable ? kSegTarget : kSegTargetSimt;
   int64_t target = (seg_target + g->BH - 1) / g->BH;
   if (target < 1) target = 1;
@@ -163,7 +163,7 @@ struct GroupPlan {
 // when it splits into passes that each are one (table groups for P <= 3, corner groups of 8 corners
 // for P = 4, 5): several fast passes beat one pass of the CUDA-core kernels by far at these widths
 bool fast_grouping(const race::Geo& g, GroupPlan* gp) {
-  if (g.dtype != RACE_BF16 || g.d != 128 || g.dv != 128 || race::tc_supported(g)) return false;
+  if (g.dtype != RACE_BF16 || g.d > 128 || g.dv > 128 || race::tc_supported(g)) return false;
   race::Geo s = g;
   if (g.P <= 3) {
     int tg = 1;

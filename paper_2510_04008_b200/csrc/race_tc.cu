@@ -244,15 +244,15 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&acc_empty[ns & 1]);
-        float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
 #pragma unroll
         for (int f = 0; f < FP; ++f)
-          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+          if (f < F && r < a.dvv) out[f * a.ldt + r] = acc[f] + acc[16 + f];
         if (r < F) {
           float tot = 0.f;
 #pragma unroll
           for (int w = 0; w < 8; ++w) tot += xp[w * FP + r];
-          out[r * LDS_T + DH] = tot;
+          out[r * a.ldt + a.dvv] = tot;
         }
       }
     }
@@ -412,13 +412,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const Item m = c.m;
       if (m.bh != prev_bh) {  // W' and S operand of this sequence (no MMA of the old one in flight)
         prev_bh = m.bh;
-        const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
+        const float* tab = a.tin + m.bh * int64_t(F) * a.ldt;
         build_wop<256>(a, m.bh, sb + OFF_W);
         float srow[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          srow[f] = f < F ? tab[f * LDS_T + r] : 0.f;
-          A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
+          srow[f] = (f < F && r < a.dvv) ? tab[f * a.ldt + r] : 0.f;
+          A[f] = f < F ? tab[f * a.ldt + a.dvv] : 0.f;
         }
         if (h == 1) write_sop(sb + OFF_SOP, r, srow);
         fence_proxy_async();
@@ -769,12 +769,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       if (m.bh != prev_bh) {  // (re)load the sequence state: W', S_in (TMEM + S operand), A_in
         prev_bh = m.bh;
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 10, gc);
-        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
         float srow[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
-          srow[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
+          A[f] = f < F ? car[f * a.ldt + a.dvv] : 0.f;
+          srow[f] = (h == 1 && f < F && r < a.dvv) ? car[f * a.ldt + r] : 0.f;
         }
         build_wop<256, CT0>(a, m.bh, sb + OFF_W);
         if (h == 1) {  // S accumulator (lane r = value column r): cols 0..7 = S_in, the rest 0
@@ -1100,7 +1100,10 @@ bool tc_supported(const Geo& g) {
   // rows), at most 3 corner bits per table; a corner group (cb < P) is one table of up to 5 hyperplanes
   const int cb = pass_corner_bits(g);
   const int F = g.T << cb;
-  return g.dtype == 1 && g.d == 128 && g.dv == 128 && F <= tcfast::FP && g.T * g.P <= 5 && cb <= 3 &&
+  // head widths up to 128 (tiles are 128 wide; TMA zero-fills / clips beyond d, dv), multiples of 8
+  // (16-byte row pitch of the TMA maps)
+  return g.dtype == 1 && g.d >= 8 && g.d <= 128 && g.d % 8 == 0 && g.dv >= 8 && g.dv <= 128 && g.dv % 8 == 0 &&
+         F <= tcfast::FP && g.T * g.P <= 5 && cb <= 3 &&
          (g.cb == 0 || g.T == 1) && g.N > 0 && g.N < (int64_t(1) << 31) && g.seg_tokens % tcfast::CH == 0 &&
          tcfast::encode_fn() != nullptr;
 }
@@ -1109,7 +1112,7 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
                          cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv;
-  if (!make_map(&mk, k, g) || !make_map(&mv, v, g)) return cudaErrorInvalidValue;
+  if (!make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tout = part;
@@ -1127,7 +1130,7 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
                        cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mo;
-  if (!make_map(&mq, q, g) || !make_map(&mo, o, g)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mo, o, g, g.dv)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tin = tab;
@@ -1145,7 +1148,7 @@ cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* 
   using namespace tcfast;
   if (g.BH * g.N == 0) return cudaSuccess;
   CUtensorMap mq, mk;
-  if (!make_map(&mq, q, g) || !make_map(&mk, k, g)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.rows_out = rows;
@@ -1163,7 +1166,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
                           const float* car, void* o, float* den, float* nrm, bool krows, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mo, mr;
-  if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mo, o, g))
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mo, o, g, g.dv))
     return cudaErrorInvalidValue;
   if (krows && (!nrm || !make_map_rows(&mr, nrm, g.BH * g.N))) return cudaErrorInvalidValue;
   if (!krows) mr = mq;  // unused

@@ -214,14 +214,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const Item m = item_of(a, it);
       if (m.bh != prev_bh) {
         prev_bh = m.bh;
-        const float* tab = a.tin + m.bh * int64_t(F) * LDS_T;
+        const float* tab = a.tin + m.bh * int64_t(F) * a.ldt;
         build_wop<256>(a, m.bh, sb + OFF_W);
         build_w2<256>(a, m.bh, sb + OFF_W2);
         float scol[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          scol[f] = f < F ? tab[f * LDS_T + r] : 0.f;
-          A[f] = f < F ? tab[f * LDS_T + DH] : 0.f;
+          scol[f] = (f < F && r < a.dvv) ? tab[f * a.ldt + r] : 0.f;
+          A[f] = f < F ? tab[f * a.ldt + a.dvv] : 0.f;
         }
         if (h == 1) write_sopT(sb + OFF_SOPT, r, scol);
         fence_proxy_async();
@@ -292,14 +292,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       // segment done: partial dS (lane r = value column r) from its TMEM buffer, dA by a block sum
       mbar_wait(&acc_full[ns & 1], (ns >> 1) & 1);
       tc_fence_after();
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
       if (h == 1) {
         float acc[32];
         tmem_ld32(tmem + lb + TM_DS + 32 * (ns & 1), acc);
         tmem_ld_wait();
 #pragma unroll
         for (int f = 0; f < FP; ++f)
-          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+          if (f < F && r < a.dvv) out[f * a.ldt + r] = acc[f] + acc[16 + f];
       } else {
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[ns & 1]);
       compute_bar256();
-      if (h == 0 && r < F) out[r * LDS_T + DH] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
+      if (h == 0 && r < F) out[r * a.ldt + a.dvv] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
       compute_bar256();  // xda is reused by the next segment
     }
   }
@@ -470,14 +470,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const int t = cur.t;
       if (m.bh != prev_bh) {
         prev_bh = m.bh;
-        const float* dtab = a.tin + m.bh * int64_t(F) * LDS_T;
+        const float* dtab = a.tin + m.bh * int64_t(F) * a.ldt;
         build_wop<256>(a, m.bh, sb + OFF_W);
         build_w2<256>(a, m.bh, sb + OFF_W2);
         float dcol[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          dcol[f] = f < F ? dtab[f * LDS_T + r] : 0.f;
-          dA[f] = f < F ? dtab[f * LDS_T + DH] : 0.f;
+          dcol[f] = (f < F && r < a.dvv) ? dtab[f * a.ldt + r] : 0.f;
+          dA[f] = f < F ? dtab[f * a.ldt + a.dvv] : 0.f;
         }
         if (h == 1) {
           write_sopT(sb + OFF_DSOPT, r, dcol);
@@ -541,7 +541,7 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
                      float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mdo, mdq;
-  if (!make_map(&mq, q, g) || !make_map(&mdo, d_o, g) || !make_map(&mdq, dq, g)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mdo, d_o, g, g.dv) || !make_map(&mdq, dq, g, g.d)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tin = tab;
@@ -564,7 +564,7 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
                      void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv, mdk, mdv;
-  if (!make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mdk, dk, g) || !make_map(&mdv, dv, g))
+  if (!make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdk, dk, g, g.d) || !make_map(&mdv, dv, g, g.dv))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;

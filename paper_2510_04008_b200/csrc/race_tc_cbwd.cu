@@ -323,12 +323,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const Item m = item_of(a, it);
       if (m.bh != prev_bh) {  // (re)load the sequence state
         prev_bh = m.bh;
-        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        const float* car = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
         float scol[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          A[f] = f < F ? car[f * LDS_T + DH] : 0.f;
-          scol[f] = (h == 1 && f < F) ? car[f * LDS_T + r] : 0.f;
+          A[f] = f < F ? car[f * a.ldt + a.dvv] : 0.f;
+          scol[f] = (h == 1 && f < F && r < a.dvv) ? car[f * a.ldt + r] : 0.f;
         }
         build_wop<256>(a, m.bh, sb + OFF_W);
         if (h == 1) {
@@ -516,14 +516,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       // ---- segment done: dS total (TMEM) and dA total (block reduction)
       mbar_wait(acc_full, ni & 1);
       tc_fence_after();
-      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+      float* out = a.tout + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
       if (h == 1) {
         float acc[32];
         tmem_ld32(tmem + lb + TM_DS, acc);
         tmem_ld_wait();
 #pragma unroll
         for (int f = 0; f < FP; ++f)
-          if (f < F) out[f * LDS_T + r] = acc[f] + acc[16 + f];
+          if (f < F && r < a.dvv) out[f * a.ldt + r] = acc[f] + acc[16 + f];
       } else {
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tc_fence_before();
       mbar_arrive(acc_empty);
       compute_bar256();
-      if (h == 0 && r < F) out[r * LDS_T + DH] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
+      if (h == 0 && r < F) out[r * a.ldt + a.dvv] = ((xda[r] + xda[FP + r]) + xda[2 * FP + r]) + xda[3 * FP + r];
     }
   }
   tc_fence_before();
@@ -863,12 +863,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
       if (m.bh != prev_bh) {  // (re)load the suffix state dS_>seg, dA_>seg and W', W''
         prev_bh = m.bh;
-        const float* dcar = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * LDS_T;
+        const float* dcar = a.tin + (m.bh * a.nseg + m.seg) * int64_t(F) * a.ldt;
         float dcol[FP];
 #pragma unroll
         for (int f = 0; f < FP; ++f) {
-          dcol[f] = f < F ? dcar[f * LDS_T + r] : 0.f;
-          dA[f] = f < F ? dcar[f * LDS_T + DH] : 0.f;
+          dcol[f] = (f < F && r < a.dvv) ? dcar[f * a.ldt + r] : 0.f;
+          dA[f] = f < F ? dcar[f * a.ldt + a.dvv] : 0.f;
         }
         build_wop<256, CT0>(a, m.bh, sb + OFF_W);
         if (h == 1) {
@@ -1068,8 +1068,8 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
                             float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdq;
-  if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mdo, d_o, g) ||
-      !make_map(&mdq, dq, g))
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdo, d_o, g, g.dv) ||
+      !make_map(&mdq, dq, g, g.d))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -1102,8 +1102,8 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
                             const float* nrm, void* dk, void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
-  if (!make_map(&mq, q, g) || !make_map(&mk, k, g) || !make_map(&mv, v, g) || !make_map(&mdo, d_o, g) ||
-      !make_map(&mdk, dk, g) || !make_map(&mdv, dv, g))
+  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdo, d_o, g, g.dv) ||
+      !make_map(&mdk, dk, g, g.d) || !make_map(&mdv, dv, g, g.dv))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -1113,7 +1113,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.dbg = trace_for("bk");
   if (!nrm) return cudaErrorInvalidValue;
   CUtensorMap mrd, mgd, mrows, mdv2;
-  if (!make_map(&mdv2, dv, g)) return cudaErrorInvalidValue;
+  if (!make_map(&mdv2, dv, g, g.dv)) return cudaErrorInvalidValue;
   const int64_t np = (g.N + 3) & ~int64_t(3);
   if (!make_map_f32_1d(&mrd, rden, g.BH * np, 128) || !make_map_f32_1d(&mgd, gden, g.BH * np, 128) ||
       !make_map_rows(&mrows, nrm, g.BH * g.N))

@@ -46,6 +46,9 @@ struct Args {
   int64_t BH, H, N, nseg, seg_tokens;
   int64_t Np;  // row pitch of the per-token rden / gden arrays: N rounded up to a multiple of 4
   int P, T, TP;
+  int dw;   // head width d of the hyperplane rows (<= DH; tiles are zero-filled beyond it by TMA)
+  int dvv;  // value width dv (<= DH): tables [F, dv + 1] have row stride ldt = dv + 1, normaliser column dv
+  int ldt;
   float beta;
   int normalize, w_per_head;
   const float* w;
@@ -248,7 +251,7 @@ __device__ __forceinline__ float inv_scale(float sumsq, int normalize) {
 // W' rows 3j, 3j+1, 3j+2 = W_hi[j], W_mid[j], W_lo[j] (W to 24 bits), K-major SW128
 template <int NTC = 128, int T0 = 64>
 __device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wop) {
-  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * a.dw : 0);
   for (int idx = threadIdx.x - T0; idx < 16 * 16; idx += NTC) {
     const int n = idx >> 4, j = idx & 15;  // row n, 8-element chunk j
     const int hp = n / 3, piece = n % 3;
@@ -260,7 +263,8 @@ __device__ __forceinline__ void build_wop(const Args& a, int64_t bh, uint32_t wo
       for (int h = 0; h < 2; ++h) {
         float v = 0.f;
         if (hp < a.TP) {
-          const float x = w[hp * DH + j * 8 + e * 2 + h];
+          const int col = j * 8 + e * 2 + h;
+          const float x = col < a.dw ? w[hp * a.dw + col] : 0.f;
           const float hi = bf16_round(x);
           const float mid = bf16_round(x - hi);
           v = piece == 0 ? hi : piece == 1 ? mid : bf16_round(x - hi - mid);
@@ -480,7 +484,7 @@ __device__ __forceinline__ uint64_t desc_w2(uint32_t base, int kk) {
 }
 template <int NTC = 128, int T0 = 64>
 __device__ __forceinline__ void build_w2(const Args& a, int64_t bh, uint32_t w2) {
-  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * a.dw : 0);
   for (int idx = threadIdx.x - T0; idx < 32 * 16; idx += NTC) {
     const int k = idx >> 4, j = idx & 15;  // K-row k, 8-element column chunk j
     const int blk = k >> 3, hp = k & 7;
@@ -492,7 +496,8 @@ __device__ __forceinline__ void build_w2(const Args& a, int64_t bh, uint32_t w2)
       for (int h = 0; h < 2; ++h) {
         float v = 0.f;
         if (blk < 3 && hp < a.TP) {
-          const float x = w[hp * DH + j * 8 + e * 2 + h];
+          const int col = j * 8 + e * 2 + h;
+          const float x = col < a.dw ? w[hp * a.dw + col] : 0.f;
           const float hi = bf16_round(x);
           v = blk == 2 ? x - hi : hi;
         }
@@ -793,7 +798,7 @@ __device__ __forceinline__ void tmem_half_to_global(uint32_t tmem_col, int h, fl
 
 // W' / W'' builds spread over the 256 compute threads
 __device__ __forceinline__ void build_ops_256(const Args& a, int64_t bh, uint32_t wop, uint32_t w2) {
-  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * a.dw : 0);
   const int tid = threadIdx.x - 64;
   for (int idx = tid; idx < 16 * 16 + 32 * 16; idx += 256) {
     uint32_t pk[4];
@@ -807,7 +812,8 @@ __device__ __forceinline__ void build_ops_256(const Args& a, int64_t bh, uint32_
         for (int hh = 0; hh < 2; ++hh) {
           float v = 0.f;
           if (hp < a.TP) {
-            const float x = w[hp * DH + j * 8 + e * 2 + hh];
+            const int col = j * 8 + e * 2 + hh;
+            const float x = col < a.dw ? w[hp * a.dw + col] : 0.f;
             const float hi = bf16_round(x);
             const float mid = bf16_round(x - hi);
             v = piece == 0 ? hi : piece == 1 ? mid : bf16_round(x - hi - mid);
@@ -827,7 +833,8 @@ __device__ __forceinline__ void build_ops_256(const Args& a, int64_t bh, uint32_
         for (int hh = 0; hh < 2; ++hh) {
           float v = 0.f;
           if (blk < 3 && hp < a.TP) {
-            const float x = w[hp * DH + j * 8 + e * 2 + hh];
+            const int col = j * 8 + e * 2 + hh;
+            const float x = col < a.dw ? w[hp * a.dw + col] : 0.f;
             const float hi = bf16_round(x);
             v = blk == 2 ? x - hi : hi;
           }
@@ -954,8 +961,11 @@ __device__ __forceinline__ void tangent_half_inplace(uint32_t tmem_col, uint8_t*
 // fp32 hyperplane rows (TP x 128, zero-padded to 5 rows) for the CUDA-core dx^ = dproj . W
 template <int NTC, int T0>
 __device__ __forceinline__ void build_wf32(const Args& a, int64_t bh, float* wf) {
-  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * DH : 0);
-  for (int idx = threadIdx.x - T0; idx < 5 * DH; idx += NTC) wf[idx] = idx < a.TP * DH ? w[idx] : 0.f;
+  const float* w = a.w + (a.w_per_head ? (bh % a.H) * int64_t(a.TP) * a.dw : 0);
+  for (int idx = threadIdx.x - T0; idx < 5 * DH; idx += NTC) {
+    const int j = idx / DH, c = idx % DH;
+    wf[idx] = (j < a.TP && c < a.dw) ? w[j * a.dw + c] : 0.f;
+  }
 }
 // columns [64h, 64h + 64) of row r: dx^ = dproj . W (fp32 FMA, W from smem), then the
 // sphere-tangent VJP dx = (dx^ - (dx^.x^) x^) / ||x||, written as bf16 over x in the SW128 tile
@@ -1029,11 +1039,14 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // [BH, N, 128] bf16 viewed as 3-D {128, N, BH}; box {64, 128, 1}; SW128
-inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g) {
+// width = the tensor's row length (d for Q, K, dQ, dK; dv for V, O, dO, dV), <= DH: the two 64-column
+// boxes of a tile read zeros beyond it and stores beyond it are clipped, so narrower heads run on the
+// same kernels without padded copies
+inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g, int width) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {cuuint64_t(DH), cuuint64_t(g.N), cuuint64_t(g.BH)};
-  cuuint64_t strides[2] = {cuuint64_t(DH) * 2, cuuint64_t(g.N) * DH * 2};
+  cuuint64_t dims[3] = {cuuint64_t(width), cuuint64_t(g.N), cuuint64_t(g.BH)};
+  cuuint64_t strides[2] = {cuuint64_t(width) * 2, cuuint64_t(g.N) * width * 2};
   cuuint32_t box[3] = {64, CH, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
@@ -1089,6 +1102,9 @@ inline Args make_args(const Geo& g) {
   a.P = pass_corner_bits(g);  // corner bits of this pass (the kernels' template P)
   a.T = g.T;
   a.TP = g.T * g.P;           // projections (all hyperplanes of the pass's tables)
+  a.dw = g.d;
+  a.dvv = g.dv;
+  a.ldt = g.dv + 1;
   a.hb = g.P - a.P;
   a.chi = int(g.chi);
   a.ext_rd = g.ext_rden;

@@ -235,31 +235,7 @@ def _race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: boo
     return dq, dk, dv
 
 
-FAST_DIM = 128  # head width of the sm_100a tcgen05 kernels
-
-
-def _padded_fast(q: torch.Tensor, v: torch.Tensor, w, p: SketchParams) -> bool:
-    """bf16 heads narrower than 128 run zero-padded to 128 when that puts them on the tcgen05 path.
-
-    Padding is exact: norms and projections are unchanged (the hyperplanes are padded with zeros),
-    the padded value columns of O are zero and every padded gradient component is zero."""
-    if q.dtype != torch.bfloat16 or not q.is_cuda or q.dim() < 2:
-        return False
-    d, dv = q.shape[-1], v.shape[-1]
-    if d > FAST_DIM or dv > FAST_DIM or (d == FAST_DIM and dv == FAST_DIM):
-        return False
-    _, per_head, heads = prepare_w(torch.as_tensor(w), p, d, q.device)
-    bh = 1
-    for x in q.shape[:-2]:
-        bh *= x
-    m = _meta(dtype=_lib.RACE_BF16, batch_heads=max(bh, 1), heads=heads, n=q.shape[-2], dim=FAST_DIM,
-              dim_v=FAST_DIM, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
-              causal=p.causal, normalize=p.normalize, w_per_head=per_head)
-    return m.fast_plan  # one tcgen05 pass, or tcgen05 table / corner groups
-
-
-def _pad(t: torch.Tensor) -> torch.Tensor:
-    return torch.nn.functional.pad(t, (0, FAST_DIM - t.shape[-1])).contiguous()
+FAST_DIM = 128  # maximum head width of the sm_100a tcgen05 kernels (narrower bf16 heads run natively)
 
 
 def _on_q_device(fn):
@@ -281,15 +257,11 @@ def race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True, pad: b
     """O, den (float32, the reference's averaged den) and the backward state.
 
     One fwd pass = key-side aggregation -> fixed-order combine -> readout
-    (non-causal) or chunked scan (causal); see race_fwd in race_b200.h.  bf16
-    heads narrower than 128 run zero-padded on the tcgen05 kernels (the state
-    then describes the padded problem; race_backward pads the same way).  ``pad=False`` keeps the
-    native width (generic CUDA-core kernels)."""
-    if pad and _padded_fast(q, v, w, p):
-        dv = v.shape[-1]
-        o, den, st = _race_forward(_pad(q), _pad(k), _pad(v), _pad(torch.as_tensor(w).to(q.device)), p,
-                                   want_state=want_state)
-        return o[..., :dv].contiguous(), den, st
+    (non-causal) or chunked scan (causal); see race_fwd in race_b200.h.  bf16 heads of any width
+    d, dv <= 128 (multiples of 8) run on the tcgen05 kernels natively: the TMA maps zero-fill the
+    tile columns beyond d and clip the stores, so no padded copies are made.  ``pad`` is accepted
+    for compatibility with round-1 callers and ignored."""
+    del pad
     return _race_forward(q, k, v, w, p, want_state=want_state)
 
 
@@ -299,18 +271,8 @@ def race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: bool
 
     ``inplace=True`` writes the gradients over q, k, v (which must be contiguous) and returns
     those tensors: the inputs are dead after the backward, so the layer holds 4 instead of 7
-    N x d tensors (race_bwd allows dq, dk, dv to alias q, k, v).  ``pad`` must match the
-    race_forward call whose state is passed."""
-    if pad and _padded_fast(q, v, w, p):
-        d, dv = q.shape[-1], v.shape[-1]
-        dq, dk, dvv = _race_backward(_pad(q), _pad(k), _pad(v), _pad(torch.as_tensor(w).to(q.device)), _pad(d_o), p,
-                                     state=state, inplace=True)
-        grads = (dq[..., :d], dk[..., :d], dvv[..., :dv])
-        if inplace:
-            for dst, src in zip((q, k, v), grads):
-                dst.copy_(src)
-            return q, k, v
-        return tuple(g.contiguous() for g in grads)
+    N x d tensors (race_bwd allows dq, dk, dv to alias q, k, v).  ``pad`` is ignored."""
+    del pad
     return _race_backward(q, k, v, w, d_o, p, state=state, inplace=inplace)
 
 

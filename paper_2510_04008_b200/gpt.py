@@ -51,9 +51,7 @@ class Block(nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         b, n, c = x.shape
         q, k, v = self.qkv(self.ln1(x)).split(c, dim=-1)
-        q, k, v = (t.view(b, n, self.heads, c // self.heads).transpose(1, 2) for t in (q, k, v))
-        if not self.attn.pad:  # the padded path copies (transpose + zero-pad) in one F.pad
-            q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        q, k, v = (t.view(b, n, self.heads, c // self.heads).transpose(1, 2).contiguous() for t in (q, k, v))
         o = self.attn(q, k, v)
         x = x + self.proj(o.transpose(1, 2).reshape(b, n, c))
         return x + self.out(F.gelu(self.fc(self.ln2(x)), approximate="tanh"))

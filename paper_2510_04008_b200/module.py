@@ -25,18 +25,14 @@ def head_hyperplanes(cfg: SketchConfig, heads: int, dim: int) -> torch.Tensor:
     return torch.from_numpy(np.stack(ws).astype(np.float32))
 
 
-FAST_DIM = 128  # head dim of the sm_100a tcgen05 kernels
-
-
 class RaceAttention(torch.nn.Module):
     """O = RACE(Q, K, V) on [B, H, N, d] CUDA tensors (fp32 or bf16), differentiable.
 
-    bf16 heads with d < 128 (e.g. the d=64 heads of a d_model=768, 12-head GPT)
-    are zero-padded to 128 on the way in and sliced on the way out, so they run
-    on the tcgen05 kernels.  Padding is exact: row norms and projections are
-    unchanged (the hyperplanes are padded with zeros), the padded value columns
-    of O are zero and every padded gradient component is zero.  ``pad_head_dim
-    = False`` keeps the native width (generic CUDA-core kernels)."""
+    bf16 heads of width up to 128 (e.g. the d=64 heads of a d_model=768, 12-head GPT) run on the
+    tcgen05 kernels at their own width (no padded copies); fp32 inputs and other widths run on
+    the CUDA-core kernels.  ``pad_head_dim`` is kept for compatibility and has no effect."""
+
+    pad = False  # narrow heads are no longer zero-padded (gpt.py checks this)
 
     def __init__(self, heads: int, dim: int, cfg: SketchConfig, pad_head_dim: bool = True):
         super().__init__()
@@ -44,17 +40,10 @@ class RaceAttention(torch.nn.Module):
         self.heads = heads
         self.dim = dim
         self.pad_head_dim = pad_head_dim
-        self.pad = pad_head_dim and dim < FAST_DIM
         self.params_ = SketchParams(cfg.hyperplanes, cfg.total_tables, float(cfg.beta), cfg.causal,
                                     cfg.normalize_inputs)
         w = head_hyperplanes(cfg, heads, dim)
         self.register_buffer("w", w, persistent=True)
-        if self.pad:
-            self.register_buffer("w_pad", torch.nn.functional.pad(w, (0, FAST_DIM - dim)), persistent=False)
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
-        if self.pad and q.dtype == torch.bfloat16:
-            extra = (0, FAST_DIM - self.dim)
-            qp, kp, vp = (torch.nn.functional.pad(t, extra) for t in (q, k, v))
-            return race_attention_torch(qp, kp, vp, self.w_pad, self.params_)[..., : v.shape[-1]]
-        return race_attention_torch(q, k, v, self.w, self.params_, pad=self.pad_head_dim)
+        return race_attention_torch(q, k, v, self.w, self.params_)

@@ -484,10 +484,12 @@ def test_inplace_backward_matches(causal, kind):
 
 
 @pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
-@pytest.mark.parametrize("dims", [(64, 64), (96, 128), (128, 32)], ids=["d64", "d96dv128", "dv32"])
-def test_narrow_bf16_heads_run_padded_on_fast_path(causal, dims):
-    """bf16 heads narrower than 128 are zero-padded onto the tcgen05 kernels by race_forward /
-    race_backward; results match the generic path at the native width and the oracle."""
+@pytest.mark.parametrize("dims", [(64, 64), (96, 128), (128, 32), (8, 8), (40, 72)],
+                         ids=["d64", "d96dv128", "dv32", "d8", "d40dv72"])
+def test_narrow_bf16_heads_run_natively_on_fast_path(causal, dims):
+    """bf16 heads narrower than 128 run on the tcgen05 kernels at their own width (TMA zero-fills the
+    tile columns beyond d, clips the stores; tables use the dv + 1 row stride); results match the
+    generic path and the oracle."""
     dev = _cuda()
     d, dv = dims
     n = 3000
@@ -497,9 +499,9 @@ def test_narrow_bf16_heads_run_padded_on_fast_path(causal, dims):
     cfg = rb.SketchConfig(hyperplanes=2, tables=2, seed=4, causal=causal)
     w = rb.head_hyperplanes(cfg, 2, d).to(dev)
     p = cfg.params()
-    from paper_2510_04008_b200.functional import _padded_fast
+    from paper_2510_04008_b200.functional import Problem
 
-    assert _padded_fast(q, v, w, p)
+    assert _lib.fast_path(Problem(q, k, v, w, p).desc)
 
     def run():
         o, den, st = rb.race_forward(q, k, v, w, p)
