@@ -34,14 +34,20 @@ constexpr uint32_t IDC_DVB = idesc_bf16(128, 128, 0, 1);  // P~^T x dO          
 // ===========================================================================
 // causal backward, query side -- pipelined 8-compute-warp version (launched)
 //
-// Same math as k_bwd_causal_q above, restructured for latency:
+// Same math as the chunk form above, restructured for latency:
 //  * contiguous CTA ranges: S, A continue across segments; dS / dA totals are
 //    emitted per segment;
+//  * no Pm = Phi_q Phi_k^T: the two row statistics it fed factor through Phi_k,
+//      sum_{j<=t} Pm_tj        = phi_q,t . C_t,   C_t = sum_{j<=t} phi_k,j  (warp scan)
+//      sum_{j<=t} Pm_tj E_tj   = phi_q,t . Z_t,   Z   = tril(E) Phi_k      (MMA)
+//    so dphi_q,t = (y_t + Z_t - rho_t (A_<c + C_t)) / D_t needs one MMA round
+//    trip per chunk after the features, and tril(E) is packed (hi / lo bf16
+//    pairs in TMEM, the A operands of Z: E to 16 bits, so rho and the key
+//    side's gden = -rho / D stay fp32-exact) as soon as E lands;
 //  * compute warps 2..9 split every 128-column pass into halves;
-//  * E~ = tril(E - rho) lives in TMEM as the A operand of Z = E~ Phi_k;
 //  * Q and dO are double-buffered, so the MMA warp issues the NEXT chunk's
-//    projection and E / Y right after this chunk's Z / dS -- they complete
-//    while the compute warps finish this chunk;
+//    E / Y right after this chunk's dx^ / dS -- they complete while the compute
+//    warps finish this chunk;
 //  * dx^ = dproj . W is one MMA pair against the projection operand W'
 //    itself (read MN-major: W_hi + W_mid + W_lo, i.e. W to 24 bits) with
 //    dproj split hi / lo; the sphere-tangent VJP writes dq over q in its
@@ -55,18 +61,18 @@ constexpr int OFF_V = 2 * TILE;
 constexpr int OFF_DO = 3 * TILE;               // two buffers
 constexpr int OFF_W = 5 * TILE;                // W' (B of the projection; B of dx^ read MN-major)
 constexpr int OFF_SOPT = OFF_W + WOP;
-constexpr int OFF_PHIQ = OFF_SOPT + WOP;       // Phi_q (A of Pm), then phi_q / D (B of dS)
-constexpr int OFF_PHIK = OFF_PHIQ + PHI;       // Phi_k (A of Pm, B of S and Z), then dproj (A of dx^)
-constexpr int OFF_X = OFF_PHIK + PHI;          // [2 parity] x { rs[2][128], nd[2][128], kp[4][8] }, then da[4][8]
-constexpr int XPAR = 256 + 256 + 32;
-constexpr int OFF_TOK = OFF_X + (2 * XPAR + 32) * 4;  // [2] x sketch rows [128][ROWW] (TMA)
+constexpr int OFF_PHIQ = OFF_SOPT + WOP;       // phi_q / D (B of dS)
+constexpr int OFF_PHIK = OFF_PHIQ + PHI;       // Phi_k (B of S and Z), then dproj (A of dx^)
+constexpr int OFF_X = OFF_PHIK + PHI;          // kp[2 parity][4][8], cs[128][8] (in-warp scans of phi_k), da[4][8]
+constexpr int XKP = 0, XCS = 64, XDA = 64 + CH * FP;
+constexpr int OFF_TOK = OFF_X + (XDA + 32) * 4;  // [2] x sketch rows [128][ROWW] (TMA)
 constexpr int TOK_BYTES = CH * ROWW * 4;
 constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "k_bwd_causal_q8 shared memory");
 static_assert(OFF_TOK % 128 == 0, "TMA destination alignment");
-constexpr uint32_t TM_Y = 32, TM_Z = 48, TM_S = 80, TM_DS = 112, TM_ET = 144, TM_PMC = 256,
-                   TM_E = 384, TM_DX = 256;
+constexpr uint32_t TM_Y = 0, TM_Z = 32, TM_S = 64, TM_DS = 96, TM_ETH = 128, TM_ETL = 192, TM_DX = 256,
+                   TM_E = 384;
 // W' [16 x 128] (rows = hyperplane pieces, d contiguous, two SW128 64-column sub-tiles) as an MN-major B
 __device__ __forceinline__ uint64_t desc_wT(uint32_t base) { return smem_desc(base, 2048, 1024, kSw128); }
 // dproj expanded to W's rows: K cols 3j..3j+2 = dproj_j (hi) and 16 + 3j.. (lo)
@@ -111,10 +117,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   uint64_t* fullV = bars + 14;
   uint64_t* emptyV = bars + 15;
   uint64_t* c1 = bars + 16;        // projection + E + Y
-  uint64_t* c2 = bars + 17;        // Pm + S state
-  uint64_t* c3 = bars + 18;        // Z + dS
-  uint64_t* phi_ready = bars + 19;
-  uint64_t* et_ready = bars + 20;
+  uint64_t* c2 = bars + 17;        // Z + S state
+  uint64_t* phi_ready = bars + 19;  // Phi_k + tril(E) staged (256 arrivals)
   uint64_t* wready = bars + 21;
   uint64_t* acc_full = bars + 22;
   uint64_t* acc_empty = bars + 23;
@@ -135,7 +139,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     }
     for (int i = 12; i < 19; ++i) mbar_init(&bars[i], 1);
     mbar_init(phi_ready, 256);
-    mbar_init(et_ready, 256);
     mbar_init(wready, 256);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 256);
@@ -246,28 +249,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           tc_fence_after();
           issue_front(gc);
         }
-        mbar_wait(phi_ready, par);
+        mbar_wait(phi_ready, par);  // Phi_k and tril(E) (hi / lo) staged
         RACE_TRACE(a, 6, gc);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem + TM_PMC, desc_phi_k(sb + OFF_PHIQ, kk), desc_phi_k(sb + OFF_PHIK, kk), IDC_PM, kk > 0);
+          for (int kk = 0; kk < 8; ++kk)  // Z = tril(E) Phi_k: dphi_q's intra-chunk term and the row statistic
+            umma_bf16_ts(tmem + TM_Z, tmem + TM_ETH + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // E to 16 bits: rho (and gden for the key side) stays fp32-exact
+            umma_bf16_ts(tmem + TM_Z, tmem + TM_ETL + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, 1u);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             umma_bf16(tmem + TM_S, desc_tile_mn(sb + OFF_V, kk), desc_phi_mn(sb + OFF_PHIK, kk), IDC_ST, 1u);
           umma_commit(c2);
           umma_commit(emptyV);
-        }
-        __syncwarp();
-        mbar_wait(et_ready, par);
-        RACE_TRACE(a, 7, gc);
-        tc_fence_after();
-        if (elect_one()) {  // Z (dphi_q's intra-chunk term): on the dq-critical path
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16_ts(tmem + TM_Z, tmem + TM_ET + kk * 8, desc_phi_mn(sb + OFF_PHIK, kk), IDC_Z, kk > 0);
-          umma_commit(c3);
         }
         __syncwarp();
         mbar_wait(dp_ready, par);
@@ -307,13 +303,16 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
     const float invT = 1.f / float(a.T);
     const int F = a.T << a.P;
     float* xbase = reinterpret_cast<float*>(smem + OFF_X);
-    float* xda = xbase + 2 * XPAR;
-    {  // E~ blocks above the diagonal are never written: zero the A operand once
+    float* xcs = xbase + XCS;
+    float* xda = xbase + XDA;
+    {  // tril(E) blocks above the diagonal are never written: zero the A operands once
       uint32_t z[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) z[j] = 0u;
-      tmem_st16u(tmem + lb + TM_ET + 32 * h, z);
-      tmem_st16u(tmem + lb + TM_ET + 32 * h + 16, z);
+      tmem_st16u(tmem + lb + TM_ETH + 32 * h, z);
+      tmem_st16u(tmem + lb + TM_ETH + 32 * h + 16, z);
+      tmem_st16u(tmem + lb + TM_ETL + 32 * h, z);
+      tmem_st16u(tmem + lb + TM_ETL + 32 * h + 16, z);
       tmem_st_wait();
     }
     float A[FP], dA[FP];
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const uint32_t par = gc & 1;
         const int s = gc & 1;
         uint8_t* qtile = smem + OFF_Q + s * TILE;
-        float* xpar = xbase + par * XPAR;
+        float* xkp = xbase + XKP + par * 32;
         const bool valid = t + r < m.t1;
         const GroupPre pre = GRP ? group_prefetch(a, m.bh, t, r, valid) : GroupPre{};
         mbar_wait(&fullT[s], (gc >> 1) & 1);
@@ -367,140 +366,127 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive(&emptyT[s]);
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 9, gc);
         float phq[FP], uq[5];
-        if (h == 0) {
-          row_features_hat<P, HB>(a, hq, valid, phq, uq);
-          write_phi_q(sb + OFF_PHIQ, r, phq);
-          fence_proxy_async();
-          tc_fence_before();
-          mbar_arrive(phi_ready);
-        } else {
+        if (h == 1) {  // Phi_k operand, in-warp inclusive scan of phi_k (C_t) and the warp totals
           float phk[FP], uk[5];
           row_features_hat<P, HB>(a, hatk, valid, phk, uk);
           write_phi_k(sb + OFF_PHIK, r, phk);
-          fence_proxy_async();
-          tc_fence_before();
-          mbar_arrive(phi_ready);
+          const int lane = lane_id();
 #pragma unroll
-          for (int f = 0; f < FP; ++f) {
+          for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) phk[f] += __shfl_xor_sync(0xffffffffu, phk[f], o);
+            for (int f = 0; f < FP; ++f) {
+              const float x = __shfl_up_sync(0xffffffffu, phk[f], o);
+              if (lane >= o) phk[f] += x;
+            }
           }
-          if (lane_id() == 0) {
 #pragma unroll
-            for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
+          for (int f = 0; f < FP; ++f) xcs[r * FP + f] = phk[f];
+          if (lane == 31) {
+#pragma unroll
+            for (int f = 0; f < FP; ++f) xkp[qw * FP + f] = phk[f];
           }
-          row_features_hat<P, HB>(a, hq, valid, phq, uq);
         }
-        float yv[16];
+        row_features_hat<P, HB>(a, hq, valid, phq, uq);
+        // tril(E) -> hi / lo bf16 pairs into TMEM (A operands of Z), my 64 columns
         mbar_wait(c1, par);
         tc_fence_after();
-        tmem_ld16(tmem + lb + TM_Y, yv);
-        tmem_ld_wait();
-        float y[FP], Dint = 0.f, ydot = 0.f;
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-          y[f] = yv[f] + yv[8 + f];
-          Dint = fmaf(phq[f], A[f], Dint);
-          ydot = fmaf(phq[f], y[f], ydot);
-        }
-        // ---- row statistics from Pm and E over my 64 columns
-        mbar_wait(c2, par);
-        if (threadIdx.x == a.ttid) RACE_TRACE(a, 10, gc);
-        tc_fence_after();
-        float rs = 0.f, nd = 0.f;
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int c0 = 64 * h + 32 * b;
           if ((c0 >> 5) <= qw) {  // warp-uniform
-#pragma unroll
-            for (int hh = 0; hh < 32; hh += 16) {  // 16 columns at a time: keeps register pressure down
-              float pm[16], e[16];
-              tmem_ld16(tmem + lb + TM_PMC + c0 + hh, pm);
-              tmem_ld16(tmem + lb + TM_E + c0 + hh, e);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float pmj = (c0 + hh + j <= r) ? pm[j] : 0.f;
-                rs += pmj;
-                nd = fmaf(pmj, e[j], nd);
-              }
-            }
-          }
-        }
-        xpar[h * 128 + r] = rs;
-        xpar[256 + h * 128 + r] = nd;
-        compute_bar256();
-        const float D = Dint + (xpar[r] + xpar[128 + r]);
-        const float ndt = xpar[256 + r] + xpar[384 + r];
-        const bool live = valid && D * invT > kDegenerateDenEps;
-        float rD = live ? 1.f / D : 0.f;
-        float rho = (ydot + ndt) * rD;
-        if (GRP && a.ext_rd) {  // table / corner group: normalisers of the whole estimator
-          rD = pre.rd;
-          rho = rD != 0.f ? -pre.gd / rD : 0.f;
-        }
-        // E~ = tril(E - rho) -> bf16 pairs into TMEM (A of Z)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int c0 = 64 * h + 32 * b;
-          if ((c0 >> 5) <= qw) {
             float e[32];
-            uint32_t u[16];
+            uint32_t uh[16], ul[16];
             tmem_ld32(tmem + lb + TM_E + c0, e);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              u[j] = pack_bf16((c0 + 2 * j <= r) ? e[2 * j] - rho : 0.f,
-                               (c0 + 2 * j + 1 <= r) ? e[2 * j + 1] - rho : 0.f);
-            tmem_st16u(tmem + lb + TM_ET + (c0 >> 1), u);
+            for (int j = 0; j < 16; ++j) {
+              const float e0 = (c0 + 2 * j <= r) ? e[2 * j] : 0.f;
+              const float e1 = (c0 + 2 * j + 1 <= r) ? e[2 * j + 1] : 0.f;
+              const float h0 = bf16_round(e0), h1 = bf16_round(e1);
+              uh[j] = pack_bf16(h0, h1);
+              ul[j] = pack_bf16(e0 - h0, e1 - h1);
+            }
+            tmem_st16u(tmem + lb + TM_ETH + (c0 >> 1), uh);
+            tmem_st16u(tmem + lb + TM_ETL + (c0 >> 1), ul);
           }
-        }
-        if (h == 1) {
-          float pht[FP];
-#pragma unroll
-          for (int f = 0; f < FP; ++f) pht[f] = phq[f] * rD;
-          write_phi_k(sb + OFF_PHIQ, r, pht);  // Phi_q is dead after Pm (c2): reuse its buffer
-          // S_<=c for the next chunk's y (the Y MMA of this chunk completed at c1)
-          float sacc[32];
-          tmem_ld32(tmem + lb + TM_S, sacc);
-          tmem_ld_wait();
-          float snext[FP];
-#pragma unroll
-          for (int f = 0; f < FP; ++f) snext[f] = sacc[f] + sacc[16 + f];
-          write_sopT(sb + OFF_SOPT, r, snext);
-        } else {
-#pragma unroll
-          for (int f = 0; f < FP; ++f) dA[f] = fmaf(phq[f], -rho * rD, dA[f]);
         }
         tmem_st_wait();
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(et_ready);
-        if (h == 0 && valid && !a.ext_rd) {
-          rden[m.bh * a.Np + t + r] = rD;  // row pitch Np (multiple of 4: 16-byte TMA tiles)
-          gden[m.bh * a.Np + t + r] = -rho * rD;
-        }
-        // ---- dphi_q -> dproj
-        mbar_wait(c3, par);
-        if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
-        tc_fence_after();
-        float zz[32];
-        tmem_ld32(tmem + lb + TM_Z, zz);
+        mbar_arrive(phi_ready);
+        float yv[16];
+        tmem_ld16(tmem + lb + TM_Y, yv);
+        compute_bar256();  // the phi_k scans and warp totals are visible
+        float y[FP], C[FP], Dint = 0.f, ydot = 0.f, rs = 0.f;
         tmem_ld_wait();
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          float c = xcs[r * FP + f];
+          for (int w = 0; w < qw; ++w) c += xkp[w * FP + f];  // warp-uniform trip count
+          C[f] = c;
+          y[f] = yv[f] + yv[8 + f];
+          Dint = fmaf(phq[f], A[f], Dint);
+          ydot = fmaf(phq[f], y[f], ydot);
+          rs = fmaf(phq[f], c, rs);
+        }
+        // ---- Z landed: row statistics, dphi_q -> dproj
+        mbar_wait(c2, par);
+        if (threadIdx.x == a.ttid) RACE_TRACE(a, 10, gc);
+        tc_fence_after();
+        float zhi[8], zlo[8];
+        tmem_ld8(tmem + lb + TM_Z, zhi);
+        tmem_ld8(tmem + lb + TM_Z + 16, zlo);
+        tmem_ld_wait();
+        float Z[FP], nd = 0.f;
+#pragma unroll
+        for (int f = 0; f < FP; ++f) {
+          Z[f] = zhi[f] + zlo[f];
+          nd = fmaf(phq[f], Z[f], nd);
+        }
+        const float D = Dint + rs;
+        const bool live = valid && D * invT > kDegenerateDenEps;
+        float rD = live ? 1.f / D : 0.f;
+        float rho = (ydot + nd) * rD;
+        if (GRP && a.ext_rd) {  // table / corner group: normalisers of the whole estimator
+          rD = pre.rd;
+          rho = rD != 0.f ? -pre.gd / rD : 0.f;
+        }
         float dphi[FP];
 #pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f] + zz[f] + zz[16 + f]) * rD;
+        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] + Z[f] - rho * (A[f] + C[f])) * rD;
         float dproj[8];
         row_feature_vjp<P, HB>(a, uq, phq, dphi, dproj);
         if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
         const float dotq = dot_from_proj(dproj, hq);
-        if (h == 0) write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z (c3)
+        if (h == 0) {
+          write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z and S (c2)
 #pragma unroll
-        for (int f = 0; f < FP; ++f)
-          A[f] += ((xpar[512 + f] + xpar[512 + FP + f]) + xpar[512 + 2 * FP + f]) + xpar[512 + 3 * FP + f];
+          for (int f = 0; f < FP; ++f) dA[f] = fmaf(phq[f], -rho * rD, dA[f]);
+        } else {
+          float pht[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) pht[f] = phq[f] * rD;
+          write_phi_k(sb + OFF_PHIQ, r, pht);  // B of dS (the previous chunk's dS MMA is done: dsdone)
+          // S_<=c for the next chunk's y (the Y MMA of this chunk completed at c1); columns 8..15
+          // and 24..31 of the N = 32 product are the duplicate hi copy and padding: not read
+          float shi[8], slo[8];
+          tmem_ld8(tmem + lb + TM_S, shi);
+          tmem_ld8(tmem + lb + TM_S + 16, slo);
+          tmem_ld_wait();
+          float snext[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) snext[f] = shi[f] + slo[f];
+          write_sopT(sb + OFF_SOPT, r, snext);
+        }
+#pragma unroll
+        for (int f = 0; f < FP; ++f) A[f] += ((xkp[f] + xkp[FP + f]) + xkp[2 * FP + f]) + xkp[3 * FP + f];
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(dp_ready);
+        if (h == 0 && valid && !a.ext_rd) {
+          rden[m.bh * a.Np + t + r] = rD;  // row pitch Np (multiple of 4: 16-byte TMA tiles)
+          gden[m.bh * a.Np + t + r] = -rho * rD;
+        }
         // ---- dq (my 64 columns) in place of q; the producer stores it
         mbar_wait(c4, par);
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 12, gc);
