@@ -348,53 +348,101 @@ __device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
 }
 
 // num_acc (+)= o_g * D_g, d_acc (+)= D_g with D_g = den_g * tg (den_g is the group's averaged den);
-// one warp per row (no index division per element), 4 columns per lane step when VEC
+// one warp per kAccRows rows (no index division per element; every load of the rows issued before the
+// first store), 4 columns per lane step when VEC
+constexpr int kAccRows = 4;
 template <typename T, bool VEC>
 __global__ void k_group_fwd_acc(int64_t rows, int dv, const T* __restrict__ o, const float* __restrict__ den, float tg,
                                 int first, float* __restrict__ num_acc, float* __restrict__ d_acc) {
-  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kAccRows;
   const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float D = den[r] * tg;
-  const T* orow = o + r * dv;
-  float* nrow = num_acc + r * dv;
-  if (VEC) {
-    for (int c = 4 * lane; c < dv; c += 128) {
-      const float4 x = ld4(orow + c);
-      float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(nrow + c);
-      a.x = fmaf(x.x, D, a.x);
-      a.y = fmaf(x.y, D, a.y);
-      a.z = fmaf(x.z, D, a.z);
-      a.w = fmaf(x.w, D, a.w);
-      st4(nrow + c, a);
+  if (r0 >= rows) return;
+  if (VEC && dv <= 128) {  // every load of the warp's rows first
+    const int c = 4 * lane;
+    float4 x[kAccRows], acc[kAccRows];
+    float D[kAccRows];
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      const bool ok = r < rows && c < dv;
+      D[q] = r < rows ? den[r] * tg : 0.f;
+      x[q] = ok ? ld4(o + r * dv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = (ok && !first) ? ld4(num_acc + r * dv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      if (r < rows && c < dv)
+        st4(num_acc + r * dv + c, make_float4(fmaf(x[q].x, D[q], acc[q].x), fmaf(x[q].y, D[q], acc[q].y),
+                                              fmaf(x[q].z, D[q], acc[q].z), fmaf(x[q].w, D[q], acc[q].w)));
     }
   } else {
-    for (int c = lane; c < dv; c += 32) nrow[c] = fmaf(to_f32(orow[c]), D, first ? 0.f : nrow[c]);
+    for (int q = 0; q < kAccRows && r0 + q < rows; ++q) {
+      const int64_t r = r0 + q;
+      const float D = den[r] * tg;
+      const T* orow = o + r * dv;
+      float* nrow = num_acc + r * dv;
+      if (VEC) {
+        for (int c = 4 * lane; c < dv; c += 128) {
+          const float4 x = ld4(orow + c);
+          float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(nrow + c);
+          st4(nrow + c, make_float4(fmaf(x.x, D, a.x), fmaf(x.y, D, a.y), fmaf(x.z, D, a.z), fmaf(x.w, D, a.w)));
+        }
+      } else {
+        for (int c = lane; c < dv; c += 32) nrow[c] = fmaf(to_f32(orow[c]), D, first ? 0.f : nrow[c]);
+      }
+    }
   }
-  if (lane == 0) d_acc[r] = first ? D : d_acc[r] + D;
+  if (lane < kAccRows && r0 + lane < rows) {
+    const int64_t r = r0 + lane;
+    const float D = den[r] * tg;
+    d_acc[r] = first ? D : d_acc[r] + D;
+  }
 }
 
 // o = num / D (zero when the averaged den is degenerate, ra/forward.py:157-163), den = D / T
 template <typename T, bool VEC>
 __global__ void k_group_fwd_out(int64_t rows, int dv, const float* __restrict__ num_acc,
                                 const float* __restrict__ d_acc, float T_, T* __restrict__ o, float* __restrict__ den) {
-  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kAccRows;
   const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float D = d_acc[r];
-  const bool live = D / T_ > race::kDegenerateDenEps;
-  const float rD = live ? 1.f / D : 0.f;
-  const float* nrow = num_acc + r * dv;
-  T* orow = o + r * dv;
-  if (VEC) {
-    for (int c = 4 * lane; c < dv; c += 128) {
-      const float4 a = ld4(nrow + c);
-      st4(orow + c, make_float4(a.x * rD, a.y * rD, a.z * rD, a.w * rD));
+  if (r0 >= rows) return;
+  if (VEC && dv <= 128) {
+    const int c = 4 * lane;
+    float4 a[kAccRows];
+    float rD[kAccRows];
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      const float D = r < rows ? d_acc[r] : 0.f;
+      rD[q] = D / T_ > race::kDegenerateDenEps ? 1.f / D : 0.f;
+      a[q] = (r < rows && c < dv) ? ld4(num_acc + r * dv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      if (r < rows && c < dv)
+        st4(o + r * dv + c, make_float4(a[q].x * rD[q], a[q].y * rD[q], a[q].z * rD[q], a[q].w * rD[q]));
     }
   } else {
-    for (int c = lane; c < dv; c += 32) orow[c] = from_f32<T>(live ? nrow[c] / D : 0.f);
+    for (int q = 0; q < kAccRows && r0 + q < rows; ++q) {
+      const int64_t r = r0 + q;
+      const float D = d_acc[r];
+      const bool live = D / T_ > race::kDegenerateDenEps;
+      const float rD = live ? 1.f / D : 0.f;
+      const float* nrow = num_acc + r * dv;
+      T* orow = o + r * dv;
+      if (VEC) {
+        for (int c = 4 * lane; c < dv; c += 128) {
+          const float4 a = ld4(nrow + c);
+          st4(orow + c, make_float4(a.x * rD, a.y * rD, a.z * rD, a.w * rD));
+        }
+      } else {
+        for (int c = lane; c < dv; c += 32) orow[c] = from_f32<T>(live ? nrow[c] / D : 0.f);
+      }
+    }
   }
-  if (lane == 0) den[r] = D / T_;
+  if (lane < kAccRows && r0 + lane < rows) den[r0 + lane] = d_acc[r0 + lane] / T_;
 }
 
 // rden = 1 / D, gden = -(dO . O) / D of the whole estimator; one warp per row
@@ -402,26 +450,54 @@ template <typename T>
 __global__ void k_group_rg(int64_t BH, int64_t N, int dv, const float* __restrict__ num_acc,
                            const float* __restrict__ d_acc, const T* __restrict__ d_o, float T_,
                            float* __restrict__ rden, float* __restrict__ gden, int vec) {
-  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t rows = BH * N;
+  const int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kAccRows;
   const int lane = threadIdx.x & 31;
-  if (r >= BH * N) return;
-  const float D = d_acc[r];
-  const bool live = D / T_ > race::kDegenerateDenEps;
-  const float rD = live ? 1.f / D : 0.f;
-  float dot = 0.f;
-  if (vec) {  // 4 columns per lane (16-byte fp32 / 8-byte bf16 loads; the host checked the alignment)
-    for (int c = 4 * lane; c < dv; c += 128) {
-      const float4 g = ld4(d_o + r * dv + c), n = ld4(num_acc + r * dv + c);
-      dot = fmaf(g.x, n.x * rD, fmaf(g.y, n.y * rD, fmaf(g.z, n.z * rD, fmaf(g.w, n.w * rD, dot))));
-    }
-  } else {
-    for (int c = lane; c < dv; c += 32) dot = fmaf(to_f32(d_o[r * dv + c]), num_acc[r * dv + c] * rD, dot);
+  if (r0 >= rows) return;
+  float rD[kAccRows], dot[kAccRows];
+#pragma unroll
+  for (int q = 0; q < kAccRows; ++q) {
+    const int64_t r = r0 + q;
+    const float D = r < rows ? d_acc[r] : 0.f;
+    rD[q] = D / T_ > race::kDegenerateDenEps ? 1.f / D : 0.f;
+    dot[q] = 0.f;
   }
-  dot = race::warp_sum(dot);
+  if (vec && dv <= 128) {  // 4 columns per lane (16-byte fp32 / 8-byte bf16 loads; the host checked the alignment)
+    const int c = 4 * lane;
+    float4 g[kAccRows], n[kAccRows];
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      const bool ok = r < rows && c < dv;
+      g[q] = ok ? ld4(d_o + r * dv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      n[q] = ok ? ld4(num_acc + r * dv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q)
+      dot[q] = fmaf(g[q].x, n[q].x * rD[q],
+                    fmaf(g[q].y, n[q].y * rD[q], fmaf(g[q].z, n[q].z * rD[q], g[q].w * (n[q].w * rD[q]))));
+  } else {
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      if (r < rows)
+        for (int c = lane; c < dv; c += 32) dot[q] = fmaf(to_f32(d_o[r * dv + c]), num_acc[r * dv + c] * rD[q], dot[q]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
   if (lane == 0) {
-    const int64_t i = (r / N) * ((N + 3) & ~int64_t(3)) + r % N;
-    rden[i] = rD;
-    gden[i] = -dot * rD;
+#pragma unroll
+    for (int q = 0; q < kAccRows; ++q) {
+      const int64_t r = r0 + q;
+      if (r < rows) {
+        const int64_t i = (r / N) * ((N + 3) & ~int64_t(3)) + r % N;
+        rden[i] = rD[q];
+        gden[i] = -dot[q] * rD[q];
+      }
+    }
   }
 }
 
@@ -452,17 +528,18 @@ __global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int mode, f
 // dx from the summed per-row dproj of all groups (grouped tcgen05 backward): dx^ = sum_j dproj_j w_j over
 // every hyperplane, then the sphere-tangent VJP dx = (dx^ - (dx^.x^) x^) / ||x|| of ra/core.py:126-139
 // (zero-norm rows and unnormalised inputs pass dx^ through).  One warp per row; the hyperplanes of every
-// head sit in shared memory, the row's dproj in lane registers (broadcast by shuffles), and a lane's
-// columns c = lane + 32 i in registers, so each operand is read once.
+// head sit in shared memory (each chunk read once per kDxRows rows of one sequence), the rows' dproj in
+// lane registers (broadcast by shuffles), and a lane's columns c = lane + 32 i in registers.  FULL: d is
+// exactly 128 NCH (no per-lane column guards in the inner loop).
 constexpr int kDxRows = 4;  // rows per warp iteration (independent chains: latency hiding)
 // NCH = 4-column chunks per lane (d <= 128 * NCH); 32-bit shared-memory indexing throughout
-template <typename T, int NCH>
-__global__ void __launch_bounds__(256, 4) k_dx_from_dproj(int64_t rows, int64_t N, int d, int tp,
+template <typename T, int NCH, bool FULL>
+__global__ void __launch_bounds__(256, 3) k_dx_from_dproj(int64_t rows, int64_t N, int d, int tp,
                                                        const T* __restrict__ x, const float* __restrict__ dproj,
                                                        const float* __restrict__ w, int nheads_w, int H,
                                                        int normalize, T* __restrict__ dx) {
   extern __shared__ float4 wsm4[];  // [nheads_w, tp, d / 4] float4
-  const int d4 = d / 4;
+  const int d4 = FULL ? 32 * NCH : d / 4;
   const int hstride = tp * d4;
   {
     const float4* w4 = reinterpret_cast<const float4*>(w);
@@ -474,43 +551,62 @@ __global__ void __launch_bounds__(256, 4) k_dx_from_dproj(int64_t rows, int64_t 
   const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const int64_t nquads = (rows + kDxRows - 1) / kDxRows;
   for (int64_t qd = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; qd < nquads; qd += nwarps) {
+    const int64_t r0 = qd * kDxRows;
+    const int nr = int(rows - r0 < kDxRows ? rows - r0 : kDxRows);  // rows of this quad (warp-uniform)
+    // sequence of the quad's first row (32-bit division when the sizes allow it: the common case)
+    const int64_t bh0 = (rows < (int64_t(1) << 31)) ? int64_t(uint32_t(r0) / uint32_t(N)) : r0 / N;
+    const bool one_seq = (r0 - bh0 * N) + nr <= N;  // all rows in one sequence: one W block
     float4 xv[kDxRows][NCH], acc[kDxRows][NCH];
     float mine[kDxRows];
-    int woff[kDxRows];
-    // head of the quad's first row: one division per quad; rows crossing into the next sequence step it
-    int64_t bh = (qd * kDxRows) / N, bh_end = (bh + 1) * N;
-    int head = nheads_w > 1 ? int(bh % H) : 0;
 #pragma unroll
-    for (int q = 0; q < kDxRows; ++q) {  // every load of the four rows first
-      const int64_t r = qd * kDxRows + q;
-      const bool ok = r < rows;
-      const int64_t rr = ok ? r : rows - 1;
-      while (rr >= bh_end) {
-        bh_end += N;
-        if (++head == H) head = 0;
-      }
-      woff[q] = (nheads_w > 1 ? head * hstride : 0) + lane;
-      mine[q] = (ok && lane < tp) ? dproj[rr * tp + lane] : 0.f;
+    for (int q = 0; q < kDxRows; ++q) {  // every load of the quad first
+      const int64_t rr = r0 + (q < nr ? q : 0);
+      mine[q] = (q < nr && lane < tp) ? dproj[rr * tp + lane] : 0.f;
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
         const int c4 = lane + 32 * i;
-        xv[q][i] = (ok && c4 < d4) ? ld4(x + rr * d + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        xv[q][i] = (q < nr && (FULL || c4 < d4)) ? ld4(x + rr * d + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
         acc[q][i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-    for (int j = 0; j < tp; ++j) {  // tp <= 32 (checked by the caller)
+    // dx^ = sum_j dproj_j w_j: dproj_j broadcast by shuffles, each W chunk read once for the quad's rows
+    if (one_seq || nheads_w == 1) {
+      const int wbase = (nheads_w > 1 ? int(uint32_t(bh0) % uint32_t(H)) * hstride : 0) + lane;
+      for (int j = 0; j < tp; ++j) {  // tp <= 32 (checked by the caller)
+        float pj[kDxRows];
 #pragma unroll
-      for (int q = 0; q < kDxRows; ++q) {
-        const float pj = __shfl_sync(0xffffffffu, mine[q], j);
-        const int base = woff[q] + j * d4;
+        for (int q = 0; q < kDxRows; ++q) pj[q] = __shfl_sync(0xffffffffu, mine[q], j);
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
-          if (lane + 32 * i < d4) {
-            const float4 wv = wsm4[base + 32 * i];
-            acc[q][i].x = fmaf(pj, wv.x, acc[q][i].x);
-            acc[q][i].y = fmaf(pj, wv.y, acc[q][i].y);
-            acc[q][i].z = fmaf(pj, wv.z, acc[q][i].z);
-            acc[q][i].w = fmaf(pj, wv.w, acc[q][i].w);
+          if (FULL || lane + 32 * i < d4) {
+            const float4 wv = wsm4[wbase + j * d4 + 32 * i];
+#pragma unroll
+            for (int q = 0; q < kDxRows; ++q) {
+              acc[q][i].x = fmaf(pj[q], wv.x, acc[q][i].x);
+              acc[q][i].y = fmaf(pj[q], wv.y, acc[q][i].y);
+              acc[q][i].z = fmaf(pj[q], wv.z, acc[q][i].z);
+              acc[q][i].w = fmaf(pj[q], wv.w, acc[q][i].w);
+            }
+          }
+        }
+      }
+    } else {  // the quad straddles two sequences (rare): W block per row
+      int wb[kDxRows];
+#pragma unroll
+      for (int q = 0; q < kDxRows; ++q) wb[q] = int(((r0 + (q < nr ? q : 0)) / N) % H) * hstride + lane;
+      for (int j = 0; j < tp; ++j) {
+#pragma unroll
+        for (int q = 0; q < kDxRows; ++q) {
+          const float pj = __shfl_sync(0xffffffffu, mine[q], j);
+#pragma unroll
+          for (int i = 0; i < NCH; ++i) {
+            if (FULL || lane + 32 * i < d4) {
+              const float4 wv = wsm4[wb[q] + j * d4 + 32 * i];
+              acc[q][i].x = fmaf(pj, wv.x, acc[q][i].x);
+              acc[q][i].y = fmaf(pj, wv.y, acc[q][i].y);
+              acc[q][i].z = fmaf(pj, wv.z, acc[q][i].z);
+              acc[q][i].w = fmaf(pj, wv.w, acc[q][i].w);
+            }
           }
         }
       }
@@ -536,16 +632,15 @@ __global__ void __launch_bounds__(256, 4) k_dx_from_dproj(int64_t rows, int64_t 
       }
 #pragma unroll
     for (int q = 0; q < kDxRows; ++q) {
-      const int64_t r = qd * kDxRows + q;
-      if (r < rows) {
-        const float nrm = sqrtf(ss[q]);
-        const bool tang = normalize && nrm >= race::kZeroRowEps;
-        const float inv = tang ? 1.f / nrm : 1.f;
+      if (q < nr) {
+        const int64_t r = r0 + q;
+        const bool tang = normalize && ss[q] >= race::kZeroRowEps * race::kZeroRowEps;  // ||x|| >= eps
+        const float inv = tang ? rsqrtf(ss[q]) : 1.f;
         const float dt = tang ? dot[q] * inv : 0.f;  // dx^ . x^
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
           const int c4 = lane + 32 * i;
-          if (c4 < d4) {
+          if (FULL || c4 < d4) {
             float4 o = acc[q][i];
             if (tang)
               o = make_float4((o.x - dt * xv[q][i].x * inv) * inv, (o.y - dt * xv[q][i].y * inv) * inv,
@@ -885,10 +980,10 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
       if (g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0)
-        k_group_fwd_acc<T, true><<<blocks_for(rows * 32), 256, 0, st>>>(
+        k_group_fwd_acc<T, true><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
             rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       else
-        k_group_fwd_acc<T, false><<<blocks_for(rows * 32), 256, 0, st>>>(
+        k_group_fwd_acc<T, false><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
             rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       race::note_launch();
       return cudaGetLastError();
@@ -901,10 +996,10 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     const bool vec = g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(T))) == 0 &&
                      (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0;
     if (vec)
-      k_group_fwd_out<T, true><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+      k_group_fwd_out<T, true><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
                                                                             float(g.T), static_cast<T*>(o), den);
     else
-      k_group_fwd_out<T, false><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+      k_group_fwd_out<T, false><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
                                                                              float(g.T), static_cast<T*>(o), den);
     race::note_launch();
     return cudaGetLastError();
@@ -932,7 +1027,7 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     using T = std::remove_pointer_t<decltype(tag)>;
     const int vec = g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(d_o) % 16) == 0 &&
                     (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0;
-    k_group_rg<T><<<blocks_for(rows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
+    k_group_rg<T><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
                                                                 static_cast<const T*>(d_o), float(g.T), ws.rden,
                                                                 ws.gden,
                                                                 vec);
@@ -1033,7 +1128,9 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     using T = std::remove_pointer_t<decltype(tag)>;
     const int nheads_w = g.w_per_head ? int(g.H) : 1;
     const size_t smem = sizeof(float) * size_t(nheads_w) * tp_all * g.d;
-    auto kern = g.d <= 128 ? k_dx_from_dproj<T, 1> : k_dx_from_dproj<T, 2>;
+    auto kern = g.d == 128 ? k_dx_from_dproj<T, 1, true>
+                : g.d <= 128 ? k_dx_from_dproj<T, 1, false>
+                : g.d == 256 ? k_dx_from_dproj<T, 2, true> : k_dx_from_dproj<T, 2, false>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (err != cudaSuccess) return err;
     const unsigned grid = unsigned(std::min<int64_t>(blocks_for((rows + kDxRows - 1) / kDxRows * 32), 148 * 8));
