@@ -983,13 +983,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(c3, par);
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
       tc_fence_after();
-      float zz[32], zv[16];
-      tmem_ld32(tmem + lb + TM_Z, zz);
+      float zhi[8], zlo[8], zv[16];  // Z columns 8..15 / 24..31: the duplicate hi copy and padding (not read)
+      tmem_ld8(tmem + lb + TM_Z, zhi);
+      tmem_ld8(tmem + lb + TM_Z + 16, zlo);
       tmem_ld16(tmem + lb + TM_ZV, zv);
       tmem_ld_wait();
       float dphi[FP];
 #pragma unroll
-      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zz[f] + zz[16 + f];
+      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zhi[f] + zlo[f];
       float dproj[8];
       row_feature_vjp<P, HB>(a, uk, phk, dphi, dproj);
       if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
@@ -1006,12 +1007,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(cdv, par);
       tc_fence_after();
       if (h == 1) {
-        float dsa[32];
-        tmem_ld32(tmem + lb + TM_DS, dsa);
+        float dhi[8], dlo[8];
+        tmem_ld8(tmem + lb + TM_DS, dhi);
+        tmem_ld8(tmem + lb + TM_DS + 16, dlo);
         tmem_ld_wait();
         float dsn[FP];
 #pragma unroll
-        for (int f = 0; f < FP; ++f) dsn[f] = dsa[f] + dsa[16 + f];
+        for (int f = 0; f < FP; ++f) dsn[f] = dhi[f] + dlo[f];
         write_sopT(sb + OFF_DSOPT, r, dsn);
         write_sop(sb + OFF_DSOP, r, dsn);
       }
