@@ -146,6 +146,39 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k,
              const float* state, void* dq, void* dk, void* dv,
              void* workspace, void* stream);
 
+/* ---- strided operands ------------------------------------------------ */
+
+/* Element strides of one [B, H, N, width] operand whose rows (width
+ * elements) are contiguous: token, head and batch strides.  token == 0
+ * means the default contiguous [B*H, N, width] layout.  Example: the q of
+ * a fused projection qkv[B, N, 3, H, d] has token = 3*H*d, head = d,
+ * batch = N*3*H*d; an O written as [B, N, H, dv] has token = H*dv.       */
+typedef struct {
+  int64_t token, head, batch;
+} race_stride_t;
+
+typedef struct {
+  race_stride_t q, k, v, o, d_o, dq, dk, dv;
+} race_layout_t;
+
+/* race_fwd / race_bwd on strided operands (layout may be NULL: contiguous).
+ * Strides are multiples of 8 elements.  Strided operands run on the
+ * one-pass tcgen05 path only (bf16, d and dv <= 128 and multiples of 8,
+ * F <= 8), which reads and writes them in place through 4-D TMA maps --
+ * no transposed copies; otherwise RACE_EUNSUPPORTED.  No in-place
+ * backward with a layout.  Sizes, workspace and state are those of the
+ * same desc.  (No reference counterpart: the reference takes one 2-D
+ * matrix per head, ra/bench.py:172-178.)                                  */
+int race_fwd_layout(const race_desc_t* desc, const race_layout_t* layout,
+                    const void* q, const void* k, const void* v,
+                    const float* w, void* o, float* den, float* state,
+                    void* workspace, void* stream);
+int race_bwd_layout(const race_desc_t* desc, const race_layout_t* layout,
+                    const void* q, const void* k, const void* v,
+                    const float* w, const void* d_o, const float* state,
+                    void* dq, void* dk, void* dv, void* workspace,
+                    void* stream);
+
 /* ---- split-phase entry points (sequence sharding across GPUs) --------- */
 
 /* Key-side aggregation per segment: part[bh][s] = phi(K_s)^T [V_s | 1]

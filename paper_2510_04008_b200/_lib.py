@@ -28,6 +28,7 @@ EXPORTS = (
     "race_kside_partials", "race_combine", "race_fwd_readout", "race_fwd_causal",
     "race_bwd_qside", "race_bwd_kside", "race_bwd_causal_q", "race_bwd_causal_k",
     "race_kside_partials_rows", "race_fwd_causal_krows", "race_group_plan",
+    "race_fwd_layout", "race_bwd_layout",
 )
 
 
@@ -50,6 +51,18 @@ class RaceDesc(ctypes.Structure):
         ("w_per_head", ctypes.c_int32),
         ("reserved", ctypes.c_int32 * 4),
     ]
+
+
+class RaceStride(ctypes.Structure):
+    """Mirror of ``race_stride_t``: element strides (token, head, batch); token 0 = contiguous."""
+
+    _fields_ = [("token", ctypes.c_int64), ("head", ctypes.c_int64), ("batch", ctypes.c_int64)]
+
+
+class RaceLayout(ctypes.Structure):
+    """Mirror of ``race_layout_t``."""
+
+    _fields_ = [(n, RaceStride) for n in ("q", "k", "v", "o", "d_o", "dq", "dk", "dv")]
 
 
 class RaceError(RuntimeError):
@@ -85,6 +98,8 @@ _SIGS = {
     "race_bwd_causal_k": ([_P] * 14, ctypes.c_int),
     "race_kside_partials_rows": ([_P] * 8, ctypes.c_int),
     "race_fwd_causal_krows": ([_P] * 11, ctypes.c_int),
+    "race_fwd_layout": ([_P] * 11, ctypes.c_int),
+    "race_bwd_layout": ([_P] * 13, ctypes.c_int),
 }
 _I32, _I64, _F64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 # include/race_aux.h (validation-side GPU functions; float64 compute)

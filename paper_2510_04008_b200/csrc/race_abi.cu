@@ -84,6 +84,10 @@ const int64_t kSegTargetSimt = [] {
   return e && e[0] ? int64_t(atoll(e)) : int64_t(148) * 2 * 7;
 }();
 
+// operand strides of the race_fwd_layout / race_bwd_layout call in progress on this thread (every entry
+// point it calls resolves its Geo through resolve_shape, which copies them in)
+thread_local const race_layout_t* t_layout = nullptr;
+
 int resolve_shape(const race_desc_t* d, race::Geo* g) {
   if (!d) return fail(RACE_EBADSHAPE, "null descriptor");
   if (d->abi_version != RACE_ABI_VERSION)
@@ -124,6 +128,11 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   g->seg_tokens = per;
   g->nseg = g->N > 0 ? (g->N + per - 1) / per : 1;
   if (g->nseg > 0x7fffffff) return fail(RACE_EUNSUPPORTED, "too many segments");
+  if (t_layout) {
+    const race_stride_t* src[race::L_COUNT] = {&t_layout->q,  &t_layout->k,  &t_layout->v,  &t_layout->o,
+                                               &t_layout->d_o, &t_layout->dq, &t_layout->dk, &t_layout->dv};
+    for (int i = 0; i < race::L_COUNT; ++i) g->lay[i] = race::Lay{src[i]->token, src[i]->head, src[i]->batch};
+  }
   return RACE_OK;
 }
 
@@ -932,6 +941,56 @@ int race_bwd(const race_desc_t* desc, const void* q, const void* k, const void* 
   if (!dq_later) return RACE_OK;
   const size_t n = size_t(g.BH * g.N) * g.d * (g.dtype == RACE_BF16 ? 2 : 4);
   return cuda_status(cudaMemcpyAsync(dq, ws.dqtmp, n, cudaMemcpyDeviceToDevice, S(stream)), "dq copy");
+}
+
+// strided operands: the tcgen05 path reads and writes them through 4-D TMA maps; everything else
+// (CUDA-core kernels, grouped sketches, split-phase calls) takes the contiguous layout
+static int check_layout(const race_desc_t* desc, const race_layout_t* lay, race::Geo* g) {
+  const race_layout_t* saved = t_layout;
+  t_layout = nullptr;
+  GroupPlan gp;
+  int rc = group_plan(desc, g, &gp);
+  t_layout = saved;
+  if (rc) return rc;
+  const race_stride_t* all[race::L_COUNT] = {&lay->q, &lay->k, &lay->v, &lay->o, &lay->d_o, &lay->dq, &lay->dk, &lay->dv};
+  bool any = false;
+  for (const race_stride_t* s : all) {
+    if (!s->token) continue;
+    any = true;
+    if (s->token < 0 || s->head < 0 || s->batch < 0 || s->token % 8 || s->head % 8 || s->batch % 8)
+      return fail(RACE_EBADSHAPE, "operand strides must be non-negative multiples of 8 elements (16 bytes)");
+  }
+  if (any && (gp.grouped(*g) || !race::tc_supported(*g)))
+    return fail(RACE_EUNSUPPORTED, "strided operands need the one-pass tcgen05 path (bf16, d and dv <= 128 "
+                                   "multiples of 8, F <= 8); pass contiguous [B*H, N, d] tensors otherwise");
+  return RACE_OK;
+}
+
+struct LayoutScope {  // the layout is visible to every entry point the call runs, and only to them
+  explicit LayoutScope(const race_layout_t* l) { t_layout = l; }
+  ~LayoutScope() { t_layout = nullptr; }
+};
+
+int race_fwd_layout(const race_desc_t* desc, const race_layout_t* layout, const void* q, const void* k, const void* v,
+                    const float* w, void* o, float* den, float* state, void* workspace, void* stream) {
+  if (layout) {
+    race::Geo g;
+    if (int rc = check_layout(desc, layout, &g)) return rc;
+  }
+  LayoutScope scope(layout);
+  return race_fwd(desc, q, k, v, w, o, den, state, workspace, stream);
+}
+
+int race_bwd_layout(const race_desc_t* desc, const race_layout_t* layout, const void* q, const void* k, const void* v,
+                    const float* w, const void* d_o, const float* state, void* dq, void* dk, void* dv,
+                    void* workspace, void* stream) {
+  if (layout) {
+    race::Geo g;
+    if (int rc = check_layout(desc, layout, &g)) return rc;
+    if (dq == q || dk == k || dv == v) return fail(RACE_EUNSUPPORTED, "in-place backward needs contiguous operands");
+  }
+  LayoutScope scope(layout);
+  return race_bwd(desc, q, k, v, w, d_o, state, dq, dk, dv, workspace, stream);
 }
 
 }  // extern "C"

@@ -7,6 +7,13 @@
 
 namespace race {
 
+// Element strides of one [B, H, N, width] operand (row elements contiguous): token, head, batch.
+// token == 0 means the contiguous [B*H, N, width] layout.
+struct Lay {
+  int64_t token = 0, head = 0, batch = 0;
+};
+enum LayIdx { L_Q = 0, L_K, L_V, L_O, L_DO, L_DQ, L_DK, L_DV, L_COUNT };
+
 // Resolved problem geometry (validated copy of race_desc_t + segmentation).
 struct Geo {
   int64_t BH, H, N;
@@ -30,6 +37,13 @@ struct Geo {
   float* dproj_q = nullptr;
   float* dproj_k = nullptr;
   int dproj_ld = 0, dproj_col = 0, dproj_acc = 0;
+  // strided operands (race_fwd_layout / race_bwd_layout, tcgen05 path only): e.g. [B, N, H, d] views
+  Lay lay[L_COUNT];
+  bool strided() const {
+    for (const Lay& l : lay)
+      if (l.token) return true;
+    return false;
+  }
 };
 
 // corners per table a kernel pass sees

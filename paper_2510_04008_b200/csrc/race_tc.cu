@@ -61,7 +61,7 @@ static_assert(SMEM <= 232448, "k_aggregate2 shared memory");
 constexpr uint32_t TM_PK = 0, TM_ACC = 32;  // accumulators at 32 and 64
 }  // namespace agg2
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_aggregate2(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   using namespace agg2;
@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
         uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
         for (int h = 0; h < 2; ++h) {
-          tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
-          tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
         }
       }
     }
@@ -288,7 +288,7 @@ static_assert(SMEM <= 232448, "k_readout8 shared memory");
 constexpr uint32_t TM_NUM_R = 128;
 }  // namespace rdo8
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_readout8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
   using namespace rdo8;
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const int s = j % STAGES;
         mbar_wait(&ostaged[s], (j / STAGES) & 1);
         for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + h * SUB), h * 64, ot[s], ob[s]);
+          tile_store<M4>(a, &tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + h * SUB), h * 64, ot[s], ob[s]);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
         uint8_t* st = smem + OFF_STAGE + s * STAGE_BYTES;
-        for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+        for (int h = 0; h < 2; ++h) tile_load<M4>(a, st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
         ot[s] = cur.t;
         ob[s] = cur.m.bh;
       }
@@ -549,7 +549,7 @@ static_assert(SMEM <= 232448, "k_causal_fwd8 shared memory");
 
 // KR: the k halves of the sketch rows were written by the key-side aggregation (k_aggregate2),
 // so this pass reads Q, V and those rows instead of K (no K tile, no K projection).
-template <int P, bool KR, int HB = 0>
+template <int P, bool KR, int HB = 0, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_causal_fwd8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(&ostaged[s], (j >> 1) & 1);
         const int ot = int(s ? ot1 : ot0), ob = int(s ? ob1 : ob0);
         for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE + h * SUB),
+          tile_store<M4>(a, &tmO, reinterpret_cast<void*>(smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE + h * SUB),
                        h * 64, ot, ob);
         tma_store_commit();
       };
@@ -624,22 +624,22 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           const int tp = int(cur.t) + a.pf * CH;
           if (tp < a.N)
             for (int h = 0; h < 2; ++h) {
-              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmQ, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmK, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmV, h * 64, tp, int(cur.m.bh));
             }
         }
         mbar_wait(&emptyqk[s], ((gc >> 1) & 1) ^ 1);
         RACE_TRACE(a, 0, gc);
         if (KR) {  // Q tile + the chunk's sketch rows (in the unused K slot)
           mbar_arrive_expect_tx(&fullqk[s], TILE + CH * ROWW * 4);
-          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+          for (int h = 0; h < 2; ++h) tile_load<M4>(a, st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
           tma_load_2d(st + TILE, &tmROWS, &fullqk[s], 0, int(cur.m.bh) * int(a.N) + int(cur.t), pol);
         } else {
           mbar_arrive_expect_tx(&fullqk[s], 2 * TILE);
           for (int h = 0; h < 2; ++h) {
-            tma_load_3d(st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
-            tma_load_3d(st + TILE + h * SUB, &tmK, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+            tile_load<M4>(a, st + h * SUB, &tmQ, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+            tile_load<M4>(a, st + TILE + h * SUB, &tmK, &fullqk[s], h * 64, int(cur.t), int(cur.m.bh), pol);
           }
         }
         if (gc >= 2) {
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         RACE_TRACE(a, 9, gc);
         mbar_arrive_expect_tx(&fullv[s], TILE);
         for (int h = 0; h < 2; ++h)
-          tma_load_3d(st + 2 * TILE + h * SUB, &tmV, &fullv[s], h * 64, int(cur.t), int(cur.m.bh), pol);
+          tile_load<M4>(a, st + 2 * TILE + h * SUB, &tmV, &fullv[s], h * 64, int(cur.t), int(cur.m.bh), pol);
         if (s) { ot1 = cur.t; ob1 = cur.m.bh; } else { ot0 = cur.t; ob0 = cur.m.bh; }
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_o(j);
@@ -950,7 +950,7 @@ constexpr int OFF_BAR = OFF_W + WOP;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace prj
 
-template <int P, int HB = 0>
+template <int P, int HB = 0, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_project(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, Args a) {
   using namespace prj;
@@ -993,8 +993,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
         uint8_t* st = smem + s * STAGE_BYTES;
         for (int h = 0; h < 2; ++h) {
-          tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
-          tma_load_3d(st + TILE + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + TILE + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
         }
       }
     }
@@ -1112,11 +1112,16 @@ cudaError_t tc_aggregate(const Geo& g, const void* k, const void* v, const float
                          cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv;
-  if (!make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv)) return cudaErrorInvalidValue;
+  if (!make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tout = part;
   a.rows_out = rows;
+  if (g.strided()) switch (pass_corner_bits(g)) {  // one-pass problems only (race_fwd_layout checks)
+      case 1: return launch_nt(k_aggregate2<1, 0, true>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      case 2: return launch_nt(k_aggregate2<2, 0, true>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+      default: return launch_nt(k_aggregate2<3, 0, true>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
+    }
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_aggregate2<1>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
     case 2: return launch_nt(k_aggregate2<2>, NTHREADS8, agg2::SMEM, grid_for(g), st, mk, mv, a);
@@ -1130,11 +1135,16 @@ cudaError_t tc_readout(const Geo& g, const void* q, const float* w, const float*
                        cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mo;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mo, o, g, g.dv)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mo, o, g, g.dv, L_O)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tin = tab;
   a.den = den;
+  if (g.strided()) switch (pass_corner_bits(g)) {
+      case 1: return launch_nt(k_readout8<1, 0, true>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+      case 2: return launch_nt(k_readout8<2, 0, true>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+      default: return launch_nt(k_readout8<3, 0, true>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
+    }
   switch (pass_corner_bits(g)) {
     case 1: return launch_nt(k_readout8<1>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
     case 2: return launch_nt(k_readout8<2>, NTHREADS8, rdo8::SMEM, grid_for(g), st, mq, mo, a);
@@ -1148,10 +1158,15 @@ cudaError_t tc_project(const Geo& g, const void* q, const void* k, const float* 
   using namespace tcfast;
   if (g.BH * g.N == 0) return cudaSuccess;
   CUtensorMap mq, mk;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.rows_out = rows;
+  if (g.strided()) switch (pass_corner_bits(g)) {
+      case 1: return launch(k_project<1, 0, true>, prj::SMEM, grid_for(g), st, mq, mk, a);
+      case 2: return launch(k_project<2, 0, true>, prj::SMEM, grid_for(g), st, mq, mk, a);
+      default: return launch(k_project<3, 0, true>, prj::SMEM, grid_for(g), st, mq, mk, a);
+    }
   switch (pass_corner_bits(g)) {
     case 1: return launch(k_project<1>, prj::SMEM, grid_for(g), st, mq, mk, a);
     case 2: return launch(k_project<2>, prj::SMEM, grid_for(g), st, mq, mk, a);
@@ -1166,7 +1181,7 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
                           const float* car, void* o, float* den, float* nrm, bool krows, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mo, mr;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mo, o, g, g.dv))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mo, o, g, g.dv, L_O))
     return cudaErrorInvalidValue;
   if (krows && (!nrm || !make_map_rows(&mr, nrm, g.BH * g.N))) return cudaErrorInvalidValue;
   if (!krows) mr = mq;  // unused
@@ -1177,14 +1192,15 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
   a.rows_out = nrm;
   a.dbg = trace_for("fwd");
   switch (pass_corner_bits(g)) {
-#define RACE_FWD8(PP, HB)                                                                                     \
-  return krows ? launch_nt(k_causal_fwd8<PP, true, HB>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
-               : launch_nt(k_causal_fwd8<PP, false, HB>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)
-    case 1: RACE_FWD8(1, 0);
-    case 2: RACE_FWD8(2, 0);
+#define RACE_FWD8(PP, HB, M4)                                                                                     \
+  return krows ? launch_nt(k_causal_fwd8<PP, true, HB, M4>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a) \
+               : launch_nt(k_causal_fwd8<PP, false, HB, M4>, NTHREADS8, cfw8::SMEM, grid_for(g), st, mq, mk, mv, mo, mr, a)
+    case 1: if (g.strided()) RACE_FWD8(1, 0, true); RACE_FWD8(1, 0, false);
+    case 2: if (g.strided()) RACE_FWD8(2, 0, true); RACE_FWD8(2, 0, false);
     default:
-      if (g.cb) RACE_FWD8(3, 2);
-      RACE_FWD8(3, 0);
+      if (g.strided()) RACE_FWD8(3, 0, true);
+      if (g.cb) RACE_FWD8(3, 2, false);
+      RACE_FWD8(3, 0, false);
 #undef RACE_FWD8
   }
 }

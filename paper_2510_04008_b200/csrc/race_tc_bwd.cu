@@ -75,7 +75,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;  // DS: two accumulators at 32 and 64
 }  // namespace bq8n
 
-template <int P, int HB = 0, bool GRP = false>
+template <int P, int HB = 0, bool GRP = false, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
              const __grid_constant__ CUtensorMap tmDQ, Args a) {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(&dqstaged[s], (j >> 1) & 1);
         if (!a.dproj_out)  // grouped backward: dq is formed from the summed dproj afterwards
           for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, qt[s], qb[s]);
+            tile_store<M4>(a, &tmDQ, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, qt[s], qb[s]);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
         uint8_t* st = smem + s * STAGE_BYTES;
         for (int h = 0; h < 2; ++h) {
-          tma_load_3d(st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
-          tma_load_3d(st + TILE + h * SUB, &tmDO, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + h * SUB, &tmQ, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + TILE + h * SUB, &tmDO, &full[s], h * 64, cur.t, cur.m.bh, pol);
         }
         qt[s] = cur.t;
         qb[s] = cur.m.bh;
@@ -341,7 +341,7 @@ using bk::TM_DV;
 using bk::TM_DX;
 }  // namespace bk8n
 
-template <int P, int HB = 0, bool GRP = false>
+template <int P, int HB = 0, bool GRP = false, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_k8(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
              const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, Args a) {
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(&staged[s], (j >> 1) & 1);
         for (int h = 0; h < 2; ++h) {
           if (!a.dproj_out)  // grouped backward: dk is formed from the summed dproj afterwards
-            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, kt[s], kb[s]);
-          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + s * STAGE_BYTES + TILE + h * SUB), h * 64, kt[s], kb[s]);
+            tile_store<M4>(a, &tmDK, reinterpret_cast<void*>(smem + s * STAGE_BYTES + h * SUB), h * 64, kt[s], kb[s]);
+          tile_store<M4>(a, &tmDV, reinterpret_cast<void*>(smem + s * STAGE_BYTES + TILE + h * SUB), h * 64, kt[s], kb[s]);
         }
         tma_store_commit();
       };
@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
         uint8_t* st = smem + s * STAGE_BYTES;
         for (int h = 0; h < 2; ++h) {
-          tma_load_3d(st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
-          tma_load_3d(st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + h * SUB, &tmK, &full[s], h * 64, cur.t, cur.m.bh, pol);
+          tile_load<M4>(a, st + TILE + h * SUB, &tmV, &full[s], h * 64, cur.t, cur.m.bh, pol);
         }
         kt[s] = cur.t;
         kb[s] = cur.m.bh;
@@ -541,7 +541,7 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
                      float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mdo, mdq;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mdo, d_o, g, g.dv) || !make_map(&mdq, dq, g, g.d)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mdo, d_o, g, g.dv, L_DO) || !make_map(&mdq, dq, g, g.d, L_DQ)) return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tin = tab;
@@ -550,9 +550,10 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
   const bool grp = g.ext_rden || g.dproj_q;  // a pass of a grouped backward (race_abi.cu)
 #define RACE_BQ8(...) return launch_nt(k_bwd_q8<__VA_ARGS__>, NTHREADS8, bq8n::SMEM, grid_for(g), st, mq, mdo, mdq, a)
   switch (pass_corner_bits(g)) {
-    case 1: if (grp) RACE_BQ8(1, 0, true); RACE_BQ8(1);
-    case 2: if (grp) RACE_BQ8(2, 0, true); RACE_BQ8(2);
+    case 1: if (g.strided()) RACE_BQ8(1, 0, false, true); if (grp) RACE_BQ8(1, 0, true); RACE_BQ8(1);
+    case 2: if (g.strided()) RACE_BQ8(2, 0, false, true); if (grp) RACE_BQ8(2, 0, true); RACE_BQ8(2);
     default:
+      if (g.strided()) RACE_BQ8(3, 0, false, true);  // strided operands: one-pass problems only
       if (g.cb) RACE_BQ8(3, 2, true);
       if (grp) RACE_BQ8(3, 0, true);
       RACE_BQ8(3);
@@ -564,7 +565,7 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
                      void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv, mdk, mdv;
-  if (!make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdk, dk, g, g.d) || !make_map(&mdv, dv, g, g.dv))
+  if (!make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdk, dk, g, g.d, L_DK) || !make_map(&mdv, dv, g, g.dv, L_DV))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -574,9 +575,10 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
 #define RACE_BK8(...) \
   return launch_nt(k_bwd_k8<__VA_ARGS__>, NTHREADS8, bk8n::SMEM, grid_for(g), st, mk, mv, mdk, mdv, a)
   switch (pass_corner_bits(g)) {
-    case 1: if (grp) RACE_BK8(1, 0, true); RACE_BK8(1);
-    case 2: if (grp) RACE_BK8(2, 0, true); RACE_BK8(2);
+    case 1: if (g.strided()) RACE_BK8(1, 0, false, true); if (grp) RACE_BK8(1, 0, true); RACE_BK8(1);
+    case 2: if (g.strided()) RACE_BK8(2, 0, false, true); if (grp) RACE_BK8(2, 0, true); RACE_BK8(2);
     default:
+      if (g.strided()) RACE_BK8(3, 0, false, true);  // strided operands: one-pass problems only
       if (g.cb) RACE_BK8(3, 2, true);
       if (grp) RACE_BK8(3, 0, true);
       RACE_BK8(3);

@@ -97,7 +97,7 @@ __device__ __forceinline__ void write_dproj_w(uint32_t buf, int r, const float* 
 }
 }  // namespace cq8
 
-template <int P, int HB = 0, bool GRP = false>
+template <int P, int HB = 0, bool GRP = false, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_q8(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const int qt = int(s ? qt1 : qt0), qb = int(s ? qb1 : qb0);
         if (!a.dproj_out)  // grouped backward: dq is formed from the summed dproj afterwards
           for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDQ, reinterpret_cast<void*>(smem + OFF_Q + s * TILE + h * SUB), h * 64, qt, qb);
+            tile_store<M4>(a, &tmDQ, reinterpret_cast<void*>(smem + OFF_Q + s * TILE + h * SUB), h * 64, qt, qb);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -181,10 +181,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           const int tp = int(cur.t) + a.pf * CH;
           if (tp < a.N)
             for (int h = 0; h < 2; ++h) {
-              tma_prefetch_3d(&tmQ, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmQ, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmK, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmV, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmDO, h * 64, tp, int(cur.m.bh));
             }
         }
         const uint32_t par1 = (gc & 1) ^ 1;          // single buffers: one phase per chunk
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         }
         RACE_TRACE(a, 3, gc);
         mbar_arrive_expect_tx(&fullQ[s], TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_Q + s * TILE + h * SUB, &tmQ, &fullQ[s], h * 64, t, bh, pol);
+        for (int h = 0; h < 2; ++h) tile_load<M4>(a, smem + OFF_Q + s * TILE + h * SUB, &tmQ, &fullQ[s], h * 64, t, bh, pol);
         if (s) { qt1 = t; qb1 = bh; } else { qt0 = t; qb0 = bh; }
         mbar_wait(&emptyT[s], par2);
         mbar_arrive_expect_tx(&fullT[s], TOK_BYTES);
@@ -205,12 +205,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_wait(emptyV, par1);
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(fullV, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
+        for (int h = 0; h < 2; ++h) tile_load<M4>(a, smem + OFF_V + h * SUB, &tmV, fullV, h * 64, t, bh, pol);
         mbar_wait(&emptyO[s], par2);
         RACE_TRACE(a, 2, gc);
         mbar_arrive_expect_tx(&fullO[s], TILE);
         for (int h = 0; h < 2; ++h)
-          tma_load_3d(smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
+          tile_load<M4>(a, smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dq(j);
       tma_store_wait_all<0>();
@@ -589,7 +589,7 @@ struct RCursor {
   }
 };
 
-template <int P, int HB = 0, bool GRP = false>
+template <int P, int HB = 0, bool GRP = false, bool M4 = false>
 __global__ void __launch_bounds__(NTHREADS8, 1)
     k_bwd_causal_k8(const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -668,14 +668,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const int s = j & 1;
         mbar_wait(&dvstaged[s], (j >> 1) & 1);
         for (int h = 0; h < 2; ++h)
-          tma_store_3d(&tmDV, reinterpret_cast<void*>(smem + OFF_V + s * TILE + h * SUB), h * 64, vt[s], vb[s]);
+          tile_store<M4>(a, &tmDV, reinterpret_cast<void*>(smem + OFF_V + s * TILE + h * SUB), h * 64, vt[s], vb[s]);
         tma_store_commit();
       };
       auto store_dk = [&](uint32_t j) {
         mbar_wait(dkstaged, j & 1);
         if (!a.dproj_out)  // grouped backward: dk is formed from the summed dproj afterwards
           for (int h = 0; h < 2; ++h)
-            tma_store_3d(&tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, kt, kb);
+            tile_store<M4>(a, &tmDK, reinterpret_cast<void*>(smem + OFF_K + h * SUB), h * 64, kt, kb);
         tma_store_commit();
       };
       uint32_t gc = 0;
@@ -685,9 +685,9 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           const int tp = int(cur.t) - a.pf * CH;
           if (tp >= 0)
             for (int h = 0; h < 2; ++h) {
-              tma_prefetch_3d(&tmK, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmV, h * 64, tp, int(cur.m.bh));
-              tma_prefetch_3d(&tmDO, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmK, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmV, h * 64, tp, int(cur.m.bh));
+              tile_prefetch<M4>(a, &tmDO, h * 64, tp, int(cur.m.bh));
             }
         }
         const int s = gc & 1;
@@ -711,12 +711,12 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         RACE_TRACE(a, 1, gc);
         mbar_arrive_expect_tx(&fullV[s], TILE);
         for (int h = 0; h < 2; ++h)
-          tma_load_3d(smem + OFF_V + s * TILE + h * SUB, &tmV, &fullV[s], h * 64, t, bh, pol);
+          tile_load<M4>(a, smem + OFF_V + s * TILE + h * SUB, &tmV, &fullV[s], h * 64, t, bh, pol);
         mbar_wait(&emptyO[s], ((gc >> 1) & 1) ^ 1);
         RACE_TRACE(a, 2, gc);
         mbar_arrive_expect_tx(&fullO[s], TILE);
         for (int h = 0; h < 2; ++h)
-          tma_load_3d(smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
+          tile_load<M4>(a, smem + OFF_DO + s * TILE + h * SUB, &tmDO, &fullO[s], h * 64, t, bh, pol);
         // K last: its one buffer holds the previous chunk's dK until that is stored (K is only
         // needed by the tangent step, late in the chunk)
         if (gc >= 1) {
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         kt = t;
         kb = bh;
         mbar_arrive_expect_tx(fullK, TILE);
-        for (int h = 0; h < 2; ++h) tma_load_3d(smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
+        for (int h = 0; h < 2; ++h) tile_load<M4>(a, smem + OFF_K + h * SUB, &tmK, fullK, h * 64, t, bh, pol);
       }
       for (uint32_t j = gc >= 2 ? gc - 2 : 0; j < gc; ++j) store_dv(j);
       if (gc >= 1) store_dk(gc - 1);
@@ -1056,8 +1056,8 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
                             float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdq;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdo, d_o, g, g.dv) ||
-      !make_map(&mdq, dq, g, g.d))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdo, d_o, g, g.dv, L_DO) ||
+      !make_map(&mdq, dq, g, g.d, L_DQ))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -1074,9 +1074,10 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
   return launch_nt(k_bwd_causal_q8<__VA_ARGS__>, NTHREADS8, cq8::SMEM, grid_for(g), st, mq, mk, mv, mdo, mdq, \
                    mrows, a, rden, gden)
   switch (pass_corner_bits(g)) {
-    case 1: if (grp) RACE_CQ8(1, 0, true); RACE_CQ8(1);
-    case 2: if (grp) RACE_CQ8(2, 0, true); RACE_CQ8(2);
+    case 1: if (g.strided()) RACE_CQ8(1, 0, false, true); if (grp) RACE_CQ8(1, 0, true); RACE_CQ8(1);
+    case 2: if (g.strided()) RACE_CQ8(2, 0, false, true); if (grp) RACE_CQ8(2, 0, true); RACE_CQ8(2);
     default:
+      if (g.strided()) RACE_CQ8(3, 0, false, true);  // strided operands: one-pass problems only
       if (g.cb) RACE_CQ8(3, 2, true);
       if (grp) RACE_CQ8(3, 0, true);
       RACE_CQ8(3);
@@ -1090,8 +1091,8 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
                             const float* nrm, void* dk, void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
-  if (!make_map(&mq, q, g, g.d) || !make_map(&mk, k, g, g.d) || !make_map(&mv, v, g, g.dv) || !make_map(&mdo, d_o, g, g.dv) ||
-      !make_map(&mdk, dk, g, g.d) || !make_map(&mdv, dv, g, g.dv))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdo, d_o, g, g.dv, L_DO) ||
+      !make_map(&mdk, dk, g, g.d, L_DK) || !make_map(&mdv, dv, g, g.dv, L_DV))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -1101,7 +1102,7 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   a.dbg = trace_for("bk");
   if (!nrm) return cudaErrorInvalidValue;
   CUtensorMap mrd, mgd, mrows, mdv2;
-  if (!make_map(&mdv2, dv, g, g.dv)) return cudaErrorInvalidValue;
+  if (!make_map(&mdv2, dv, g, g.dv, L_DV)) return cudaErrorInvalidValue;
   const int64_t np = (g.N + 3) & ~int64_t(3);
   if (!make_map_f32_1d(&mrd, rden, g.BH * np, 128) || !make_map_f32_1d(&mgd, gden, g.BH * np, 128) ||
       !make_map_rows(&mrows, nrm, g.BH * g.N))
@@ -1111,9 +1112,10 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
   return launch_nt(k_bwd_causal_k8<__VA_ARGS__>, NTHREADS8, ck8::SMEM, grid_for(g), st, mk, mv, mdo, mdk, mrd, \
                    mgd, mrows, mdv2, a)
   switch (pass_corner_bits(g)) {
-    case 1: if (grp) RACE_CK8(1, 0, true); RACE_CK8(1);
-    case 2: if (grp) RACE_CK8(2, 0, true); RACE_CK8(2);
+    case 1: if (g.strided()) RACE_CK8(1, 0, false, true); if (grp) RACE_CK8(1, 0, true); RACE_CK8(1);
+    case 2: if (g.strided()) RACE_CK8(2, 0, false, true); if (grp) RACE_CK8(2, 0, true); RACE_CK8(2);
     default:
+      if (g.strided()) RACE_CK8(3, 0, false, true);  // strided operands: one-pass problems only
       if (g.cb) RACE_CK8(3, 2, true);
       if (grp) RACE_CK8(3, 0, true);
       RACE_CK8(3);

@@ -69,7 +69,46 @@ struct Args {
   // grouped backward: per-row dproj out (Geo::dproj_q / dproj_k) instead of the dq / dk store
   float* dproj_out;
   int dproj_ld, dproj_col, dproj_acc;
+  uint64_t hmagic;  // ceil(2^32 / H): sequence bh -> (head, batch) of the 4-D tensor maps (seq_hb)
 };
+
+// tile (c0 column, token t, sequence bh) of a make_map operand: sequence bh = b * H + h.  b = bh / H by
+// a multiply-high with hmagic = ceil(2^32 / H), exact for bh, H < 2^16 (BH <= 65535 is enforced): the
+// producer issues ~16 of these per chunk and sits on the chunk pipeline's critical path
+__device__ __forceinline__ int2 seq_hb(const Args& a, int bh) {
+  const int b = int((uint64_t(uint32_t(bh)) * a.hmagic) >> 32);
+  return make_int2(bh - b * int(a.H), b);
+}
+// M4 (compile time): strided operands, 4-D {width, N, H, B} maps; otherwise the 3-D {width, N, B*H}
+// maps of contiguous operands, with no index split on the default path
+template <bool M4>
+__device__ __forceinline__ void tile_load(const Args& a, void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int t,
+                                          int bh, uint64_t policy) {
+  if constexpr (M4) {
+    const int2 hb = seq_hb(a, bh);
+    tma_load_4d(dst, m, bar, c0, t, hb.x, hb.y, policy);
+  } else {
+    tma_load_3d(dst, m, bar, c0, t, bh, policy);
+  }
+}
+template <bool M4>
+__device__ __forceinline__ void tile_prefetch(const Args& a, const CUtensorMap* m, int c0, int t, int bh) {
+  if constexpr (M4) {
+    const int2 hb = seq_hb(a, bh);
+    tma_prefetch_4d(m, c0, t, hb.x, hb.y);
+  } else {
+    tma_prefetch_3d(m, c0, t, bh);
+  }
+}
+template <bool M4>
+__device__ __forceinline__ void tile_store(const Args& a, const CUtensorMap* m, const void* src, int c0, int t, int bh) {
+  if constexpr (M4) {
+    const int2 hb = seq_hb(a, bh);
+    tma_store_4d(m, src, c0, t, hb.x, hb.y);
+  } else {
+    tma_store_3d(m, src, c0, t, bh);
+  }
+}
 
 // Grouped backward extras, loaded at the start of a chunk so their global-memory latency stays off the
 // compute chain: the whole estimator's 1/D, -rho/D (ext) and, for corner groups, the dproj already
@@ -1038,18 +1077,32 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// [BH, N, 128] bf16 viewed as 3-D {128, N, BH}; box {64, 128, 1}; SW128
-// width = the tensor's row length (d for Q, K, dQ, dK; dv for V, O, dO, dV), <= DH: the two 64-column
-// boxes of a tile read zeros beyond it and stores beyond it are clipped, so narrower heads run on the
-// same kernels without padded copies
-inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g, int width) {
+// [B, H, N, width] bf16 viewed as 4-D {width, N, H, B} (strides of Geo::lay[which], or the contiguous
+// [B*H, N, width] layout); box {64, 128, 1, 1}; SW128.  width = the tensor's row length (d for Q, K, dQ,
+// dK; dv for V, O, dO, dV), <= DH: the two 64-column boxes of a tile read zeros beyond it and stores
+// beyond it are clipped, so narrower heads run on the same kernels without padded copies.  The
+// per-dimension strides need not be monotonic: a [B, N, H, d] view (token stride H*d, head stride d)
+// is described in place, without a transposed copy.
+inline bool make_map(CUtensorMap* m, const void* ptr, const Geo& g, int width, LayIdx which) {
   auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {cuuint64_t(width), cuuint64_t(g.N), cuuint64_t(g.BH)};
-  cuuint64_t strides[2] = {cuuint64_t(width) * 2, cuuint64_t(g.N) * width * 2};
-  cuuint32_t box[3] = {64, CH, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+  if (!fn || g.H <= 0 || g.BH % g.H) return false;
+  if (!g.strided()) {  // 3-D {width, N, B*H} (kernels instantiated with M4 = false)
+    cuuint64_t dims[3] = {cuuint64_t(width), cuuint64_t(g.N), cuuint64_t(g.BH)};
+    cuuint64_t strides[2] = {cuuint64_t(width) * 2, cuuint64_t(g.N) * width * 2};
+    cuuint32_t box[3] = {64, CH, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const Lay& l = g.lay[which];
+  const int64_t st = l.token ? l.token : width, sh = l.token ? l.head : g.N * width,
+                sbt = l.token ? l.batch : g.H * g.N * width;
+  cuuint64_t dims[4] = {cuuint64_t(width), cuuint64_t(g.N), cuuint64_t(g.H), cuuint64_t(g.BH / g.H)};
+  cuuint64_t strides[3] = {cuuint64_t(st) * 2, cuuint64_t(sh) * 2, cuuint64_t(sbt) * 2};
+  cuuint32_t box[4] = {64, CH, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -1102,6 +1155,7 @@ inline Args make_args(const Geo& g) {
   a.P = pass_corner_bits(g);  // corner bits of this pass (the kernels' template P)
   a.T = g.T;
   a.TP = g.T * g.P;           // projections (all hyperplanes of the pass's tables)
+  a.hmagic = ((uint64_t(1) << 32) + uint64_t(g.H) - 1) / uint64_t(g.H);
   a.dw = g.d;
   a.dvv = g.dv;
   a.ldt = g.dv + 1;

@@ -144,6 +144,10 @@ class Problem:
         self.w, per_head, heads = prepare_w(w, p, self.d, q.device)
         if per_head and (len(self.lead) == 0 or self.lead[-1] != heads):
             raise ValueError(f"per-head hyperplanes for {heads} heads but inputs have lead dims {self.lead}")
+        # desc heads = the operands' head dimension (W indexing uses it only when per_head; strided
+        # operands are addressed as [B, H, N, w] through it)
+        if not per_head and self.lead:
+            heads = max(self.lead[-1], 1)
         m = _meta(dtype=_DTYPES[q.dtype], batch_heads=max(bh, 1), heads=heads, n=self.n, dim=self.d,
                   dim_v=self.dv, hyperplanes=p.hyperplanes, tables=p.tables, beta=float(p.beta),
                   causal=p.causal, normalize=p.normalize, w_per_head=per_head)
@@ -151,6 +155,7 @@ class Problem:
         self.nseg, self.seg_tokens = m.nseg, m.seg_tokens
         self._ws_bytes, self._state_elems = m.ws_bytes, m.state_elems
         self.grouped = m.grouped
+        self.one_pass_fast = bool(m.fast) and not m.grouped
         self.table_elems = (p.tables << p.hyperplanes) * (self.dv + 1)
 
     def ws(self) -> torch.Tensor:
@@ -192,11 +197,51 @@ def _c(t: torch.Tensor) -> torch.Tensor:
     return t.clone(memory_format=torch.contiguous_format) if t.is_contiguous() else t.contiguous()
 
 
+def _strides(t: torch.Tensor):
+    """(token, head, batch) element strides of a non-contiguous [B, H, N, w] view the tcgen05 kernels can
+    read in place through their 4-D TMA maps (rows contiguous, 16-byte aligned base and strides), e.g.
+    ``x.view(B, N, H, d).transpose(1, 2)`` of a [B, N, H*d] projection; None otherwise."""
+    if t.dim() != 4 or t.is_contiguous() or t.stride(-1) != 1 or t.data_ptr() % 16:
+        return None
+    sb, sh, sn = t.stride(0), t.stride(1), t.stride(2)
+    if sb % 8 or sh % 8 or sn % 8 or min(sb, sh, sn) < 0:
+        return None
+    return sn, sh, sb
+
+
+def _bnhd(like: torch.Tensor, width: int) -> torch.Tensor:
+    """An uninitialised [B, H, N, width] tensor stored as [B, N, H, width] (the layout of ``like``'s
+    producer), so the caller's transpose back to [B, N, H*width] is a free view."""
+    b, h, n = like.shape[:3]
+    return torch.empty((b, n, h, width), dtype=like.dtype, device=like.device).transpose(1, 2)
+
+
+def _layout(**tensors):
+    """RaceLayout of the given operands (contiguous ones keep token stride 0)."""
+    lay = _lib.RaceLayout()
+    for name, t in tensors.items():
+        st = _strides(t) if t is not None else None
+        if st is not None:
+            getattr(lay, name).token, getattr(lay, name).head, getattr(lay, name).batch = st
+    return lay
+
+
+def _strided_ok(pr: "Problem", *ts) -> bool:
+    """Use the strided path: some operand is a readable strided view and the problem runs as one tcgen05
+    pass (everything else takes contiguous copies)."""
+    return pr.one_pass_fast and any(_strides(t) is not None for t in ts) and \
+        all((t.is_contiguous() and t.data_ptr() % 16 == 0) or _strides(t) is not None for t in ts)
+
+
 def _race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
-    """race_forward at the tensors' own width."""
-    q, k, v = _c(q), _c(k), _c(v)
+    """race_forward at the tensors' own width.  [B, N, H, d]-strided q, k, v views (a fused projection's
+    output) run in place on the one-pass tcgen05 path, and O is then returned in the same
+    [B, N, H, dv] storage order."""
     pr = Problem(q, k, v, w, p)
-    o = torch.empty_like(v)
+    strided = _strided_ok(pr, q, k, v)
+    if not strided:
+        q, k, v = _c(q), _c(k), _c(v)
+    o = _bnhd(v, pr.dv) if strided and _strides(v) is not None else torch.empty_like(v, memory_format=torch.contiguous_format)
     den = torch.empty(pr.lead + (pr.n,), dtype=torch.float32, device=pr.device)
     shape = pr.state_shape() if want_state else None
     state = torch.empty(shape, dtype=torch.float32, device=pr.device) if shape is not None else None
@@ -205,8 +250,13 @@ def _race_forward(q, k, v, w, p: SketchParams, *, want_state: bool = True):
             state.zero_()
         return o, den, state
     ws = pr.ws()
-    _lib.check(_lib.lib().race_fwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(o), _vp(den),
-                                   _vp(state), _vp(ws), _stream()), "race_fwd")
+    if strided:
+        lay = _layout(q=q, k=k, v=v, o=o)
+        _lib.check(_lib.lib().race_fwd_layout(pr.dref, ctypes.byref(lay), _vp(q), _vp(k), _vp(v), _vp(pr.w),
+                                              _vp(o), _vp(den), _vp(state), _vp(ws), _stream()), "race_fwd_layout")
+    else:
+        _lib.check(_lib.lib().race_fwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(o), _vp(den),
+                                       _vp(state), _vp(ws), _stream()), "race_fwd")
     return o, den, state
 
 
@@ -214,15 +264,18 @@ def _race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: boo
     """race_backward at the tensors' own width."""
     if inplace and not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
         raise ValueError("inplace backward needs contiguous q, k, v")
-    q, k, v, d_o = _c(q), _c(k), _c(v), _c(d_o)
     pr = Problem(q, k, v, w, p)
     _check_device(pr.device, d_o=d_o, state=state)
     if d_o.shape != v.shape or d_o.dtype != v.dtype:
         raise ValueError(f"d_out shape {tuple(d_o.shape)} does not match output shape {tuple(v.shape)}")
+    strided = not inplace and _strided_ok(pr, q, k, v, d_o)
+    if not strided:
+        q, k, v, d_o = _c(q), _c(k), _c(v), _c(d_o)
     if inplace:
         dq, dk, dv = q, k, v
-    else:
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    else:  # gradients in their inputs' storage order (a strided q gets a [B, N, H, d]-ordered dq)
+        dq, dk, dv = (_bnhd(x, x.shape[-1]) if strided and _strides(x) is not None
+                      else torch.empty_like(x, memory_format=torch.contiguous_format) for x in (q, k, v))
     if pr.n == 0 or pr.bh == 0:
         return dq, dk, dv
     if state is not None:
@@ -230,8 +283,14 @@ def _race_backward(q, k, v, w, d_o, p: SketchParams, state=None, *, inplace: boo
         if tuple(state.shape) != pr.state_shape() or state.dtype != torch.float32:
             raise ValueError("state does not match this problem")
     ws = pr.ws()
-    _lib.check(_lib.lib().race_bwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(d_o), _vp(state),
-                                   _vp(dq), _vp(dk), _vp(dv), _vp(ws), _stream()), "race_bwd")
+    if strided:
+        lay = _layout(q=q, k=k, v=v, d_o=d_o, dq=dq, dk=dk, dv=dv)
+        _lib.check(_lib.lib().race_bwd_layout(pr.dref, ctypes.byref(lay), _vp(q), _vp(k), _vp(v), _vp(pr.w),
+                                              _vp(d_o), _vp(state), _vp(dq), _vp(dk), _vp(dv), _vp(ws), _stream()),
+                   "race_bwd_layout")
+    else:
+        _lib.check(_lib.lib().race_bwd(pr.dref, _vp(q), _vp(k), _vp(v), _vp(pr.w), _vp(d_o), _vp(state),
+                                       _vp(dq), _vp(dk), _vp(dv), _vp(ws), _stream()), "race_bwd")
     return dq, dk, dv
 
 

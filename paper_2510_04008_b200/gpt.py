@@ -51,7 +51,10 @@ class Block(nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         b, n, c = x.shape
         q, k, v = self.qkv(self.ln1(x)).split(c, dim=-1)
-        q, k, v = (t.view(b, n, self.heads, c // self.heads).transpose(1, 2).contiguous() for t in (q, k, v))
+        # [B, H, N, d] views of the projection's [B, N, H*d] columns: the tcgen05 kernels read them in
+        # place (4-D TMA maps, race_fwd_layout) and write O in [B, N, H, d] order, so neither the
+        # transposes here nor the one below copy
+        q, k, v = (t.view(b, n, self.heads, c // self.heads).transpose(1, 2) for t in (q, k, v))
         o = self.attn(q, k, v)
         x = x + self.proj(o.transpose(1, 2).reshape(b, n, c))
         return x + self.out(F.gelu(self.fc(self.ln2(x)), approximate="tanh"))
