@@ -63,9 +63,11 @@ constexpr int OFF_W = 5 * TILE;                // W' (B of the projection; B of 
 constexpr int OFF_SOPT = OFF_W + WOP;
 constexpr int OFF_PHIQ = OFF_SOPT + WOP;       // phi_q / D (B of dS)
 constexpr int OFF_PHIK = OFF_PHIQ + PHI;       // Phi_k (B of S and Z), then dproj (A of dx^)
-constexpr int OFF_X = OFF_PHIK + PHI;          // kp[2 parity][4][8], cs[128][8] (in-warp scans of phi_k), da[4][8]
+constexpr int OFF_X = OFF_PHIK + PHI;          // kp[2 parity][4][8], cs[128][8] (in-warp scans of phi_k), da[4][8],
+                                               // pq[128][8], dot[128]
 constexpr int XKP = 0, XCS = 64, XDA = 64 + CH * FP;
-constexpr int OFF_TOK = OFF_X + (XDA + 32) * 4;  // [2] x sketch rows [128][ROWW] (TMA)
+constexpr int XPQ = XDA + 32, XDOT = XPQ + CH * FP;  // phi_q [128][8] and dx^.x^ [128]: first half -> second
+constexpr int OFF_TOK = OFF_X + (XDOT + CH) * 4;  // [2] x sketch rows [128][ROWW] (TMA)
 constexpr int TOK_BYTES = CH * ROWW * 4;
 constexpr int OFF_BAR = OFF_TOK + 2 * TOK_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
@@ -365,6 +367,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         const Scale scq = row_scale(valid ? trow[7] : 0.f, a.normalize);
         mbar_arrive(&emptyT[s]);
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 9, gc);
+        // the first half computes phi_q (and later the feature VJP) for both; the second half computes
+        // phi_k, its operand and scan, and reads phi_q back after the barrier below
         float phq[FP], uq[5];
         if (h == 1) {  // Phi_k operand, in-warp inclusive scan of phi_k (C_t) and the warp totals
           float phk[FP], uk[5];
@@ -385,8 +389,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xkp[qw * FP + f] = phk[f];
           }
+        } else {
+          row_features_hat<P, HB>(a, hq, valid, phq, uq);
+#pragma unroll
+          for (int f = 0; f < FP; ++f) xbase[XPQ + r * FP + f] = phq[f];
         }
-        row_features_hat<P, HB>(a, hq, valid, phq, uq);
         // tril(E) -> hi / lo bf16 pairs into TMEM (A operands of Z), my 64 columns
         mbar_wait(c1, par);
         tc_fence_after();
@@ -416,7 +423,11 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive(phi_ready);
         float yv[16];
         tmem_ld16(tmem + lb + TM_Y, yv);
-        compute_bar256();  // the phi_k scans and warp totals are visible
+        compute_bar256();  // the phi_k scans, warp totals and phi_q are visible
+        if (h == 1) {
+#pragma unroll
+          for (int f = 0; f < FP; ++f) phq[f] = xbase[XPQ + r * FP + f];
+        }
         float y[FP], C[FP], Dint = 0.f, ydot = 0.f, rs = 0.f;
         tmem_ld_wait();
 #pragma unroll
@@ -451,14 +462,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           rD = pre.rd;
           rho = rD != 0.f ? -pre.gd / rD : 0.f;
         }
-        float dphi[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] + Z[f] - rho * (A[f] + C[f])) * rD;
-        float dproj[8];
-        row_feature_vjp<P, HB>(a, uq, phq, dphi, dproj);
-        if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
-        const float dotq = dot_from_proj(dproj, hq);
         if (h == 0) {
+          float dphi[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) dphi[f] = (y[f] + Z[f] - rho * (A[f] + C[f])) * rD;
+          float dproj[8];
+          row_feature_vjp<P, HB>(a, uq, phq, dphi, dproj);
+          if (GRP && a.dproj_out && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
+          xbase[XDOT + r] = dot_from_proj(dproj, hq);  // read by the second half after c4
           write_dproj_w(sb + OFF_PHIK, r, dproj, a.TP);  // Phi_k is dead after Z and S (c2)
 #pragma unroll
           for (int f = 0; f < FP; ++f) dA[f] = fmaf(phq[f], -rho * rD, dA[f]);
@@ -492,7 +503,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         if (threadIdx.x == a.ttid) RACE_TRACE(a, 12, gc);
         tc_fence_after();
         mbar_wait(&fullQ[s], (gc >> 1) & 1);  // q itself is only read here (x^ of the tangent step)
-        tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, dotq);
+        tangent_half_inplace(tmem + lb + TM_DX, qtile, r, h, scq, xbase[XDOT + r]);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
