@@ -564,7 +564,7 @@ constexpr int OFF_DSOP = OFF_DSOPT + WOP;  // [128 x 32] B of dV_a = Phi_k dS_v
 constexpr int OFF_PHIQ = OFF_DSOP + PHI;   // [hi|hi|lo|0]  B of Pm^T (K) and of Z (MN); then dproj (A of dx^)
 constexpr int OFF_PHIK = OFF_PHIQ + PHI;   // [hi|lo|hi|0]  A of Pm^T and dV_a
 constexpr int OFF_PHIT = OFF_PHIK + PHI;   // phi_q / D     B of dS (MN)
-constexpr int OFF_X = OFF_PHIT + PHI;      // [2 parity] x { unused[256], dac[4][8] }
+constexpr int OFF_X = OFF_PHIT + PHI;      // [2 parity] x { dx^.x^ [128], unused[128], dac[4][8] }
 constexpr int XPAR = 256 + 32;
 constexpr int OFF_TOK = OFF_X + 2 * XPAR * 4;  // [2 parity] x { rden[128], gden[128], sketch rows[128][ROWW] } (TMA)
 constexpr int TOK_BYTES = (256 + CH * ROWW) * 4;
@@ -926,7 +926,6 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
             for (int f = 0; f < FP; ++f) xpar[256 + qw * FP + f] = dac[f];
           }
-          row_features_hat<P, HB>(a, hk, valid, phk, uk);  // for dk (off the MMA path)
         }
       }
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 24, gc);
@@ -994,19 +993,23 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       mbar_wait(c3, par);
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 11, gc);
       tc_fence_after();
-      float zhi[8], zlo[8], zv[16];  // Z columns 8..15 / 24..31: the duplicate hi copy and padding (not read)
-      tmem_ld8(tmem + lb + TM_Z, zhi);
-      tmem_ld8(tmem + lb + TM_Z + 16, zlo);
-      tmem_ld16(tmem + lb + TM_ZV, zv);
-      tmem_ld_wait();
-      float dphi[FP];
+      // (the second half, which holds phi_k, runs the feature VJP for both; the first half reads the dS
+      // state out below)
+      if (h == 1) {
+        float zhi[8], zlo[8], zv[16];  // Z columns 8..15 / 24..31: the duplicate hi copy and padding
+        tmem_ld8(tmem + lb + TM_Z, zhi);
+        tmem_ld8(tmem + lb + TM_Z + 16, zlo);
+        tmem_ld16(tmem + lb + TM_ZV, zv);
+        tmem_ld_wait();
+        float dphi[FP];
 #pragma unroll
-      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zhi[f] + zlo[f];
-      float dproj[8];
-      row_feature_vjp<P, HB>(a, uk, phk, dphi, dproj);
-      if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
-      const float dotk = dot_from_proj(dproj, hk);
-      if (h == 1) cq8::write_dproj_w(sb + OFF_PHIQ, r, dproj, a.TP);  // Phi_q is dead after Pm, Z (c3)
+        for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f] + zhi[f] + zlo[f];
+        float dproj[8];
+        row_feature_vjp<P, HB>(a, uk, phk, dphi, dproj);
+        if (GRP && a.dproj_out && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
+        xpar[r] = dot_from_proj(dproj, hk);  // dx^.x^ for both halves' tangent step (read after c4)
+        cq8::write_dproj_w(sb + OFF_PHIQ, r, dproj, a.TP);  // Phi_q is dead after Pm, Z (c3)
+      }
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dp_ready);
@@ -1017,7 +1020,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       // ---- dV out; dS_>c-1 operands for the next (earlier) chunk once the dV MMA has read DSOP
       mbar_wait(cdv, par);
       tc_fence_after();
-      if (h == 1) {
+      if (h == 0) {
         float dhi[8], dlo[8];
         tmem_ld8(tmem + lb + TM_DS, dhi);
         tmem_ld8(tmem + lb + TM_DS + 16, dlo);
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 12, gc);
       tc_fence_after();
       mbar_wait(fullK, gc & 1);  // k itself is only read here (x^ of the tangent step)
-      tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K, r, h, sck, dotk);
+      tangent_half_inplace(tmem + lb + TM_DX, smem + OFF_K, r, h, sck, xpar[r]);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(dkstaged);
