@@ -539,8 +539,8 @@ using cfw::OFF_W;
 using cfw::OFF_PHIQ;
 using cfw::OFF_PHIK;
 using cfw::OFF_SOP;
-constexpr int OFF_X = cfw::OFF_BAR;  // [2 parity] x { sq[2][128], rs[2][128], kp[4][8] } floats
-constexpr int XPAR = 256 + 256 + 32;
+constexpr int OFF_X = cfw::OFF_BAR;  // [2 parity] x { sq[2][128], rs[2][128], kp[4][8], phi_q.A[128] } floats
+constexpr int XPAR = 256 + 256 + 32 + 128;
 constexpr int OFF_BAR = OFF_X + 2 * XPAR * 4;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_PA = 192;  // P~ as bf16 pairs: 128 lanes x 64 columns
@@ -814,17 +814,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tc_fence_before();
         mbar_arrive(phi_full);
       } else {
-        float pq[16], phk[FP];
+        float phk[FP];  // (phi_q is the first half's: this half gets phi_q . A from it below)
         if (KR) {
           float u[5];
           row_features_hat<P, HB>(a, hk, valid, phk, u);
-          tmem_ld16(tmem + lb + TM_PROJQ, pq);
           write_phi_k(sb + OFF_PHIK, r, phk);
-          tmem_ld_wait();
         } else {
           float pk[16];
           tmem_ld16(tmem + lb + TM_PROJK, pk);
-          tmem_ld16(tmem + lb + TM_PROJQ, pq);
           tmem_ld_wait();
           row_features<P, HB>(a, pk, invk, valid, phk);
           write_phi_k(sb + OFF_PHIK, r, phk);
@@ -847,11 +844,13 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
 #pragma unroll
           for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
         }
-        row_features<P, HB>(a, pq, invq, valid, phq);
       }
       float D = 0.f;
+      if (h == 0) {
 #pragma unroll
-      for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
+        for (int f = 0; f < FP; ++f) D = fmaf(phq[f], A[f], D);
+        xpar[544 + r] = D;  // for the second half (read after the barrier below)
+      }
       // ---- intra-chunk weights: P~ = tril(Pm) -> bf16 pairs into TMEM (my 64 columns)
       mbar_wait(pm_full, gc & 1);
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 6, gc);
@@ -900,6 +899,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       if (threadIdx.x == CT0 && cur.ok()) mbar_arrive(&emptyqk[(gc + 1) & 1]);
       sqq = xpar[r];
       sqk = xpar[128 + r];
+      if (h == 1) D = xpar[544 + r];
       D += xpar[256 + r] + xpar[384 + r];
       if (h == 0 && valid) a.den[m.bh * a.N + t + r] = D * invT;
       const float rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
