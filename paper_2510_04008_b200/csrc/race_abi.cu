@@ -1,16 +1,18 @@
-#include <cstdlib>
 // race_abi.cu -- the extern "C" boundary declared in include/race_b200.h.
 //
 // Validation mirrors the reference's ValueError rules (SketchConfig
 // ra/core.py:70-82, AttnInputs ra/exact.py:34-39); the Python layer maps the
 // returned status back to ValueError.  Every entry point is stream-ordered,
-// allocation-free and thread-safe (the only global is the thread-local error
-// string).
+// allocation-free and thread-safe (globals: the thread-local error string and
+// call layout, and a mutex-guarded per-shape segmentation cache).
 #include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <type_traits>
 
@@ -77,7 +79,11 @@ int report_cuda(cudaError_t e, const char* where) { return cuda_status(e, where)
 
 namespace {
 
-constexpr int64_t kSegTarget = 148 * 8;  // work items to aim for across all (b, h): tcgen05 kernels
+// work items to aim for across all (b, h): tcgen05 kernels; RACE_SEG_TARGET overrides (tuning)
+const int64_t kSegTarget = [] {
+  const char* e = getenv("RACE_SEG_TARGET");
+  return e && e[0] ? int64_t(atoll(e)) : int64_t(148) * 8;
+}();
 // CUDA-core kernels (one CTA per item, 2 per SM); RACE_SIMT_SEG_TARGET overrides (tuning)
 const int64_t kSegTargetSimt = [] {
   const char* e = getenv("RACE_SIMT_SEG_TARGET");
@@ -87,6 +93,53 @@ const int64_t kSegTargetSimt = [] {
 // operand strides of the race_fwd_layout / race_bwd_layout call in progress on this thread (every entry
 // point it calls resolves its Geo through resolve_shape, which copies them in)
 thread_local const race_layout_t* t_layout = nullptr;
+
+// segment length (a multiple of 128 tokens) for about `items` work items across all (b, h)
+int64_t segment_for(int64_t BH, int64_t N, int64_t items) {
+  int64_t target = (items + BH - 1) / BH;
+  if (target < 1) target = 1;
+  int64_t per = (N + target - 1) / target;
+  per = ((per + 127) / 128) * 128;
+  return per < 128 ? 128 : per;
+}
+
+// tcgen05 path: the persistent kernels give each of the 148 CTAs a contiguous range of items (cta_range:
+// an even split by count) and carry the bucket state across the items of a range, but every item end
+// drains the pipeline (partial totals out).  Among 1, 2, 4 and 8 items per CTA, take the segment length
+// whose busiest CTA has the fewest 128-token chunks, and among those the fewest items (measured at the
+// headline shape: 8 items per CTA 457 us, 2 items per CTA 451 us per causal step).  Cached per shape.
+int64_t fast_segment(int64_t BH, int64_t N) {
+  static std::mutex mu;
+  static std::map<std::pair<int64_t, int64_t>, int64_t> cache;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({BH, N});
+    if (it != cache.end()) return it->second;
+  }
+  const int64_t G = 148, cps = (N + 127) / 128;
+  int64_t best = 0, best_load = INT64_MAX;
+  for (int64_t per_cta = 1; per_cta <= 8; per_cta *= 2) {
+    const int64_t seg = segment_for(BH, N, G * per_cta), sc = seg / 128;
+    const int64_t nseg = N > 0 ? (N + seg - 1) / seg : 1, items = BH * nseg;
+    const int64_t grid = items < G ? items : G;
+    int64_t load = 0;
+    for (int64_t b = 0; b < grid; ++b) {  // chunks of CTA b's item range
+      int64_t sum = 0;
+      for (int64_t i = b * items / grid; i < (b + 1) * items / grid; ++i) {
+        const int64_t s = i % nseg;
+        sum += s + 1 < nseg ? sc : cps - s * sc;
+      }
+      load = sum > load ? sum : load;
+    }
+    if (load < best_load) {  // ties keep the earlier (longer-segment) candidate
+      best_load = load;
+      best = seg;
+    }
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache[{BH, N}] = best;
+  return best;
+}
 
 int resolve_shape(const race_desc_t* d, race::Geo* g) {
   if (!d) return fail(RACE_EBADSHAPE, "null descriptor");
@@ -119,14 +172,10 @@ int resolve_shape(const race_desc_t* d, race::Geo* g) {
   // per SM: aim for ~7 full waves of 2 x 148 so the last wave's tail is small (3.5 waves of 512-token
   // segments left the last wave half empty at N = 131072, H = 4).
   const bool fast_capable = g->dtype == RACE_BF16 && g->d <= 128 && g->dv <= 128 && g->d % 8 == 0 && g->dv % 8 == 0;
-  const int64_t seg_target = fast_capable ? kSegTarget : kSegTargetSimt;
-  int64_t target = (seg_target + g->BH - 1) / g->BH;
-  if (target < 1) target = 1;
-  int64_t per = (g->N + target - 1) / target;
-  per = ((per + 127) / 128) * 128;
-  if (per < 128) per = 128;
-  g->seg_tokens = per;
-  g->nseg = g->N > 0 ? (g->N + per - 1) / per : 1;
+  g->seg_tokens = fast_capable && !getenv("RACE_SEG_TARGET") ? fast_segment(g->BH, g->N)
+                                                              : segment_for(g->BH, g->N, fast_capable ? kSegTarget
+                                                                                                    : kSegTargetSimt);
+  g->nseg = g->N > 0 ? (g->N + g->seg_tokens - 1) / g->seg_tokens : 1;
   if (g->nseg > 0x7fffffff) return fail(RACE_EUNSUPPORTED, "too many segments");
   if (t_layout) {
     const race_stride_t* src[race::L_COUNT] = {&t_layout->q,  &t_layout->k,  &t_layout->v,  &t_layout->o,
