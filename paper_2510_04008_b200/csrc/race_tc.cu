@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
 
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
 
@@ -594,6 +596,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
   if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
@@ -980,6 +983,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
   if (warp == 0) {

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
 
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
 

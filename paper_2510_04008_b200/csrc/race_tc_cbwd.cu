@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
   if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);
@@ -658,6 +659,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   int64_t i0, i1;
   cta_range(a.BH * a.nseg, i0, i1);
   if (threadIdx.x == 0) RACE_CTA_TIME(a, 0);

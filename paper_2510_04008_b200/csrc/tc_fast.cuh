@@ -1233,21 +1233,37 @@ inline unsigned grid_for(const Geo& g) {
   return unsigned(items < num_sms() ? items : num_sms());
 }
 
+// Every tcgen05 kernel is launched with programmatic stream serialisation (PDL): its CTAs may start on
+// SMs the previous kernel's CTAs have left, run their prologue (barrier init, TMEM allocation, tensor-map
+// prefetch) and block in grid_dep_wait() until that kernel has completed.  RACE_NO_PDL=1 disables it.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RACE_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 template <typename K, typename... Ts>
 cudaError_t launch_nt(K kernel, int nthreads, int smem, unsigned grid, cudaStream_t st, Ts... args) {
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem);
   if (e != cudaSuccess) return e;
-  kernel<<<grid, nthreads, smem, st>>>(args...);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(nthreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kernel, args...);
   note_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 template <typename K, typename... Ts>
 cudaError_t launch(K kernel, int smem, unsigned grid, cudaStream_t st, Ts... args) {
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem);
-  if (e != cudaSuccess) return e;
-  kernel<<<grid, NTHREADS, smem, st>>>(args...);
-  note_launch();
-  return cudaGetLastError();
+  return launch_nt(kernel, NTHREADS, smem, grid, st, args...);
 }
 
 }  // namespace tcfast
