@@ -18,6 +18,8 @@
 //
 // Determinism: no atomics; every reduction has a fixed order, so results are
 // bit-identical run to run (the reference's criterion 9, ra/acceptance.py:419).
+#include <cstdlib>
+
 #include "race_common.cuh"
 #include "race_internal.h"
 
@@ -962,6 +964,7 @@ __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, i
                                                      const float* __restrict__ part, const float* __restrict__ carry,
                                                      float* __restrict__ out) {
   __shared__ float gs[CG][33];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL after the partials' kernel
   const int lx = threadIdx.x & 31, gy = threadIdx.x >> 5;
   const int64_t e = int64_t(blockIdx.x) * 32 + lx;
   const int64_t bh = blockIdx.y;
@@ -1130,10 +1133,19 @@ cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const 
 }
 cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st) {
   const int64_t E = (int64_t(g.T) << pass_corner_bits(g)) * (g.dv + 1);
-  dim3 grid(unsigned((E + 31) / 32), unsigned(g.BH));
-  simt::k_combine<<<grid, 32 * simt::CG, 0, st>>>(g.BH, g.nseg, E, mode, part, carry, out);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned((E + 31) / 32), unsigned(g.BH));
+  cfg.blockDim = dim3(32 * simt::CG);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];  // programmatic dependent launch (see tcfast::launch_nt)
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  const char* nopdl = getenv("RACE_NO_PDL");
+  cfg.attrs = attr;
+  cfg.numAttrs = (nopdl && nopdl[0] == '1') ? 0 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, simt::k_combine, g.BH, g.nseg, E, mode, part, carry, out);
   note_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace race
