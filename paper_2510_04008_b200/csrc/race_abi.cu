@@ -941,7 +941,11 @@ int race_fwd(const race_desc_t* desc, const void* q, const void* k, const void* 
     // the aggregation also writes the k halves of the sketch rows, so the scan reads Q, V and those rows
     float* nrm = state ? state + carry_elems(g) : ws.rows;
     if (int rc = race_kside_partials_rows(desc, k, v, w, ws.part, nrm, workspace, stream)) return rc;
-    if (int rc = race_combine(desc, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, stream)) return rc;
+    // into a state: the carries' alignment gap is zeroed too, so the whole state is deterministic
+    const int pad = state ? int(carry_elems(g) - g.BH * g.nseg * table_elems(g)) : 0;
+    if (int rc = cuda_status(race::combine(g, RACE_COMBINE_PREFIX, ws.part, nullptr, tabs, S(stream), pad),
+                             "combine"))
+      return rc;
     return race_fwd_causal_krows(desc, q, k, v, w, tabs, o, den, nrm, workspace, stream);
   }
   if (int rc = race_kside_partials(desc, k, v, w, ws.part, workspace, stream)) return rc;

@@ -69,6 +69,9 @@ cudaError_t simt_bwd_causal_q(const Geo& g, const void* q, const void* k, const 
 cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const void* v, const void* d_o,
                               const float* w, const float* rden, const float* gden, const float* dcar, void* dk,
                               void* dv, cudaStream_t st);
-cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st);
+// pad > 0: also zero the `pad` floats after the BH * nseg * E outputs (the causal state's alignment gap, so
+// the state is bitwise deterministic; only when `out` is a race_fwd state)
+cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st,
+                    int pad = 0);
 
 }  // namespace race

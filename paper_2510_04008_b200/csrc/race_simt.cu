@@ -962,9 +962,10 @@ constexpr int CG = 16;
 constexpr int CPER = 16;  // segments per group held in registers (nseg <= CG * CPER); longer groups loop
 __global__ void __launch_bounds__(32 * CG) k_combine(int64_t BH, int64_t nseg, int64_t E, int mode,
                                                      const float* __restrict__ part, const float* __restrict__ carry,
-                                                     float* __restrict__ out) {
+                                                     float* __restrict__ out, int pad) {
   __shared__ float gs[CG][33];
   asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL after the partials' kernel
+  if (pad > 0 && blockIdx.x == 0 && blockIdx.y == 0 && int(threadIdx.x) < pad) out[BH * nseg * E + threadIdx.x] = 0.f;
   const int lx = threadIdx.x & 31, gy = threadIdx.x >> 5;
   const int64_t e = int64_t(blockIdx.x) * 32 + lx;
   const int64_t bh = blockIdx.y;
@@ -1131,7 +1132,8 @@ cudaError_t simt_bwd_causal_k(const Geo& g, const void* q, const void* k, const 
                               void* dv, cudaStream_t st) {
   return RACE_DISPATCH(bwd_causal_k, g, q, k, v, d_o, w, rden, gden, dcar, dk, dv, st);
 }
-cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st) {
+cudaError_t combine(const Geo& g, int mode, const float* part, const float* carry, float* out, cudaStream_t st,
+                    int pad) {
   const int64_t E = (int64_t(g.T) << pass_corner_bits(g)) * (g.dv + 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned((E + 31) / 32), unsigned(g.BH));
@@ -1143,7 +1145,7 @@ cudaError_t combine(const Geo& g, int mode, const float* part, const float* carr
   const char* nopdl = getenv("RACE_NO_PDL");
   cfg.attrs = attr;
   cfg.numAttrs = (nopdl && nopdl[0] == '1') ? 0 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, simt::k_combine, g.BH, g.nseg, E, mode, part, carry, out);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, simt::k_combine, g.BH, g.nseg, E, mode, part, carry, out, pad);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
