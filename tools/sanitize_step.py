@@ -11,5 +11,11 @@ for causal in (True, False):
     o, den, st = rb.race_forward(q, k, v, w, cfg.params())
     dq, dk, dv = rb.race_backward(q, k, v, w, g, cfg.params(), state=st)
     dq2 = rb.race_backward(q, k, v, w, g, cfg.params())
+    # strided [B, N, H, d] operands (4-D TMA maps) and a narrow head width
+    qkv = torch.randn(1, 1000, 3 * 2 * 64, device=dev).to(torch.bfloat16)
+    qs, ks, vs = (x.view(1, 1000, 2, 64).transpose(1, 2) for x in qkv.split(128, dim=-1))
+    w64 = rb.head_hyperplanes(cfg, 2, 64).to(dev)
+    o, den, st = rb.race_forward(qs, ks, vs, w64, cfg.params())
+    rb.race_backward(qs, ks, vs, w64, o, cfg.params(), state=st)
 torch.cuda.synchronize()
 print("ok")
