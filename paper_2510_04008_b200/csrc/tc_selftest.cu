@@ -298,3 +298,98 @@ extern "C" int tc_selftest_gemm(int M, int N, int K, int a_mn, int b_mn, int a_s
   }
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Throughput probes (tools/tmem_probe.py): how fast one SM reads TMEM with tcgen05.ld and how many
+// cycles one tcgen05.mma of the shapes the causal kernels issue takes, A from shared memory (SS) or
+// from TMEM (TS).  Results (cycles) go to out[]; nothing here is on the library's hot path.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_tmem_ld_rate(int iters, long long* out) {
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+  const uint32_t col0 = uint32_t(warp >> 2) * 32 % 512;
+  float acc = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    float v0[32], v1[32];
+    tmem_ld32(tmem + lane_base + ((col0 + 64 * (i & 3)) & 511), v0);
+    tmem_ld32(tmem + lane_base + ((col0 + 64 * (i & 3) + 32) & 511), v1);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc += v0[j] + v1[j];
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  if (acc == 12345.f) out[gridDim.x] = 1;  // keep the loads live
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// n_mma tcgen05.mma of M = 128, N = n, K = 16 (bf16) per round, `rounds` rounds, each ended by a commit and
+// its mbarrier wait; ts: A from TMEM (columns 256..) instead of shared memory
+__global__ void k_mma_rate(int n, int ts, int n_mma, int rounds, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t base = (smem_u32(sm) + 1023) & ~1023u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t idesc = idesc_bf16(128, n, 0, 0);
+  long long t = 0;
+  if (warp == 0) {
+    const uint64_t da = smem_desc(base, 16, 1024, 2), db = smem_desc(base + 32768, 16, 1024, 2);
+    for (int rd = 0; rd < rounds; ++rd) {
+      const long long t0 = clock64();
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < n_mma; ++i) {
+          if (ts)
+            umma_bf16_ts(tmem, tmem + 256 + (i & 7) * 8, db, idesc, 1u);
+          else
+            umma_bf16(tmem, da, db, idesc, 1u);
+        }
+        umma_commit(&bar);
+      }
+      __syncwarp();
+      mbar_wait(&bar, rd & 1);
+      if (rd > 0) t += clock64() - t0;  // the first round warms up
+    }
+    if (threadIdx.x == 0) out[0] = t / (rounds - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+// cycles of `iters` x (two 32-column tcgen05.ld per warp) with `warps` warps (multiple of 4) per CTA
+extern "C" int tc_tmem_ld_rate(int ctas, int warps, int iters, long long* out, void* stream) {
+  k_tmem_ld_rate<<<ctas, 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(iters, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+// cycles per round of n_mma MMAs (M = 128, N = n, K = 16)
+extern "C" int tc_mma_rate(int n, int ts, int n_mma, int rounds, long long* out, void* stream) {
+  const int smem = 65536 + 1024;
+  cudaFuncSetAttribute(k_mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_mma_rate<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(n, ts, n_mma, rounds, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
