@@ -440,7 +440,7 @@ def gpt_train_step(dev, steps=5, warmup=3):
     return {"model": "RaceGPT 6 layers, d_model 768, 12 heads (d=64 heads on the tcgen05 kernels at their own width, q, k, v read in place from the projection)",
             "params_M": round(sum(p.numel() for p in model.parameters()) / 1e6, 1), "seq_len": cfg.seq_len,
             "batch": 1, "ms_per_step": round(ms, 3), "tokens_per_s": cfg.seq_len / (ms / 1e3),
-            "loss": float(loss), "data": "synthetic random tokens", "dtype": "bf16 autocast, fp32 master"}
+            "loss": float(loss), "data": "synthetic random tokens", "dtype": "bf16 autocast, fp32 master, cross-entropy on the bf16 logits (fp32 reductions)"}
 
 
 # ---------------------------------------------------------------------------

