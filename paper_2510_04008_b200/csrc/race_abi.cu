@@ -728,6 +728,29 @@ const float* group_w(const race::Geo& g, const float* w, int t0, int cnt, const 
   return ws.w;
 }
 
+// Table groups on the tcgen05 path keep each pass's own forward state (its carries and sketch rows, or its
+// tables) after the summed numerators / denominators, so the grouped backward skips each pass's
+// aggregation, projection and combine.  Layout: [num BH*N*dv | den BH*N | pad to 64 | pass 0 | pass 1 ...].
+bool saves_pass_states(const race::Geo& g, const GroupPlan& gp) {
+  if (gp.cb || !gp.grouped(g)) return false;
+  int t0, cnt;
+  const int64_t n = gp.count(g);
+  return race::tc_supported(group_geo(g, gp, 0, &t0, &cnt)) && race::tc_supported(group_geo(g, gp, n - 1, &t0, &cnt));
+}
+int64_t pass_state_elems(const race::Geo& gs) {
+  const int64_t e = gs.causal ? carry_elems(gs) + 16 * gs.BH * gs.N : gs.BH * table_elems(gs);
+  return (e + 63) & ~int64_t(63);
+}
+// offset (floats) of pass i's state in a grouped state buffer
+int64_t pass_state_offset(const race::Geo& g, const GroupPlan& gp, int64_t i) {
+  int64_t off = (g.BH * g.N * (g.dv + 1) + 63) & ~int64_t(63);
+  for (int64_t j = 0; j < i; ++j) {
+    int t0, cnt;
+    off += pass_state_elems(group_geo(g, gp, j, &t0, &cnt));
+  }
+  return off;
+}
+
 int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp, const void* q, const void* k,
                 const void* v, const float* w, void* o, float* den, float* state, void* workspace, void* stream,
                 bool final_out);
@@ -785,7 +808,7 @@ int race_state_elems(const race_desc_t* desc, int64_t* elems) {
   GroupPlan gp;
   if (int rc = group_plan(desc, &g, &gp)) return rc;
   if (gp.grouped(g)) {  // table / corner groups: the summed numerators [BH, N, dv] and denominators [BH, N]
-    *elems = g.BH * g.N * (g.dv + 1);
+    *elems = saves_pass_states(g, gp) ? pass_state_offset(g, gp, gp.count(g)) : g.BH * g.N * (g.dv + 1);
     return RACE_OK;
   }
   *elems = g.causal ? carry_elems(g) + 16 * g.BH * g.N : g.BH * table_elems(g);
@@ -1072,7 +1095,8 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     if (!gp.cb) {  // table group: a plain sub-problem (may run on the tcgen05 path)
       race_desc_t sd = *desc;
       sd.tables = cnt;
-      if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, nullptr, ws.sub, stream)) return rc;
+      float* pst = state && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
+      if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, pst, ws.sub, stream)) return rc;
     } else {  // corner group: the kernels restricted to the group's corners
       const WsLayout sub = ws_layout(gs, ws.sub);
       const bool fast = race::tc_supported(gs);
@@ -1178,7 +1202,20 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
     const WsLayout sub = ws_layout(gs, ws.sub);
     const cudaStream_t st = S(stream);
-    if (race::tc_supported(gs)) {  // tcgen05 kernels, query side on the whole estimator's 1/D, -rho/D
+    const float* pst = state && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
+    if (pst) {  // this pass's forward state (tables / carries and sketch rows) saved by the grouped forward
+      if (!g.causal) {
+        e = race::tc_bwd_q(gs, q, d_o, wg, pst, ws.dq, sub.dpart, st);
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.dpart, nullptr, sub.dtables, st);
+        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, ws.dv, st);
+      } else {
+        float* prow = const_cast<float*>(pst) + carry_elems(gs);
+        e = race::tc_bwd_causal_q(gs, q, k, v, d_o, wg, pst, prow, ws.dq, sub.rden, sub.gden, sub.dpart, st);
+        if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_SUFFIX, sub.dpart, nullptr, sub.dtables, st);
+        if (e == cudaSuccess)
+          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, prow, ws.dk, ws.dv, st);
+      }
+    } else if (race::tc_supported(gs)) {  // tcgen05 kernels, query side on the whole estimator's 1/D, -rho/D
       e = race::tc_aggregate(gs, k, v, wg, sub.part, nullptr, st);
       if (!g.causal) {
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);

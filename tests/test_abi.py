@@ -105,3 +105,17 @@ def test_bad_abi_version():
     d.abi_version = 99
     with pytest.raises(ValueError):
         _lib.segments(d)
+
+
+@pytest.mark.gpu  # the plan depends on the tcgen05 path being available (a driver entry point)
+@pytest.mark.parametrize("causal", [True, False])
+def test_table_group_state_keeps_pass_states(causal):
+    """bf16 table groups on the tcgen05 path: the grouped state is the summed numerators / denominators
+    (padded to 64 floats) followed by every pass's own forward state (carries + sketch rows, or
+    tables), which the grouped backward reuses instead of re-aggregating each pass."""
+    d = _desc(tables=4, causal=causal)  # F = 16: two passes of two tables
+    plan = _lib.group_plan(d)
+    assert plan["passes"] == 2 and plan["fast"] and plan["tables_per_pass"] == 2
+    one = _lib.state_elems(_desc(tables=2, causal=causal))  # one pass of two tables
+    head = ((4 * 131072 * 129 + 63) // 64) * 64
+    assert _lib.state_elems(d) == head + 2 * ((one + 63) // 64) * 64

@@ -329,3 +329,21 @@ def test_misaligned_views_match_aligned(sk, dtype):
         outs.append((o, den) + tuple(rb.race_backward(q, k, v, w, g, p, state=st)))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
+def test_table_group_backward_from_saved_pass_states(causal):
+    """The grouped backward that reuses each pass's saved forward state gives the same gradients, bit for
+    bit, as the state-less backward that re-aggregates every pass (P2L4: two tcgen05 passes)."""
+    dev = _cuda()
+    gen = torch.Generator(device=dev).manual_seed(12)
+    q, k, v, g = (torch.randn(1, 4, 5000, 128, generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
+    cfg = rb.SketchConfig(hyperplanes=2, tables=4, seed=8, causal=causal)
+    w = rb.head_hyperplanes(cfg, 4, 128).to(dev)
+    p = cfg.params()
+    o, den, st = rb.race_forward(q, k, v, w, p)
+    with_state = rb.race_backward(q, k, v, w, g, p, state=st)
+    without = rb.race_backward(q, k, v, w, g, p)
+    torch.cuda.synchronize()
+    for a, b in zip(with_state, without):
+        assert torch.equal(a, b)
