@@ -122,8 +122,8 @@ int race_workspace_bytes(const race_desc_t* desc, size_t* bytes);
  * grouped descs (race_group_plan passes > 1): the summed (unaveraged)
  *         numerators [BH, N, dv] then denominators [BH, N] of the whole
  *         estimator, from which race_bwd takes 1/D and -(dO.O)/D without
- *         re-running the grouped forward; for table groups on the tcgen05
- *         path (race_group_plan fast, corner_bits == P) these are padded to
+ *         re-running the grouped forward; for groups on the tcgen05 path
+ *         (race_group_plan fast) these are padded to
  *         64 floats and followed by every pass's own state (the layout
  *         above for that pass's tables), so race_bwd does not re-aggregate
  *         the passes either.                                              */

@@ -728,11 +728,11 @@ const float* group_w(const race::Geo& g, const float* w, int t0, int cnt, const 
   return ws.w;
 }
 
-// Table groups on the tcgen05 path keep each pass's own forward state (its carries and sketch rows, or its
-// tables) after the summed numerators / denominators, so the grouped backward skips each pass's
-// aggregation, projection and combine.  Layout: [num BH*N*dv | den BH*N | pad to 64 | pass 0 | pass 1 ...].
+// Table and corner groups on the tcgen05 path keep each pass's own forward state (its carries and sketch
+// rows, or its tables) after the summed numerators / denominators, so the grouped backward skips each
+// pass's aggregation, projection and combine.  Layout: [num BH*N*dv | den BH*N | pad to 64 | pass 0 | pass 1 ...].
 bool saves_pass_states(const race::Geo& g, const GroupPlan& gp) {
-  if (gp.cb || !gp.grouped(g)) return false;
+  if (!gp.grouped(g)) return false;
   int t0, cnt;
   const int64_t n = gp.count(g);
   return race::tc_supported(group_geo(g, gp, 0, &t0, &cnt)) && race::tc_supported(group_geo(g, gp, n - 1, &t0, &cnt));
@@ -1100,13 +1100,18 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     } else {  // corner group: the kernels restricted to the group's corners
       const WsLayout sub = ws_layout(gs, ws.sub);
       const bool fast = race::tc_supported(gs);
+      // tcgen05 passes with a grouped state: this pass's carries / tables and sketch rows go into it
+      float* pst = state && fast && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
+      float* tabs = pst ? pst : sub.tables;
+      float* prow = pst && g.causal ? pst + carry_elems(gs) : sub.rows;
+      const int pad = pst && g.causal ? int(carry_elems(gs) - gs.BH * gs.nseg * table_elems(gs)) : 0;
       e = fast ? race::tc_aggregate(gs, k, v, wg, sub.part, nullptr, st) : race::simt_aggregate(gs, k, v, wg, sub.part, st);
       if (e == cudaSuccess)
-        e = race::combine(gs, g.causal ? RACE_COMBINE_PREFIX : RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
+        e = race::combine(gs, g.causal ? RACE_COMBINE_PREFIX : RACE_COMBINE_TOTAL, sub.part, nullptr, tabs, st, pad);
       if (e == cudaSuccess) {
         if (fast)
-          e = g.causal ? race::tc_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, sub.rows, false, st)
-                       : race::tc_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
+          e = g.causal ? race::tc_causal_fwd(gs, q, k, v, wg, tabs, ws.o, ws.den, prow, false, st)
+                       : race::tc_readout(gs, q, wg, tabs, ws.o, ws.den, st);
         else
           e = g.causal ? race::simt_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, nullptr, st)
                        : race::simt_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);

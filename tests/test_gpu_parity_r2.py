@@ -332,13 +332,15 @@ def test_misaligned_views_match_aligned(sk, dtype):
 
 
 @pytest.mark.parametrize("causal", [False, True], ids=["noncausal", "causal"])
-def test_table_group_backward_from_saved_pass_states(causal):
+@pytest.mark.parametrize("pl", [(2, 4), (4, 2)], ids=["P2L4_tables", "P4L2_corners"])
+def test_table_group_backward_from_saved_pass_states(causal, pl):
     """The grouped backward that reuses each pass's saved forward state gives the same gradients, bit for
-    bit, as the state-less backward that re-aggregates every pass (P2L4: two tcgen05 passes)."""
+    bit, as the state-less backward that re-aggregates every pass (tcgen05 table groups and corner
+    groups)."""
     dev = _cuda()
     gen = torch.Generator(device=dev).manual_seed(12)
     q, k, v, g = (torch.randn(1, 4, 5000, 128, generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
-    cfg = rb.SketchConfig(hyperplanes=2, tables=4, seed=8, causal=causal)
+    cfg = rb.SketchConfig(hyperplanes=pl[0], tables=pl[1], seed=8, causal=causal)
     w = rb.head_hyperplanes(cfg, 4, 128).to(dev)
     p = cfg.params()
     o, den, st = rb.race_forward(q, k, v, w, p)
