@@ -1142,9 +1142,12 @@ cudaError_t combine(const Geo& g, int mode, const float* part, const float* carr
   cudaLaunchAttribute attr[1];  // programmatic dependent launch (see tcfast::launch_nt)
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  const char* nopdl = getenv("RACE_NO_PDL");
+  static const bool pdl = [] {
+    const char* e = getenv("RACE_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
   cfg.attrs = attr;
-  cfg.numAttrs = (nopdl && nopdl[0] == '1') ? 0 : 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, simt::k_combine, g.BH, g.nseg, E, mode, part, carry, out, pad);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
