@@ -119,3 +119,34 @@ def test_table_group_state_keeps_pass_states(causal):
     one = _lib.state_elems(_desc(tables=2, causal=causal))  # one pass of two tables
     head = ((4 * 131072 * 129 + 63) // 64) * 64
     assert _lib.state_elems(d) == head + 2 * ((one + 63) // 64) * 64
+
+
+def _busiest_cta_chunks(bh, n, nseg, seg, grid=148):
+    """Chunks (128 tokens) of the busiest CTA when `bh * nseg` items are split evenly by count over the
+    persistent grid (cta_range in tc_fast.cuh)."""
+    items = bh * nseg
+    g = min(items, grid)
+    cps = -(-n // 128)
+    load = 0
+    for b in range(g):
+        tot = 0
+        for i in range(b * items // g, (b + 1) * items // g):
+            s = i % nseg
+            tot += seg // 128 if s + 1 < nseg else cps - s * (seg // 128)
+        load = max(load, tot)
+    return load
+
+
+@pytest.mark.parametrize("bh,n", [(4, 131072), (12, 16384), (1, 131072), (8, 65536), (4, 20971520), (3, 5000)])
+def test_fast_segmentation_balances_the_persistent_grid(bh, n):
+    """The tcgen05 path's segment length (fast_segment in race_abi.cu): the busiest CTA gets no more
+    128-token chunks than under the old fixed ~8-segments-per-CTA policy, with no more segments."""
+    d = _desc(batch_heads=bh, heads=bh, n=n)
+    nseg, seg = _lib.segments(d)
+    target = -(-(148 * 8) // bh)
+    old_seg = max(128, -(-(-(-n // target)) // 128) * 128)
+    old_nseg = -(-n // old_seg)
+    assert _busiest_cta_chunks(bh, n, nseg, seg) <= _busiest_cta_chunks(bh, n, old_nseg, old_seg)
+    assert nseg <= old_nseg
+    if (bh, n) == (4, 131072):  # the headline: one 28-chunk segment per CTA
+        assert (nseg, seg) == (37, 3584)
