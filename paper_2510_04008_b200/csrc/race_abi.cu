@@ -356,6 +356,7 @@ struct GroupWs {
   float* dv_acc;
   float* dproj_q;   // [BH*N, T*P] summed dproj of the query / key side (tcgen05 groups)
   float* dproj_k;
+  void* dv_pass;    // [passes, BH, N, dv] each tcgen05 pass's dV (dtype), summed once at the end
   size_t bytes;
 };
 
@@ -385,6 +386,7 @@ GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
   w.dv_acc = static_cast<float*>(take(sizeof(float) * tok * g.dv));
   w.dproj_q = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
   w.dproj_k = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
+  w.dv_pass = take(e * tok * g.dv * size_t(gp.count(g)));
   w.bytes = off;
   return w;
 }
@@ -580,6 +582,29 @@ __global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int mode, f
     const float v = to_f32(x[i]) + (mode ? acc[i] : 0.f);
     if (mode == 2) out[i] = from_f32<T>(v);
     else acc[i] = v;
+  }
+}
+
+// dV of the grouped tcgen05 backward: the passes' dV (dtype) summed in pass order in fp32 and cast once --
+// the same additions, in the same order, as accumulating pass by pass (k_group_grad_acc modes 0, 1, 2),
+// with one read of each pass's dV instead of a read-modify-write of an fp32 sum per pass
+template <typename T>
+__global__ void k_group_sum_passes(int64_t n, int passes, const T* __restrict__ x, T* __restrict__ out) {
+  const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i0 >= n) return;
+  if (i0 + 4 <= n) {
+    float4 acc = ld4(x + i0);
+    for (int p = 1; p < passes; ++p) {
+      const float4 v = ld4(x + int64_t(p) * n + i0);
+      acc = make_float4(v.x + acc.x, v.y + acc.y, v.z + acc.z, v.w + acc.w);
+    }
+    st4(out + i0, acc);
+    return;
+  }
+  for (int64_t i = i0; i < n; ++i) {
+    float acc = to_f32(x[i]);
+    for (int p = 1; p < passes; ++p) acc = to_f32(x[int64_t(p) * n + i]) + acc;
+    out[i] = from_f32<T>(acc);
   }
 }
 
@@ -1185,7 +1210,8 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
                           size_t(g.w_per_head ? g.H : 1) * tp_all * g.d * sizeof(float) <= 160 * 1024 &&
                           tp_all <= 32 && g.d % 4 == 0 && g.d <= 256 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(dq) & 15) == 0 &&
-                          (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+                          (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   if (dproj_mode && gp.cb) {  // corner groups add into their table's columns
     e = cudaMemsetAsync(ws.dproj_q, 0, sizeof(float) * rows * tp_all, S(stream));
     if (e == cudaSuccess) e = cudaMemsetAsync(ws.dproj_k, 0, sizeof(float) * rows * tp_all, S(stream));
@@ -1207,18 +1233,21 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
     const WsLayout sub = ws_layout(gs, ws.sub);
     const cudaStream_t st = S(stream);
+    // tcgen05 passes keep their own dV; one kernel sums them at the end
+    void* dvp = dproj_mode ? static_cast<char*>(ws.dv_pass) + size_t(i) * rows * g.dv * (g.dtype == RACE_BF16 ? 2 : 4)
+                           : ws.dv;
     const float* pst = state && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
     if (pst) {  // this pass's forward state (tables / carries and sketch rows) saved by the grouped forward
       if (!g.causal) {
         e = race::tc_bwd_q(gs, q, d_o, wg, pst, ws.dq, sub.dpart, st);
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.dpart, nullptr, sub.dtables, st);
-        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, ws.dv, st);
+        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, dvp, st);
       } else {
         float* prow = const_cast<float*>(pst) + carry_elems(gs);
         e = race::tc_bwd_causal_q(gs, q, k, v, d_o, wg, pst, prow, ws.dq, sub.rden, sub.gden, sub.dpart, st);
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_SUFFIX, sub.dpart, nullptr, sub.dtables, st);
         if (e == cudaSuccess)
-          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, prow, ws.dk, ws.dv, st);
+          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, prow, ws.dk, dvp, st);
       }
     } else if (race::tc_supported(gs)) {  // tcgen05 kernels, query side on the whole estimator's 1/D, -rho/D
       e = race::tc_aggregate(gs, k, v, wg, sub.part, nullptr, st);
@@ -1226,7 +1255,7 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.part, nullptr, sub.tables, st);
         if (e == cudaSuccess) e = race::tc_bwd_q(gs, q, d_o, wg, sub.tables, ws.dq, sub.dpart, st);
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_TOTAL, sub.dpart, nullptr, sub.dtables, st);
-        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, ws.dv, st);
+        if (e == cudaSuccess) e = race::tc_bwd_k(gs, k, v, wg, sub.dtables, ws.dk, dvp, st);
       } else {
         if (e == cudaSuccess) e = race::tc_project(gs, q, k, wg, sub.rows, st);
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_PREFIX, sub.part, nullptr, sub.tables, st);
@@ -1235,7 +1264,7 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
                                     st);
         if (e == cudaSuccess) e = race::combine(gs, RACE_COMBINE_SUFFIX, sub.dpart, nullptr, sub.dtables, st);
         if (e == cudaSuccess)
-          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, sub.rows, ws.dk, ws.dv, st);
+          e = race::tc_bwd_causal_k(gs, q, k, v, d_o, wg, ws.rden, ws.gden, sub.dtables, sub.rows, ws.dk, dvp, st);
       }
     } else {
     e = race::simt_aggregate(gs, k, v, wg, sub.part, st);
@@ -1267,15 +1296,26 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
           k_group_grad_acc<T, false><<<blocks_for(n), 256, 0, st>>>(n, static_cast<const T*>(x), mode, a,
                                                                     static_cast<T*>(out));
       };
-      if (!dproj_mode) {
-        acc(rows * g.d, ws.dq, ws.dq_acc, dq);
-        acc(rows * g.d, ws.dk, ws.dk_acc, dk);
-      }
+      if (dproj_mode) return cudaSuccess;  // dq, dk from the summed dproj, dV from the pass buffers (below)
+      acc(rows * g.d, ws.dq, ws.dq_acc, dq);
+      acc(rows * g.d, ws.dk, ws.dk_acc, dk);
       acc(rows * g.dv, ws.dv, ws.dv_acc, dv);
-      race::note_launch(dproj_mode ? 1 : 3);
+      race::note_launch(3);
       return cudaGetLastError();
     });
     if (int rc = cuda_status(e, "table group gradient sum")) return rc;
+  }
+  if (dproj_mode) {
+    e = by_dtype(g.dtype, [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      const int64_t n = rows * g.dv;
+      k_group_sum_passes<T><<<blocks_for((n + 3) / 4), 256, 0, S(stream)>>>(n, int(ngroups),
+                                                                           static_cast<const T*>(ws.dv_pass),
+                                                                           static_cast<T*>(dv));
+      race::note_launch();
+      return cudaGetLastError();
+    });
+    if (int rc = cuda_status(e, "dv from the passes")) return rc;
   }
   if (!dproj_mode) return RACE_OK;  // the last group's accumulation wrote dq, dk, dv
   e = by_dtype(g.dtype, [&](auto* tag) {
