@@ -360,6 +360,8 @@ struct GroupWs {
   size_t bytes;
 };
 
+constexpr int64_t kMaxPassBuffers = 16;
+
 GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
   int t0, tg;
   const race::Geo s = group_geo(g, gp, 0, &t0, &tg);
@@ -386,7 +388,9 @@ GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
   w.dv_acc = static_cast<float*>(take(sizeof(float) * tok * g.dv));
   w.dproj_q = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
   w.dproj_k = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
-  w.dv_pass = take(e * tok * g.dv * size_t(gp.count(g)));
+  // per-pass dV buffers only for a few tcgen05 passes (P = 20 corner groups would be 2^17 passes)
+  w.dv_pass = gp.count(g) <= kMaxPassBuffers && race::tc_supported(s) ? take(e * tok * g.dv * size_t(gp.count(g)))
+                                                                      : nullptr;
   w.bytes = off;
   return w;
 }
@@ -1212,6 +1216,8 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
                           (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(dq) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  // each tcgen05 pass keeps its own dV and k_group_sum_passes adds them once at the end
+  const bool pass_dv = dproj_mode && ws.dv_pass != nullptr;
   if (dproj_mode && gp.cb) {  // corner groups add into their table's columns
     e = cudaMemsetAsync(ws.dproj_q, 0, sizeof(float) * rows * tp_all, S(stream));
     if (e == cudaSuccess) e = cudaMemsetAsync(ws.dproj_k, 0, sizeof(float) * rows * tp_all, S(stream));
@@ -1234,8 +1240,8 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     const WsLayout sub = ws_layout(gs, ws.sub);
     const cudaStream_t st = S(stream);
     // tcgen05 passes keep their own dV; one kernel sums them at the end
-    void* dvp = dproj_mode ? static_cast<char*>(ws.dv_pass) + size_t(i) * rows * g.dv * (g.dtype == RACE_BF16 ? 2 : 4)
-                           : ws.dv;
+    void* dvp = pass_dv ? static_cast<char*>(ws.dv_pass) + size_t(i) * rows * g.dv * (g.dtype == RACE_BF16 ? 2 : 4)
+                        : ws.dv;
     const float* pst = state && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
     if (pst) {  // this pass's forward state (tables / carries and sketch rows) saved by the grouped forward
       if (!g.causal) {
@@ -1296,16 +1302,17 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
           k_group_grad_acc<T, false><<<blocks_for(n), 256, 0, st>>>(n, static_cast<const T*>(x), mode, a,
                                                                     static_cast<T*>(out));
       };
-      if (dproj_mode) return cudaSuccess;  // dq, dk from the summed dproj, dV from the pass buffers (below)
-      acc(rows * g.d, ws.dq, ws.dq_acc, dq);
-      acc(rows * g.d, ws.dk, ws.dk_acc, dk);
-      acc(rows * g.dv, ws.dv, ws.dv_acc, dv);
-      race::note_launch(3);
+      if (!dproj_mode) {  // (dproj mode: dq, dk from the summed dproj at the end)
+        acc(rows * g.d, ws.dq, ws.dq_acc, dq);
+        acc(rows * g.d, ws.dk, ws.dk_acc, dk);
+      }
+      if (!pass_dv) acc(rows * g.dv, ws.dv, ws.dv_acc, dv);  // (else: the pass buffers, summed below)
+      race::note_launch((dproj_mode ? 0 : 2) + (pass_dv ? 0 : 1));
       return cudaGetLastError();
     });
     if (int rc = cuda_status(e, "table group gradient sum")) return rc;
   }
-  if (dproj_mode) {
+  if (pass_dv) {
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
       const int64_t n = rows * g.dv;
