@@ -356,7 +356,8 @@ struct GroupWs {
   float* dv_acc;
   float* dproj_q;   // [BH*N, T*P] summed dproj of the query / key side (tcgen05 groups)
   float* dproj_k;
-  void* dv_pass;    // [passes, BH, N, dv] each tcgen05 pass's dV (dtype), summed once at the end
+  void* dv_pass;    // [passes, BH, N, dv] each tcgen05 pass's dV (backward) or O (forward), summed once
+  float* den_pass;  // [passes, BH, N] each tcgen05 pass's den (forward)
   size_t bytes;
 };
 
@@ -389,8 +390,9 @@ GroupWs group_ws(const race::Geo& g, const GroupPlan& gp, void* base) {
   w.dproj_q = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
   w.dproj_k = static_cast<float*>(take(sizeof(float) * tok * g.T * g.P));
   // per-pass dV buffers only for a few tcgen05 passes (P = 20 corner groups would be 2^17 passes)
-  w.dv_pass = gp.count(g) <= kMaxPassBuffers && race::tc_supported(s) ? take(e * tok * g.dv * size_t(gp.count(g)))
-                                                                      : nullptr;
+  const bool passbuf = gp.count(g) <= kMaxPassBuffers && race::tc_supported(s);
+  w.dv_pass = passbuf ? take(e * tok * g.dv * size_t(gp.count(g))) : nullptr;
+  w.den_pass = passbuf ? static_cast<float*>(take(sizeof(float) * tok * size_t(gp.count(g)))) : nullptr;
   w.bytes = off;
   return w;
 }
@@ -586,6 +588,44 @@ __global__ void k_group_grad_acc(int64_t n, const T* __restrict__ x, int mode, f
     const float v = to_f32(x[i]) + (mode ? acc[i] : 0.f);
     if (mode == 2) out[i] = from_f32<T>(v);
     else acc[i] = v;
+  }
+}
+
+// Grouped tcgen05 forward: every pass keeps its O (dtype) and den; this one pass forms the whole estimator's
+// numerator num = sum_i O_i D_i (fma chain in pass order, D_i = den_i * tables_i) and denominator
+// d = sum_i D_i -- the same fp32 operations, in the same order, as k_group_fwd_acc pass by pass -- writes
+// them (the grouped state) and, for the final output, O = num / d and den = d / T as k_group_fwd_out.
+// One warp per kAccRows rows, dv <= 128, 4 columns per lane.
+template <typename T>
+__global__ void k_group_fwd_final(int64_t rows, int dv, int passes, const T* __restrict__ o_pass,
+                                  const float* __restrict__ den_pass, float tg_first, float tg_last, float T_,
+                                  float* __restrict__ num_acc, float* __restrict__ d_acc, T* __restrict__ o,
+                                  float* __restrict__ den) {
+  const int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kAccRows;
+  const int lane = threadIdx.x & 31;
+  if (r0 >= rows) return;
+  const int c = 4 * lane;
+#pragma unroll
+  for (int q = 0; q < kAccRows; ++q) {
+    const int64_t r = r0 + q;
+    if (r >= rows) break;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float dsum = 0.f;
+    for (int i = 0; i < passes; ++i) {
+      const float D = den_pass[int64_t(i) * rows + r] * (i + 1 == passes ? tg_last : tg_first);
+      dsum = i == 0 ? D : dsum + D;
+      if (c < dv) {
+        const float4 x = ld4(o_pass + (int64_t(i) * rows + r) * dv + c);
+        acc = make_float4(fmaf(x.x, D, acc.x), fmaf(x.y, D, acc.y), fmaf(x.z, D, acc.z), fmaf(x.w, D, acc.w));
+      }
+    }
+    if (c < dv) st4(num_acc + r * dv + c, acc);
+    if (lane == 0) d_acc[r] = dsum;
+    if (o) {
+      const float rD = dsum / T_ > race::kDegenerateDenEps ? 1.f / dsum : 0.f;
+      if (c < dv) st4(o + r * dv + c, make_float4(acc.x * rD, acc.y * rD, acc.z * rD, acc.w * rD));
+      if (lane == 0) den[r] = dsum / T_;
+    }
   }
 }
 
@@ -1115,9 +1155,19 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
   const int64_t rows = g.BH * g.N;
   const int64_t ngroups = gp.count(g);
   const cudaStream_t st = S(stream);
+  // tcgen05 passes keep their own O and den; k_group_fwd_final sums them once (else: per-pass accumulation)
+  const size_t esz = g.dtype == RACE_BF16 ? 2 : 4;
+  const bool pass_o = ws.dv_pass && ws.den_pass && g.dv % 4 == 0 && g.dv <= 128 &&
+                      (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0 &&
+                      (!final_out || (reinterpret_cast<uintptr_t>(o) % (4 * esz)) == 0);
+  int tg_first = 1, tg_last = 1;
   for (int64_t i = 0; i < ngroups; ++i) {
     int t0, cnt;
     const race::Geo gs = group_geo(g, gp, i, &t0, &cnt);
+    if (i == 0) tg_first = cnt;
+    if (i + 1 == ngroups) tg_last = cnt;
+    void* oi = pass_o ? static_cast<char*>(ws.dv_pass) + size_t(i) * rows * g.dv * esz : ws.o;
+    float* deni = pass_o ? ws.den_pass + size_t(i) * rows : ws.den;
     cudaError_t e = cudaSuccess;
     const float* wg = group_w(g, w, t0, cnt, ws, st, &e);
     if (int rc = cuda_status(e, "table group hyperplanes")) return rc;
@@ -1125,7 +1175,7 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
       race_desc_t sd = *desc;
       sd.tables = cnt;
       float* pst = state && saves_pass_states(g, gp) ? state + pass_state_offset(g, gp, i) : nullptr;
-      if (int rc = race_fwd(&sd, q, k, v, wg, ws.o, ws.den, pst, ws.sub, stream)) return rc;
+      if (int rc = race_fwd(&sd, q, k, v, wg, oi, deni, pst, ws.sub, stream)) return rc;
     } else {  // corner group: the kernels restricted to the group's corners
       const WsLayout sub = ws_layout(gs, ws.sub);
       const bool fast = race::tc_supported(gs);
@@ -1139,14 +1189,15 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
         e = race::combine(gs, g.causal ? RACE_COMBINE_PREFIX : RACE_COMBINE_TOTAL, sub.part, nullptr, tabs, st, pad);
       if (e == cudaSuccess) {
         if (fast)
-          e = g.causal ? race::tc_causal_fwd(gs, q, k, v, wg, tabs, ws.o, ws.den, prow, false, st)
-                       : race::tc_readout(gs, q, wg, tabs, ws.o, ws.den, st);
+          e = g.causal ? race::tc_causal_fwd(gs, q, k, v, wg, tabs, oi, deni, prow, false, st)
+                       : race::tc_readout(gs, q, wg, tabs, oi, deni, st);
         else
           e = g.causal ? race::simt_causal_fwd(gs, q, k, v, wg, sub.tables, ws.o, ws.den, nullptr, st)
                        : race::simt_readout(gs, q, wg, sub.tables, ws.o, ws.den, st);
       }
       if (int rc = cuda_status(e, "corner group forward")) return rc;
     }
+    if (pass_o) continue;
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
       if (g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0)
@@ -1159,6 +1210,17 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
       return cudaGetLastError();
     });
     if (int rc = cuda_status(e, "table group sum")) return rc;
+  }
+  if (pass_o) {
+    cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      k_group_fwd_final<T><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
+          rows, g.dv, int(ngroups), static_cast<const T*>(ws.dv_pass), ws.den_pass, float(tg_first), float(tg_last),
+          float(g.T), ws.num_acc, ws.d_acc, final_out ? static_cast<T*>(o) : nullptr, final_out ? den : nullptr);
+      race::note_launch();
+      return cudaGetLastError();
+    });
+    return cuda_status(e, "table group sum and output");
   }
   if (!final_out) return RACE_OK;
   cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
