@@ -17,5 +17,14 @@ for causal in (True, False):
     w64 = rb.head_hyperplanes(cfg, 2, 64).to(dev)
     o, den, st = rb.race_forward(qs, ks, vs, w64, cfg.params())
     rb.race_backward(qs, ks, vs, w64, o, cfg.params(), state=st)
+# grouped tcgen05 passes (table groups and corner groups) with their pass buffers and pass states
+for P, L in ((2, 4), (4, 2)):
+    for causal in (True, False):
+        cfg = rb.SketchConfig(hyperplanes=P, tables=L, seed=0, causal=causal)
+        w = rb.head_hyperplanes(cfg, 2, 128).to(dev)
+        q, k, v, g = (torch.randn(1, 2, 1500, 128, device=dev).to(torch.bfloat16) for _ in range(4))
+        o, den, st = rb.race_forward(q, k, v, w, cfg.params())
+        rb.race_backward(q, k, v, w, g, cfg.params(), state=st)
+        rb.race_backward(q, k, v, w, g, cfg.params())
 torch.cuda.synchronize()
 print("ok")
