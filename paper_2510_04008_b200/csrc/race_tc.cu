@@ -282,8 +282,8 @@ constexpr int OFF_STAGE = 0;
 constexpr int OFF_W = STAGES * STAGE_BYTES;
 constexpr int OFF_PHI = OFF_W + WOP;  // 2 buffers
 constexpr int OFF_SOP = OFF_PHI + 2 * PHI;
-constexpr int OFF_X = OFF_SOP + PHI;  // [2 parity][2 halves][128] row-norm partials
-constexpr int OFF_BAR = OFF_X + 2 * 256 * 4;
+constexpr int OFF_X = OFF_SOP + PHI;  // [2 parity][2 halves][128] row-norm partials, then [2 parity][128] D
+constexpr int OFF_BAR = OFF_X + 2 * 256 * 4 + 2 * 128 * 4;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "k_readout8 shared memory");
 constexpr uint32_t TM_NUM_R = 128;
@@ -435,18 +435,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const float inv = inv_scale(xp[r] + xp[128 + r], a.normalize);
       mbar_wait(proj_full, g & 1);
       tc_fence_after();
-      float proj[16];
-      tmem_ld16(tmem + lb + TM_PROJQ, proj);
-      tmem_ld_wait();
       const bool valid = c.t + r < m.t1;
-      float phi[FP];
-      row_features<P, HB>(a, proj, inv, valid, phi);
       float D = 0.f;
+      if (h == 0) {  // phi_q and D once, by the first half (the second half takes D in back())
+        float proj[16];
+        tmem_ld16(tmem + lb + TM_PROJQ, proj);
+        tmem_ld_wait();
+        float phi[FP];
+        row_features<P, HB>(a, proj, inv, valid, phi);
 #pragma unroll
-      for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
-      if (g >= 2) mbar_wait(&phi_empty[g & 1], ((g >> 1) - 1) & 1);
-      if (h == 0) write_phi_q(sb + OFF_PHI + (g & 1) * PHI, r, phi);
-      fence_proxy_async();
+        for (int f = 0; f < FP; ++f) D = fmaf(phi[f], A[f], D);
+        xsq[512 + (g & 1) * 128 + r] = D;
+        if (g >= 2) mbar_wait(&phi_empty[g & 1], ((g >> 1) - 1) & 1);
+        write_phi_q(sb + OFF_PHI + (g & 1) * PHI, r, phi);
+        fence_proxy_async();
+      }
       tc_fence_before();
       mbar_arrive(phi_full);
       if (h == 0 && valid) a.den[m.bh * a.N + c.t + r] = D * invT;
@@ -456,6 +459,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       const int s = g % STAGES;
       uint8_t* stage = smem + OFF_STAGE + s * STAGE_BYTES;
       mbar_wait(&num_full[g & 1], (g >> 1) & 1);
+      if (h == 1) {  // D of this chunk from the first half (written before its phi_full arrival)
+        const float D = xsq[512 + (g & 1) * 128 + r];
+        rD = (D * invT > kDegenerateDenEps) ? 1.f / D : 0.f;
+      }
       tc_fence_after();
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
