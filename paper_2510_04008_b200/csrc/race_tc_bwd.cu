@@ -69,8 +69,9 @@ using bq::OFF_W2;
 using bq::OFF_SOPT;
 using bq::OFF_PHIT;
 using bq::OFF_DPROJ;
-constexpr int OFF_X = bq::OFF_BAR;  // [2 parity][2 halves][128] norm partials, then da[4][8]
-constexpr int OFF_BAR = OFF_X + (2 * 256 + 32) * 4;
+constexpr int OFF_X = bq::OFF_BAR;  // [2 parity][2 halves][128] norm partials, da[4][8], [2 parity][128] dx^.x^
+constexpr int XDOT = 2 * 256 + 32;
+constexpr int OFF_BAR = OFF_X + (XDOT + 2 * 128) * 4;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 constexpr uint32_t TM_P = 0, TM_Y = 16, TM_DS = 32, TM_DX = 128;  // DS: two accumulators at 32 and 64
 }  // namespace bq8n
@@ -263,12 +264,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
           rD = pre.rd;
           rho = rD != 0.f ? -pre.gd / rD : 0.f;
         }
-        float dphi[FP];
-#pragma unroll
-        for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
-        float dproj[8];
-        row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
-        if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
+        float* xdot = reinterpret_cast<float*>(smem + OFF_X) + XDOT + (gc & 1) * 128;
         if (h == 0) {
           float phit[FP];
 #pragma unroll
@@ -277,7 +273,14 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
             dA[f] = fmaf(phi[f], -rho * rD, dA[f]);
           }
           write_phi_k(sb + OFF_PHIT, r, phit);  // [hi | hi | lo | 0]: MN-major B of dS += dO^T Phi~
-        } else {
+        } else {  // the feature VJP once, by the second half; dx^.x^ for both halves' tangent step
+          float dphi[FP];
+#pragma unroll
+          for (int f = 0; f < FP; ++f) dphi[f] = (y[f] - rho * A[f]) * rD;
+          float dproj[8];
+          row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
+          if (GRP && a.dproj_out && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
+          xdot[r] = dot_from_proj(dproj, ph);
           write_dproj(sb + OFF_DPROJ, r, dproj);
         }
         fence_proxy_async();
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         mbar_arrive(ready);
         mbar_wait(c2, gc & 1);
         tc_fence_after();
-        tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, dot_from_proj(dproj, ph));
+        tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, xdot[r]);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&dqstaged[s]);
@@ -333,8 +336,9 @@ using bk::OFF_DSOPT;
 using bk::OFF_DSOP;
 using bk::OFF_PHIK;
 using bk::OFF_DPROJ;
-constexpr int OFF_X = bk::OFF_BAR;  // [2 parity][2 halves][128] norm partials
-constexpr int OFF_BAR = OFF_X + 2 * 256 * 4;
+constexpr int OFF_X = bk::OFF_BAR;  // [2 parity][2 halves][128] norm partials, then [2 parity][128] dx^.x^
+constexpr int XDOT = 2 * 256;
+constexpr int OFF_BAR = OFF_X + (XDOT + 2 * 128) * 4;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 using bk::TM_P;
 using bk::TM_Z;
@@ -503,15 +507,21 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
       tmem_ld16(tmem + lb + TM_P, proj);
       tmem_ld16(tmem + lb + TM_Z, zv);
       tmem_ld_wait();
-      float phi[FP], u[5], ph[5], dphi[FP];
+      float phi[FP], u[5], ph[5];
       row_features_u<P, HB>(a, proj, sc.inv, valid, phi, u, ph);
+      float* xdot = reinterpret_cast<float*>(smem + OFF_X) + XDOT + (gc & 1) * 128;
+      if (h == 0) {
+        write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
+      } else {  // the feature VJP once, by the second half; dx^.x^ for both halves' tangent step
+        float dphi[FP];
 #pragma unroll
-      for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
-      float dproj[8];
-      row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
-      if (GRP && a.dproj_out && h == 0 && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
-      if (h == 0) write_phi_q(sb + OFF_PHIK, r, phi);  // [hi | lo | hi | 0] pairs with dS-op [hi | hi | lo | 0]
-      else write_dproj(sb + OFF_DPROJ, r, dproj);
+        for (int f = 0; f < FP; ++f) dphi[f] = zv[f] + zv[8 + f] + dA[f];
+        float dproj[8];
+        row_feature_vjp<P, HB>(a, u, phi, dphi, dproj);
+        if (GRP && a.dproj_out && valid) emit_dproj(a, m.bh * a.N + t + r, dproj, pre);
+        xdot[r] = dot_from_proj(dproj, ph);
+        write_dproj(sb + OFF_DPROJ, r, dproj);
+      }
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(ready);
@@ -525,7 +535,7 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         tmem_ld_wait();
         stage32_p(stage + TILE, r, v, c0);
       }
-      tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, dot_from_proj(dproj, ph));
+      tangent_half_inplace(tmem + lb + TM_DX, stage, r, h, sc, xdot[r]);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&staged[s]);
