@@ -781,6 +781,7 @@ __global__ void __launch_bounds__(256, 3) k_dx_from_dproj(int64_t rows, int64_t 
 }
 
 unsigned blocks_for(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+inline unsigned acc_blocks(int64_t rows) { return blocks_for((rows + kAccRows - 1) / kAccRows * 32); }
 
 template <typename F>
 cudaError_t by_dtype(int dtype, F&& f) {
@@ -1201,10 +1202,10 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
       if (g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0)
-        k_group_fwd_acc<T, true><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
+        k_group_fwd_acc<T, true><<<acc_blocks(rows), 256, 0, st>>>(
             rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       else
-        k_group_fwd_acc<T, false><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
+        k_group_fwd_acc<T, false><<<acc_blocks(rows), 256, 0, st>>>(
             rows, g.dv, static_cast<const T*>(ws.o), ws.den, float(cnt), i == 0, ws.num_acc, ws.d_acc);
       race::note_launch();
       return cudaGetLastError();
@@ -1214,7 +1215,7 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
   if (pass_o) {
     cudaError_t e = by_dtype(g.dtype, [&](auto* tag) {
       using T = std::remove_pointer_t<decltype(tag)>;
-      k_group_fwd_final<T><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, st>>>(
+      k_group_fwd_final<T><<<acc_blocks(rows), 256, 0, st>>>(
           rows, g.dv, int(ngroups), static_cast<const T*>(ws.dv_pass), ws.den_pass, float(tg_first), float(tg_last),
           float(g.T), ws.num_acc, ws.d_acc, final_out ? static_cast<T*>(o) : nullptr, final_out ? den : nullptr);
       race::note_launch();
@@ -1228,10 +1229,10 @@ int fwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     const bool vec = g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(T))) == 0 &&
                      (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0;
     if (vec)
-      k_group_fwd_out<T, true><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+      k_group_fwd_out<T, true><<<acc_blocks(rows), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
                                                                             float(g.T), static_cast<T*>(o), den);
     else
-      k_group_fwd_out<T, false><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
+      k_group_fwd_out<T, false><<<acc_blocks(rows), 256, 0, S(stream)>>>(rows, g.dv, ws.num_acc, ws.d_acc,
                                                                              float(g.T), static_cast<T*>(o), den);
     race::note_launch();
     return cudaGetLastError();
@@ -1259,7 +1260,7 @@ int bwd_grouped(const race_desc_t* desc, const race::Geo& g, const GroupPlan& gp
     using T = std::remove_pointer_t<decltype(tag)>;
     const int vec = g.dv % 4 == 0 && (reinterpret_cast<uintptr_t>(d_o) % 16) == 0 &&
                     (reinterpret_cast<uintptr_t>(ws.num_acc) % 16) == 0;
-    k_group_rg<T><<<blocks_for((rows + kAccRows - 1) / kAccRows * 32), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
+    k_group_rg<T><<<acc_blocks(rows), 256, 0, S(stream)>>>(g.BH, g.N, g.dv, ws.num_acc, ws.d_acc,
                                                                 static_cast<const T*>(d_o), float(g.T), ws.rden,
                                                                 ws.gden,
                                                                 vec);

@@ -1192,7 +1192,8 @@ cudaError_t tc_causal_fwd(const Geo& g, const void* q, const void* k, const void
                           const float* car, void* o, float* den, float* nrm, bool krows, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mo, mr;
-  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mo, o, g, g.dv, L_O))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) ||
+      !make_map(&mo, o, g, g.dv, L_O))
     return cudaErrorInvalidValue;
   if (krows && (!nrm || !make_map_rows(&mr, nrm, g.BH * g.N))) return cudaErrorInvalidValue;
   if (!krows) mr = mq;  // unused

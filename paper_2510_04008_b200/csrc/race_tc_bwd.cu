@@ -553,7 +553,8 @@ cudaError_t tc_bwd_q(const Geo& g, const void* q, const void* d_o, const float* 
                      float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mdo, mdq;
-  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mdo, d_o, g, g.dv, L_DO) || !make_map(&mdq, dq, g, g.d, L_DQ)) return cudaErrorInvalidValue;
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mdo, d_o, g, g.dv, L_DO) || !make_map(&mdq, dq, g, g.d, L_DQ))
+    return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
   a.tin = tab;
@@ -577,7 +578,8 @@ cudaError_t tc_bwd_k(const Geo& g, const void* k, const void* v, const float* w,
                      void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mk, mv, mdk, mdv;
-  if (!make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdk, dk, g, g.d, L_DK) || !make_map(&mdv, dv, g, g.dv, L_DV))
+  if (!make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdk, dk, g, g.d, L_DK) ||
+      !make_map(&mdv, dv, g, g.dv, L_DV))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;

@@ -1072,8 +1072,8 @@ cudaError_t tc_bwd_causal_q(const Geo& g, const void* q, const void* k, const vo
                             float* dpart, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdq;
-  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdo, d_o, g, g.dv, L_DO) ||
-      !make_map(&mdq, dq, g, g.d, L_DQ))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) ||
+      !make_map(&mdo, d_o, g, g.dv, L_DO) || !make_map(&mdq, dq, g, g.d, L_DQ))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
@@ -1107,8 +1107,8 @@ cudaError_t tc_bwd_causal_k(const Geo& g, const void* q, const void* k, const vo
                             const float* nrm, void* dk, void* dv, cudaStream_t st) {
   using namespace tcfast;
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
-  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) || !make_map(&mdo, d_o, g, g.dv, L_DO) ||
-      !make_map(&mdk, dk, g, g.d, L_DK) || !make_map(&mdv, dv, g, g.dv, L_DV))
+  if (!make_map(&mq, q, g, g.d, L_Q) || !make_map(&mk, k, g, g.d, L_K) || !make_map(&mv, v, g, g.dv, L_V) ||
+      !make_map(&mdo, d_o, g, g.dv, L_DO) || !make_map(&mdk, dk, g, g.d, L_DK) || !make_map(&mdv, dv, g, g.dv, L_DV))
     return cudaErrorInvalidValue;
   Args a = make_args(g);
   a.w = w;
