@@ -844,16 +844,10 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(phi_full);
-        // chunk total of phi_k: warp butterfly, per-quarter partials
-#pragma unroll
-        for (int f = 0; f < FP; ++f) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) phk[f] += __shfl_xor_sync(0xffffffffu, phk[f], o);
-        }
-        if (lane_id() == 0) {
-#pragma unroll
-          for (int f = 0; f < FP; ++f) xpar[512 + qw * FP + f] = phk[f];
-        }
+        // chunk total of phi_k: per-quarter partials by a recursive-halving warp reduction
+        static_assert(FP == 8, "warp_sum8 reduces 8 values");
+        const float tot = warp_sum8(phk);
+        if ((lane_id() & 3) == 0) xpar[512 + qw * FP + (lane_id() >> 2)] = tot;
       }
       float D = 0.f;
       if (h == 0) {

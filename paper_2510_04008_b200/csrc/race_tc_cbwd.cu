@@ -919,15 +919,8 @@ __global__ void __launch_bounds__(NTHREADS8, 1)
             dac[f] = phq[f] * gdr_c;
           }
           write_phi_k(sb + OFF_PHIT, r, pht);
-#pragma unroll
-          for (int f = 0; f < FP; ++f) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dac[f] += __shfl_xor_sync(0xffffffffu, dac[f], o);
-          }
-          if (lane_id() == 0) {
-#pragma unroll
-            for (int f = 0; f < FP; ++f) xpar[256 + qw * FP + f] = dac[f];
-          }
+          const float tot = warp_sum8(dac);  // recursive-halving warp reduction (FP == 8)
+          if ((lane_id() & 3) == 0) xpar[256 + qw * FP + (lane_id() >> 2)] = tot;
         }
       }
       if (threadIdx.x == a.ttid) RACE_TRACE(a, 24, gc);

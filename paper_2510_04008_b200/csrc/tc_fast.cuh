@@ -179,6 +179,28 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int crow() { return ((warp_id() & 3) << 5) | lane_id(); }       // compute row
 __device__ __forceinline__ uint32_t lane_base() { return uint32_t((warp_id() & 3) * 32) << 16; }
 __device__ __forceinline__ void compute_bar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// warp totals of 8 per-lane values by recursive halving (9 shuffles instead of 8 x 5): returns the total of
+// value f = 4 b4 + 2 b3 + b2 (bits of the lane id) in every lane whose low two bits are 0 (and the
+// same total in the other three lanes of its group of four); fixed order, so deterministic
+__device__ __forceinline__ float warp_sum8(const float* v) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float w[4], x[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float send = b4 ? v[k] : v[4 + k], keep = b4 ? v[4 + k] : v[k];
+    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float send = b3 ? w[k] : w[2 + k], keep = b3 ? w[2 + k] : w[k];
+    x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float y = (b2 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
 __device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
