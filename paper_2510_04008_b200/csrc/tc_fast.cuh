@@ -504,22 +504,6 @@ __device__ __forceinline__ void write_sop(uint32_t buf, int c, const float* s) {
   write_row32(buf, c, b);
 }
 
-// block-wide sum of 8 values over the 128 compute threads, fixed order
-__device__ __forceinline__ void csum8(float* v, float* scratch) {
-#pragma unroll
-  for (int f = 0; f < FP; ++f) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
-  }
-  if (lane_id() == 0) {
-#pragma unroll
-    for (int f = 0; f < FP; ++f) scratch[(warp_id() & 3) * FP + f] = v[f];
-  }
-  compute_bar();
-#pragma unroll
-  for (int f = 0; f < FP; ++f) v[f] = ((scratch[f] + scratch[FP + f]) + scratch[2 * FP + f]) + scratch[3 * FP + f];
-  compute_bar();
-}
 
 // write one [128 x 128] fp32 row (from TMEM) as bf16 into a SW128 staging tile
 __device__ __forceinline__ void stage_row_bf16(uint32_t tile, int r, const float* v, int c0) {
@@ -790,22 +774,6 @@ __device__ __forceinline__ void copy_half_row(uint32_t dst, uint32_t src, int r,
   }
 }
 
-// sum of 8 values over the 128 threads of half h (4 warps), fixed order; all get the total
-__device__ __forceinline__ void hsum8(float* v, float* scratch, int h) {
-#pragma unroll
-  for (int f = 0; f < FP; ++f) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
-  }
-  float* sc = scratch + h * 4 * FP;
-  if (lane_id() == 0) {
-#pragma unroll
-    for (int f = 0; f < FP; ++f) sc[(warp_id() & 3) * FP + f] = v[f];
-  }
-  hbar128(h);
-#pragma unroll
-  for (int f = 0; f < FP; ++f) v[f] = ((sc[f] + sc[FP + f]) + sc[2 * FP + f]) + sc[3 * FP + f];
-}
 
 // one-pass tangent VJP for columns [64h, 64h + 64) of row r; bf16 result straight to global
 __device__ __forceinline__ void tangent_half_to_global(uint32_t tmem_col, uint32_t tile, int r, int h, Scale sc,
